@@ -1,0 +1,209 @@
+/* ltfb_gpu.h — C ABI of the B200-native LTFB hot path (libltfb_gpu.so).
+ *
+ * The reference (/root/reference/proj, header-only C++20) has no plugin or
+ * FFI layer: its "interface" is the C++ API of train::Trainer,
+ * tournament::tournament_round and the surrogate::* step functions. This
+ * header is the flat C boundary under that API: plain pointers and sizes,
+ * opaque handles, int status codes; no C++ or torch types. The C++ drop-in
+ * façade (include/ltfb_b200/*.hpp) and the Python package both sit on it.
+ *
+ * Each entry point names the reference interface it replaces
+ * (file:line under /root/reference/proj/include/ltfb).
+ *
+ * Errors: every function returns LTFB_OK or one LTFB_E* code mapping 1:1
+ * onto the reference exception taxonomy (core/error.hpp:11-58);
+ * ltfb_last_error() returns the message (thread-local). LTFB_ENUMERIC keeps
+ * the reference meaning: the offending update was not applied.
+ *
+ * Networks are indexed LTFB_NET_ENC..LTFB_NET_DISC; a network crosses the
+ * ABI as one float32 blob in the reference manifest order
+ * (nn/mlp.hpp:63-84: W0, b0, W1, b1, ... with row-major [in x out] W).
+ */
+#ifndef LTFB_GPU_H
+#define LTFB_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTFB_ABI_VERSION 1
+
+enum {
+  LTFB_OK = 0,
+  LTFB_EDIMENSION = 1,    /* DimensionError */
+  LTFB_ECONTRACT = 2,     /* ContractError */
+  LTFB_ENUMERIC = 3,      /* NumericError */
+  LTFB_EIO = 4,           /* IoError */
+  LTFB_ECAPACITY = 5,     /* CapacityError */
+  LTFB_ESTORECORRUPT = 6, /* StoreCorruptError */
+  LTFB_ECONFIG = 7,       /* ConfigError */
+  LTFB_ECUDA = 8,         /* device / driver failure (no reference analogue) */
+  LTFB_EINTERNAL = 9
+};
+
+enum { LTFB_NET_ENC = 0, LTFB_NET_DEC = 1, LTFB_NET_FWD = 2, LTFB_NET_INV = 3, LTFB_NET_DISC = 4 };
+enum { LTFB_ACT_IDENTITY = 0, LTFB_ACT_RELU = 1, LTFB_ACT_LEAKY_RELU = 2, LTFB_ACT_TANH = 3,
+       LTFB_ACT_SIGMOID = 4 };
+enum { LTFB_SLICE_TOURNAMENT = 0, LTFB_SLICE_VALIDATION = 1 };
+
+/* surrogate/dims.hpp:15-53 */
+typedef struct {
+  uint32_t input_dim, latent_dim, scalar_dim, image_views, image_channels, image_h, image_w;
+} ltfb_dims;
+
+/* surrogate/model.hpp:18-30 (hidden widths per network, <= 8 each) */
+typedef struct {
+  uint32_t enc_hidden[8], dec_hidden[8], fwd_hidden[8], inv_hidden[8], disc_hidden[8];
+  uint32_t n_enc_hidden, n_dec_hidden, n_fwd_hidden, n_inv_hidden, n_disc_hidden;
+  int32_t hidden_act; /* LTFB_ACT_* */
+  double hidden_slope;
+  double lambda_adv, lambda_cyc;
+  double lr, beta1, beta2, eps; /* nn/adam.hpp:15-22 */
+} ltfb_arch;
+
+/* train/trainer.hpp:26-39 (+ device placement) */
+typedef struct {
+  int32_t trainer_id;
+  int32_t device;        /* CUDA ordinal */
+  int32_t n_shards;
+  int32_t numeric_abort_threshold;
+  uint64_t batch_size;
+  uint64_t seed;         /* epoch-plan seed */
+  double w_f, w_i;
+  double lr_fwd, lr_inv, lr_disc; /* 0 = arch.lr (runner.hpp:286-293 lr_jitter) */
+  int32_t wide_kernel;   /* 0 auto, 1 generic SIMT, 2 tcgen05 (error if unsupported) */
+  int32_t reserved;
+} ltfb_trainer_config;
+
+/* train/history.hpp:20-30 */
+typedef struct {
+  uint64_t step;
+  uint32_t epoch;
+  uint32_t skipped;
+  double d_loss, g_total, g_fwd, g_adv, g_cyc;
+} ltfb_step_record;
+
+/* train/history.hpp:38-46 */
+typedef struct {
+  uint32_t epoch;
+  uint32_t partial;
+  uint64_t steps, samples_shuffled;
+  double seconds;
+} ltfb_epoch_record;
+
+/* surrogate/train_ops.hpp:20-24 */
+typedef struct {
+  double forward_mae, inverse_mae, combined;
+} ltfb_eval_metric;
+
+typedef struct ltfb_trainer ltfb_trainer;
+typedef struct ltfb_comm ltfb_comm;
+
+const char* ltfb_last_error(void);
+int ltfb_abi_version(void);
+int ltfb_device_count(int* count);
+
+/* Fills *arch with SurrogateArch{} defaults (model.hpp:18-30). */
+void ltfb_arch_defaults(ltfb_arch* arch);
+
+/* ---- trainer lifecycle: replaces train::Trainer(TrainerConfig,
+ *      DatasetIndex, CycleGan<float>) (trainer.hpp:43-79) ---------------- */
+int ltfb_trainer_create(const ltfb_dims* dims, const ltfb_arch* arch,
+                        const ltfb_trainer_config* cfg, ltfb_trainer** out);
+int ltfb_trainer_destroy(ltfb_trainer* t);
+int ltfb_trainer_param_count(const ltfb_trainer* t, int net, uint64_t* count);
+
+/* CycleGan blobs (model.hpp:36-73) <-> HBM. */
+int ltfb_trainer_set_params(ltfb_trainer* t, int net, const float* blob, uint64_t count);
+int ltfb_trainer_get_params(ltfb_trainer* t, int net, float* blob, uint64_t count);
+/* AdamState (adam.hpp:25-47); m/v may be NULL (left unchanged / not read). */
+int ltfb_trainer_set_adam(ltfb_trainer* t, int net, const float* m, const float* v, uint64_t step);
+int ltfb_trainer_get_adam(ltfb_trainer* t, int net, float* m, float* v, uint64_t* step);
+
+/* DataStore::preload (store.hpp:100-135) into HBM: slot i holds sample
+ * ids[i]; x is [n x input_dim], y is [n x output_dim], row-major f32.
+ * owner (optional, may be NULL) is the owning shard per slot. */
+int ltfb_trainer_load_store(ltfb_trainer* t, const uint32_t* ids, uint64_t n, const float* x,
+                            const float* y, const int32_t* owner);
+/* assemble_tensors of the tournament / validation slice (trainer.hpp:74-78,
+ * runner.hpp:318) made resident in HBM. */
+int ltfb_trainer_set_slice(ltfb_trainer* t, int which, const float* x, const float* y, uint64_t rows);
+
+/* Trainer::train_steps (trainer.hpp:102-104, 190-290). Writes one record
+ * per executed step to out (capacity n) and the count to *n_out. Returns
+ * LTFB_ENUMERIC when the skip threshold was exceeded (trainer.hpp:283-289);
+ * the records up to and including the aborting step are still written. */
+int ltfb_trainer_train_steps(ltfb_trainer* t, uint64_t n, ltfb_step_record* out, uint64_t* n_out);
+int ltfb_trainer_step(const ltfb_trainer* t, uint64_t* step);
+/* Closed epoch records (epochs >= 1) since the last call; *n_out <= cap. */
+int ltfb_trainer_take_epochs(ltfb_trainer* t, ltfb_epoch_record* out, uint64_t cap, uint64_t* n_out);
+/* Trainer::flush_epoch_record (trainer.hpp:129-134). */
+int ltfb_trainer_flush_epoch(ltfb_trainer* t);
+
+/* surrogate::evaluate (train_ops.hpp:191-205) on a resident slice. NULL
+ * candidate blobs mean the trainer's own fwd/inv (eval_tournament(model()),
+ * trainer.hpp:106-112). */
+int ltfb_trainer_evaluate(ltfb_trainer* t, int which, const float* cand_fwd, const float* cand_inv,
+                          double w_f, double w_i, ltfb_eval_metric* out);
+
+/* ---- tournament (tournament/ltfb.hpp:96-164) --------------------------- */
+/* Size in floats of the generator payload fwd||inv (15,204 B default). */
+int ltfb_trainer_generator_floats(const ltfb_trainer* t, uint64_t* n);
+/* Own fwd||inv blob to host (TransferRecord hashes, ltfb.hpp:118-131). */
+int ltfb_trainer_get_generator(ltfb_trainer* t, float* dst, uint64_t n);
+/* Incoming candidate from host memory. */
+int ltfb_trainer_set_incoming(ltfb_trainer* t, const float* fwd, const float* inv);
+/* Incoming candidate = another in-process trainer's current generator
+ * (device-to-device / peer copy; the payload capture of ltfb.hpp:118-131). */
+int ltfb_trainer_copy_incoming(ltfb_trainer* dst, ltfb_trainer* src);
+/* Evaluate local vs incoming on the tournament slice in one pass, decide
+ * with incoming_wins (ltfb.hpp:82-88) IN A DEVICE KERNEL and, if the
+ * incoming generator wins, adopt it on the device: copy fwd/inv, zero their
+ * Adam moments, keep t (trainer.hpp:117-127). */
+int ltfb_trainer_tournament_decide(ltfb_trainer* t, ltfb_eval_metric* local,
+                                   ltfb_eval_metric* incoming, int32_t* adopted);
+/* Trainer::adopt_generators from host blobs. */
+int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv);
+
+/* ---- multi-GPU: one trainer per GPU, NCCL point-to-point exchange ------- */
+int ltfb_nccl_available(void);
+int ltfb_nccl_unique_id(uint8_t id[128]);
+int ltfb_comm_create(const uint8_t id[128], int nranks, int rank, int device, ltfb_comm** out);
+int ltfb_comm_destroy(ltfb_comm* c);
+/* Pairwise generator swap with `peer`: ncclSend(own fwd||inv) +
+ * ncclRecv(peer's into the incoming buffer) in one group on the trainer's
+ * stream (replaces the in-process value copy of ltfb.hpp:118-131). */
+int ltfb_trainer_exchange(ltfb_trainer* t, ltfb_comm* c, int peer);
+/* Broadcast a network blob from `root` (AE broadcast, runner.hpp:285). */
+int ltfb_trainer_broadcast(ltfb_trainer* t, ltfb_comm* c, int net, int root);
+
+/* ---- host algorithms of the path (bit-exact, product implementations) -- */
+uint64_t ltfb_mix_seed(const uint64_t* words, int n);                        /* rng.hpp:23-30 */
+uint64_t ltfb_fnv1a64(const void* bytes, uint64_t n);                        /* hash.hpp:15-22 */
+int ltfb_pair_trainers(int k, int round, uint64_t seed, int32_t* pairs, int32_t* bye,
+                       int32_t* n_pairs);                                     /* ltfb.hpp:52-66 */
+int ltfb_partition_dataset(const uint32_t* ids, uint64_t n, int k, uint64_t seed,
+                           uint32_t* out_ids, uint32_t* sizes);               /* ltfb.hpp:24-43 */
+int ltfb_split_dataset(uint64_t total, int k, double validation_fraction,
+                       double tournament_fraction, uint64_t seed, int need_tournament,
+                       uint32_t* val, uint64_t* n_val, uint32_t* train, uint32_t* train_sizes,
+                       uint32_t* tour, uint32_t* tour_sizes);                 /* runner.hpp:134-169 */
+int ltfb_epoch_permutation(const uint32_t* partition, uint64_t n, uint32_t epoch, uint64_t seed,
+                           uint32_t* out);                                    /* epoch_plan.hpp:59-89 */
+int ltfb_incoming_wins(double local, double incoming);                       /* ltfb.hpp:82-88 */
+/* generate_dataset rows [first, first+n) of a total_n sweep (generator.hpp:195-206) */
+int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                        uint64_t first, uint64_t n, uint64_t total_n, uint64_t sampling_seed,
+                        float* x, float* y, int threads);
+/* make_cyclegan blob init (model.hpp:96-132, mlp.hpp:235-244) */
+int ltfb_init_params(const ltfb_dims* dims, const ltfb_arch* arch, uint64_t seed, int net,
+                     float* blob, uint64_t count);
+int ltfb_net_param_count(const ltfb_dims* dims, const ltfb_arch* arch, int net, uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LTFB_GPU_H */

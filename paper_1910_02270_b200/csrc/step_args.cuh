@@ -1,0 +1,81 @@
+// Kernel argument blocks. Passed by value (one constant-bank copy per launch),
+// they carry every device pointer a kernel touches so a captured CUDA graph
+// of one training step can be replayed without re-binding.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace ltfb_dev {
+
+struct ModelArgs {
+  int in, lat, out, out_pad;  // input_dim, latent_dim, output_dim, padded row
+  int E1;                     // enc wide-layer width (enc layer 0: out -> E1)
+  int D;                      // dec wide-layer input width (dec last: D -> out)
+  int enc_act0;               // activation of enc layer 0
+  float enc_slope0;
+  long long enc_wide_w, enc_wide_b;  // offsets inside the enc blob
+  long long dec_wide_w, dec_wide_b;  // offsets inside the dec blob
+  NetDesc enc_tail;  // enc layers 1.. (E1 -> ... -> lat); L may be 0
+  NetDesc dec_head;  // dec layers 0..L-2 (lat -> ... -> D); L may be 0
+  NetDesc fwd, inv, disc;
+  float lambda_adv, lambda_cyc;
+};
+
+struct StepArgs {
+  ModelArgs m;
+  int B;            // configured batch size
+  int n_part;       // partition size (slots in the store)
+  int S;            // split count of the wide pass (partials)
+  int abort_threshold;
+  int rec_cap;
+  int small_ctas;   // CTAs of the small-network kernels
+  double lr[5], b1, b2, eps;
+  long long adam_cap;  // entries of the bias-correction table
+  // parameters / optimizer state (blob layout), gradient scratch
+  float* p[5];
+  float* mom1[5];
+  float* mom2[5];
+  float* g[5];
+  // HBM-resident data store and the epoch plan (two buffers, epoch parity)
+  const float* sx;
+  const float* sy;
+  const unsigned* perm[2];
+  // minibatch and wide-pass intermediates
+  float* xb;
+  float* yb;
+  float* h;         // [B x D] dec-head output, input of the wide pass
+  float* P_enc;     // [S x B x E1]
+  float* P_dec;     // [S x B x D]
+  double* mae_part; // [S]
+  float* scratch;   // small-network tapes
+  Counters* ctr;
+  StepRec* rec;
+  const double* adam_c;  // [cap x 2]: 1-b1^t, 1-b2^t (host std::pow)
+};
+
+/// Candidate evaluation (train_ops.hpp:191-205) over a resident slice.
+struct EvalArgs {
+  ModelArgs m;
+  int rows;         // slice rows
+  int nc;           // candidates (1 or 2)
+  int S;
+  const float* x;   // [rows x in]
+  const float* y;   // [rows x out_pad]
+  const float* enc; // frozen enc/dec blobs
+  const float* dec;
+  const float* cf[2];  // candidate fwd blobs
+  const float* ci[2];  // candidate inv blobs
+  float* h;            // [nc x rows x D]
+  double* inv_row;     // [nc x rows]
+  double* part;        // [S x nc]
+  double* out;         // [nc x 3]
+  double w_f, w_i;
+  // decision + adoption (tournament/ltfb.hpp:135-147, trainer.hpp:117-127)
+  int decide;
+  float* dst_fwd; float* dst_inv;
+  float* m_fwd; float* v_fwd; float* m_inv; float* v_inv;
+  long long n_fwd, n_inv;
+  Counters* ctr;
+};
+
+}  // namespace ltfb_dev

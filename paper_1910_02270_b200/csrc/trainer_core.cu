@@ -1,0 +1,579 @@
+// DeviceTrainer implementation (see trainer_core.hpp).
+#include "trainer_core.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "kernels.hpp"
+#include "ltfb_b200/host_algos.hpp"
+#include "scratch_layout.cuh"
+
+namespace ltfb_b200 {
+
+using ltfb::ContractError;
+using ltfb::DimensionError;
+using ltfb::Error;
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                ") at " + what);
+  }
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev);
+  if (prev != dev) LTFB_CUDA(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+}
+
+namespace {
+
+int act_code(const ltfb::nn::Activation& a) {
+  switch (a.kind) {
+    case ltfb::nn::Act::kIdentity: return ltfb_dev::kIdentity;
+    case ltfb::nn::Act::kRelu: return ltfb_dev::kRelu;
+    case ltfb::nn::Act::kLeakyRelu: return ltfb_dev::kLeaky;
+    case ltfb::nn::Act::kTanh: return ltfb_dev::kTanh;
+    case ltfb::nn::Act::kSigmoid: return ltfb_dev::kSigmoid;
+  }
+  return ltfb_dev::kIdentity;
+}
+
+/// Describes layers [first, last) of `spec` as a small-network descriptor
+/// whose offsets index the full blob.
+ltfb_dev::NetDesc describe(const ltfb::nn::MlpSpec& spec, std::size_t first, std::size_t last) {
+  ltfb_dev::NetDesc d{};
+  const auto man = ltfb::nn::manifest_for(spec);
+  d.L = static_cast<int>(last - first);
+  if (d.L > ltfb_dev::kMaxLayers) throw DimensionError("network has more than 8 small layers");
+  for (std::size_t l = first; l < last; ++l) {
+    const int i = static_cast<int>(l - first);
+    d.w[i] = static_cast<int>(spec.layer_widths[l]);
+    d.w[i + 1] = static_cast<int>(spec.layer_widths[l + 1]);
+    d.act[i] = act_code(spec.activations[l]);
+    d.slope[i] = static_cast<float>(spec.activations[l].slope);
+    d.off_w[i] = static_cast<long long>(man.entries[2 * l].offset);
+    d.off_b[i] = static_cast<long long>(man.entries[2 * l + 1].offset);
+  }
+  for (int i = 0; i <= d.L; ++i)
+    if (d.L > 0 && d.w[i] > ltfb_dev::kMaxSmallWidth)
+      throw DimensionError("small-network width " + std::to_string(d.w[i]) + " exceeds 256");
+  if (d.L > 0) {
+    d.base = d.off_w[0];
+    d.count = static_cast<long long>(man.total) - d.base;
+    if (last < spec.n_layers()) d.count = static_cast<long long>(man.entries[2 * last].offset) - d.base;
+  }
+  return d;
+}
+
+}  // namespace
+
+DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
+  if (spec_.n_shards < 1) throw ContractError("Trainer: n_shards must be >= 1");
+  if (spec_.batch_size < 1) throw ContractError("Trainer: batch_size must be >= 1");
+  spec_.dims.validate();
+  DeviceGuard g(spec_.device);
+  cudaDeviceProp prop{};
+  LTFB_CUDA(cudaGetDeviceProperties(&prop, spec_.device));
+  sm_count_ = prop.multiProcessorCount;
+  LTFB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+  // network specs exactly as make_cyclegan builds them (model.hpp:96-132)
+  const auto m = ltfb::surrogate::make_cyclegan<float>(spec_.dims, spec_.arch, 0);
+  specs_[0] = m.enc_spec;
+  specs_[1] = m.dec_spec;
+  specs_[2] = m.fwd_spec;
+  specs_[3] = m.inv_spec;
+  specs_[4] = m.disc_spec;
+  for (int i = 0; i < 5; ++i) counts_[i] = ltfb::nn::manifest_for(specs_[i]).total;
+  if (spec_.batch_size > 4096) throw ContractError("Trainer: batch_size above 4096 is not supported on the B200 path");
+  build_model_args();
+
+  for (int i = 0; i < 5; ++i) {
+    if (i == 2 || i == 3) continue;
+    params_[i].alloc(counts_[i]);
+  }
+  gen_.alloc(counts_[2] + counts_[3]);
+  incoming_.alloc(counts_[2] + counts_[3]);
+  for (int i = 0; i < 5; ++i) {
+    mom1_[i].alloc(counts_[i]);
+    mom2_[i].alloc(counts_[i]);
+    grads_[i].alloc(counts_[i]);
+    LTFB_CUDA(cudaMemsetAsync(mom1_[i].p, 0, mom1_[i].bytes(), stream_));
+    LTFB_CUDA(cudaMemsetAsync(mom2_[i].p, 0, mom2_[i].bytes(), stream_));
+  }
+  const int B = static_cast<int>(spec_.batch_size);
+  const auto& ma = margs_;
+  S_ = std::min<std::size_t>((ma.out + 31) / 32, static_cast<std::size_t>(sm_count_) * 2);
+  xb_.alloc(static_cast<std::size_t>(B) * ma.in);
+  yb_.alloc(static_cast<std::size_t>(B) * ma.out_pad);
+  pe_.alloc(S_ * B * ma.E1);
+  pd_.alloc(S_ * B * ma.D);
+  mae_part_.alloc(S_);
+  const auto lay = ltfb_dev::make_scratch_layout(ma, B);
+  scratch_.alloc(static_cast<std::size_t>(lay.total));
+  ctr_.alloc(1);
+  LTFB_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(ltfb_dev::Counters), stream_));
+  rec_.alloc(4096);
+  for (int i = 0; i < 2; ++i) {
+    LTFB_CUDA(cudaEventCreateWithFlags(&perm_ev_[i], cudaEventDisableTiming));
+  }
+
+  auto& a = args_;
+  a.m = margs_;
+  a.B = B;
+  a.S = static_cast<int>(S_);
+  a.abort_threshold = spec_.numeric_abort_threshold;
+  a.rec_cap = static_cast<int>(rec_.n);
+  a.small_ctas = std::max(1, (B + 15) / 16);
+  const auto& h = spec_.arch.adam;
+  for (int i = 0; i < 5; ++i) a.lr[i] = spec_.lr[i] > 0 ? spec_.lr[i] : h.lr;
+  a.b1 = h.beta1;
+  a.b2 = h.beta2;
+  a.eps = h.eps;
+  for (int i = 0; i < 5; ++i) {
+    a.p[i] = i == 2 ? gen_.p : (i == 3 ? gen_.p + counts_[2] : params_[i].p);
+    a.mom1[i] = mom1_[i].p;
+    a.mom2[i] = mom2_[i].p;
+    a.g[i] = grads_[i].p;
+  }
+  a.xb = xb_.p;
+  a.yb = yb_.p;
+  a.P_enc = pe_.p;
+  a.P_dec = pd_.p;
+  a.mae_part = mae_part_.p;
+  a.scratch = scratch_.p;
+  a.h = scratch_.p + (margs_.dec_head.L > 0 ? lay.ha[margs_.dec_head.L - 1] : lay.fa[margs_.fwd.L - 1]);
+  a.ctr = ctr_.p;
+  a.rec = rec_.p;
+  ensure_adam_table(1024);
+
+  wide_kind_ = 1;
+  if (spec_.wide_kernel != 1 && ltfb_dev::wide_tc_supported(a)) wide_kind_ = 2;
+  if (spec_.wide_kernel == 2 && wide_kind_ != 2)
+    throw ContractError("tcgen05 wide kernel requested but unsupported for this shape");
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+DeviceTrainer::~DeviceTrainer() {
+  DeviceGuard g(spec_.device);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (int i = 0; i < 2; ++i) {
+    if (pinned_perm_[i]) cudaFreeHost(pinned_perm_[i]);
+    if (perm_ev_[i]) cudaEventDestroy(perm_ev_[i]);
+  }
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void DeviceTrainer::build_model_args() {
+  auto& m = margs_;
+  m.in = static_cast<int>(spec_.dims.input_dim);
+  m.lat = static_cast<int>(spec_.dims.latent_dim);
+  m.out = static_cast<int>(spec_.dims.output_dim());
+  m.out_pad = (m.out + 3) / 4 * 4;
+  const auto& enc = specs_[0];
+  const auto& dec = specs_[1];
+  const auto em = ltfb::nn::manifest_for(enc);
+  const auto dm = ltfb::nn::manifest_for(dec);
+  m.E1 = static_cast<int>(enc.layer_widths[1]);
+  m.enc_act0 = act_code(enc.activations[0]);
+  m.enc_slope0 = static_cast<float>(enc.activations[0].slope);
+  m.enc_wide_w = static_cast<long long>(em.entries[0].offset);
+  m.enc_wide_b = static_cast<long long>(em.entries[1].offset);
+  m.enc_tail = describe(enc, 1, enc.n_layers());
+  const std::size_t dl = dec.n_layers() - 1;
+  m.D = static_cast<int>(dec.layer_widths[dl]);
+  m.dec_wide_w = static_cast<long long>(dm.entries[2 * dl].offset);
+  m.dec_wide_b = static_cast<long long>(dm.entries[2 * dl + 1].offset);
+  m.dec_head = describe(dec, 0, dl);
+  m.fwd = describe(specs_[2], 0, specs_[2].n_layers());
+  m.inv = describe(specs_[3], 0, specs_[3].n_layers());
+  m.disc = describe(specs_[4], 0, specs_[4].n_layers());
+  if (m.E1 > ltfb_dev::kMaxSmallWidth || m.D > ltfb_dev::kMaxSmallWidth)
+    throw DimensionError("wide-layer inner width above 256 is not supported on the B200 path");
+  m.lambda_adv = static_cast<float>(spec_.arch.lambda_adv);
+  m.lambda_cyc = static_cast<float>(spec_.arch.lambda_cyc);
+}
+
+void DeviceTrainer::ensure_adam_table(std::uint64_t t_max) {
+  if (t_max + 1 <= adam_cap_) return;
+  std::uint64_t cap = std::max<std::uint64_t>(1024, adam_cap_ * 2);
+  while (cap < t_max + 1) cap *= 2;
+  // nn/adam.hpp:113-116: 1 - std::pow(beta, t) in double on the host
+  std::vector<double> tab(2 * cap);
+  const auto& h = spec_.arch.adam;
+  for (std::uint64_t t = 0; t < cap; ++t) {
+    tab[2 * t] = 1.0 - std::pow(h.beta1, static_cast<double>(t));
+    tab[2 * t + 1] = 1.0 - std::pow(h.beta2, static_cast<double>(t));
+  }
+  DevBuf<double> nb;
+  nb.alloc(tab.size());
+  LTFB_CUDA(cudaMemcpyAsync(nb.p, tab.data(), nb.bytes(), cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  std::swap(adam_c_.p, nb.p);
+  std::swap(adam_c_.n, nb.n);
+  adam_cap_ = cap;
+  args_.adam_c = adam_c_.p;
+  args_.adam_cap = static_cast<long long>(cap);
+}
+
+// ------------------------------------------------------------ parameters --
+static float* net_ptr(DeviceTrainer& t, DevBuf<float>* params, DevBuf<float>& gen, int net,
+                      std::size_t c2) {
+  (void)t;
+  if (net == 2) return gen.p;
+  if (net == 3) return gen.p + c2;
+  return params[net].p;
+}
+
+void DeviceTrainer::set_params(int net, const float* blob, std::size_t count) {
+  if (net < 0 || net > 4) throw ContractError("set_params: bad network index");
+  if (count != counts_[net])
+    throw ContractError("blob length " + std::to_string(count) + " does not match manifest total " +
+                        std::to_string(counts_[net]));
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaMemcpyAsync(net_ptr(*this, params_, gen_, net, counts_[2]), blob, count * 4,
+                            cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DeviceTrainer::get_params(int net, float* blob, std::size_t count) {
+  if (net < 0 || net > 4) throw ContractError("get_params: bad network index");
+  if (count != counts_[net]) throw ContractError("get_params: wrong blob length");
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaMemcpyAsync(blob, net_ptr(*this, params_, gen_, net, counts_[2]), count * 4,
+                            cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DeviceTrainer::set_adam(int net, const float* m, const float* v, std::uint64_t t) {
+  if (net < 0 || net > 4) throw ContractError("set_adam: bad network index");
+  DeviceGuard g(spec_.device);
+  const std::size_t n = counts_[net];
+  if (m) LTFB_CUDA(cudaMemcpyAsync(mom1_[net].p, m, n * 4, cudaMemcpyHostToDevice, stream_));
+  if (v) LTFB_CUDA(cudaMemcpyAsync(mom2_[net].p, v, n * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaMemcpyAsync(&ctr_.p->t[net], &t, 8, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  t_host_max_ = std::max(t_host_max_, t);
+}
+
+void DeviceTrainer::get_adam(int net, float* m, float* v, std::uint64_t* t) {
+  if (net < 0 || net > 4) throw ContractError("get_adam: bad network index");
+  DeviceGuard g(spec_.device);
+  const std::size_t n = counts_[net];
+  if (m) LTFB_CUDA(cudaMemcpyAsync(m, mom1_[net].p, n * 4, cudaMemcpyDeviceToHost, stream_));
+  if (v) LTFB_CUDA(cudaMemcpyAsync(v, mom2_[net].p, n * 4, cudaMemcpyDeviceToHost, stream_));
+  std::uint64_t tt = 0;
+  LTFB_CUDA(cudaMemcpyAsync(&tt, &ctr_.p->t[net], 8, cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  if (t) *t = tt;
+}
+
+// ------------------------------------------------------------------ data --
+void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const float* x,
+                               const float* y, const std::int32_t* owner) {
+  if (n == 0) throw ContractError("plan_epoch: empty partition");
+  DeviceGuard g(spec_.device);
+  const auto& m = margs_;
+  part_ids_.assign(ids, ids + n);
+  owner_.assign(n, 0);
+  if (owner) owner_.assign(owner, owner + n);
+  n_part_ = n;
+  sx_.alloc(n * m.in);
+  sy_.alloc(n * m.out_pad);
+  LTFB_CUDA(cudaMemcpyAsync(sx_.p, x, n * m.in * 4, cudaMemcpyHostToDevice, stream_));
+  if (m.out_pad == m.out) {
+    LTFB_CUDA(cudaMemcpyAsync(sy_.p, y, n * m.out * 4, cudaMemcpyHostToDevice, stream_));
+  } else {
+    LTFB_CUDA(cudaMemsetAsync(sy_.p, 0, sy_.bytes(), stream_));
+    LTFB_CUDA(cudaMemcpy2DAsync(sy_.p, m.out_pad * 4, y, m.out * 4, m.out * 4, n,
+                                cudaMemcpyHostToDevice, stream_));
+  }
+  for (int i = 0; i < 2; ++i) {
+    perm_[i].alloc(n);
+    if (pinned_perm_[i]) cudaFreeHost(pinned_perm_[i]);
+    LTFB_CUDA(cudaMallocHost(&pinned_perm_[i], n * sizeof(unsigned)));
+    perm_slots_[i].resize(n);
+  }
+  auto& a = args_;
+  a.sx = sx_.p;
+  a.sy = sy_.p;
+  a.perm[0] = perm_[0].p;
+  a.perm[1] = perm_[1].p;
+  a.n_part = static_cast<int>(n);
+  steps_per_epoch_ = (n + spec_.batch_size - 1) / spec_.batch_size;
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void DeviceTrainer::generate_store(const std::uint32_t*, std::size_t, std::uint64_t, std::uint64_t,
+                                   std::uint64_t) {
+  throw ContractError("generate_store: device generator not available in this build");
+}
+
+void DeviceTrainer::set_slice(int which, const float* x, const float* y, std::size_t rows) {
+  DeviceGuard g(spec_.device);
+  const auto& m = margs_;
+  DevBuf<float>& bx = which == 0 ? tx_ : vx_;
+  DevBuf<float>& by = which == 0 ? ty_ : vy_;
+  bx.alloc(rows * m.in);
+  by.alloc(rows * m.out_pad);
+  if (rows) {
+    LTFB_CUDA(cudaMemcpyAsync(bx.p, x, rows * m.in * 4, cudaMemcpyHostToDevice, stream_));
+    LTFB_CUDA(cudaMemsetAsync(by.p, 0, by.bytes(), stream_));
+    LTFB_CUDA(cudaMemcpy2DAsync(by.p, m.out_pad * 4, y, m.out * 4, m.out * 4, rows,
+                                cudaMemcpyHostToDevice, stream_));
+  }
+  (which == 0 ? tour_rows_ : val_rows_) = rows;
+  const std::size_t mx = std::max(tour_rows_, val_rows_);
+  if (eval_h_.n < 2 * mx * m.D) {
+    eval_h_.alloc(2 * mx * m.D);
+    eval_inv_.alloc(2 * mx);
+  }
+  eval_S_ = static_cast<std::size_t>(sm_count_) * 2;
+  if (eval_part_.n < eval_S_ * 2) eval_part_.alloc(eval_S_ * 2);
+  if (!eval_out_.p) eval_out_.alloc(6);
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// -------------------------------------------------------------- training --
+cudaEvent_t DeviceTrainer::next_event() {
+  if (ev_used_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    LTFB_CUDA(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_used_++];
+}
+
+void DeviceTrainer::close_epoch_segment(bool epoch_done, bool partial) {
+  if (seg_open_) {
+    cudaEvent_t e = next_event();
+    LTFB_CUDA(cudaEventRecord(e, stream_));
+    open_segments_.push_back({seg_start_, e});
+    seg_open_ = false;
+  }
+  if (epoch_done) {
+    // resolve timings of this epoch's segments (all recorded on stream_)
+    LTFB_CUDA(cudaStreamSynchronize(stream_));
+    for (const auto& s : open_segments_) {
+      float ms = 0;
+      LTFB_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
+      epoch_seconds_ += ms * 1e-3;
+    }
+    open_segments_.clear();
+    ev_used_ = 0;
+    closed_.push_back({epoch_, epoch_steps_, epoch_shuffled_, epoch_seconds_, partial});
+    epoch_steps_ = epoch_shuffled_ = 0;
+    epoch_seconds_ = 0;
+  }
+}
+
+void DeviceTrainer::start_epoch() {
+  if (have_plan_) close_epoch_segment(true, false);
+  epoch_ += 1;
+  const int buf = static_cast<int>(epoch_ & 1);
+  // epoch_plan.hpp:69-71: shuffle(partition) == partition[shuffle(iota)],
+  // because the Fisher-Yates swaps depend only on the length.
+  auto& slots = perm_slots_[buf];
+  for (std::size_t i = 0; i < n_part_; ++i) slots[i] = static_cast<std::uint32_t>(i);
+  ltfb::Rng(ltfb::mix_seed({spec_.seed, epoch_, 0x5caff1eULL})).shuffle(slots);
+  LTFB_CUDA(cudaEventSynchronize(perm_ev_[buf]));  // previous use of this pinned buffer
+  std::memcpy(pinned_perm_[buf], slots.data(), n_part_ * sizeof(unsigned));
+  LTFB_CUDA(cudaMemcpyAsync(perm_[buf].p, pinned_perm_[buf], n_part_ * sizeof(unsigned),
+                            cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaEventRecord(perm_ev_[buf], stream_));
+  ltfb_dev::launch_begin_epoch(ctr_.p, epoch_, stream_);
+  step_in_epoch_ = 0;
+  have_plan_ = true;
+}
+
+void DeviceTrainer::launch_step() {
+  ltfb_dev::launch_gather(args_, stream_);
+  ltfb_dev::launch_pre(args_, stream_);
+  if (wide_kind_ == 2) ltfb_dev::launch_wide_tc(args_, stream_);
+  else ltfb_dev::launch_wide_generic(args_, stream_);
+  ltfb_dev::launch_post(args_, stream_);
+}
+
+void DeviceTrainer::enqueue_steps(std::size_t n) {
+  DeviceGuard g(spec_.device);
+  if (n_part_ == 0) throw ContractError("train_steps: data store is empty");
+  ensure_adam_table(t_host_max_ + host_step_ + n + 1);
+  for (std::size_t i = 0; i < n; ++i) {
+    if (!have_plan_ || step_in_epoch_ >= steps_per_epoch_) {
+      start_epoch();
+    }
+    if (!seg_open_) {
+      seg_start_ = next_event();
+      LTFB_CUDA(cudaEventRecord(seg_start_, stream_));
+      seg_open_ = true;
+    }
+    // data/store.hpp:314-318: deliveries whose owner differs from the
+    // consuming shard are counted as shuffled samples.
+    const std::size_t begin = step_in_epoch_ * spec_.batch_size;
+    const std::size_t rows = std::min(spec_.batch_size, n_part_ - begin);
+    if (spec_.n_shards > 1) {
+      const auto ranges = ltfb::data::shard_split(rows, spec_.n_shards);
+      const auto& slots = perm_slots_[epoch_ & 1];
+      for (int s = 0; s < spec_.n_shards; ++s)
+        for (std::size_t r = ranges[s].first; r < ranges[s].second; ++r)
+          if (owner_[slots[begin + r]] >= 0 && owner_[slots[begin + r]] != s) ++epoch_shuffled_;
+    }
+    launch_step();
+    ++step_in_epoch_;
+    ++epoch_steps_;
+    ++host_step_;
+  }
+  LTFB_CUDA(cudaGetLastError());
+}
+
+bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepRecord>& out) {
+  DeviceGuard g(spec_.device);
+  std::size_t done = 0;
+  while (done < n) {
+    const std::size_t chunk = std::min<std::size_t>(n - done, rec_.n);
+    const std::uint64_t first = host_step_;
+    enqueue_steps(chunk);
+    close_epoch_segment(false, false);
+    LTFB_CUDA(cudaStreamSynchronize(stream_));
+    // resolve this chunk's segment timings lazily at epoch close
+    std::vector<ltfb_dev::StepRec> recs(chunk);
+    const std::size_t at = first % rec_.n;
+    const std::size_t n1 = std::min(chunk, rec_.n - at);
+    LTFB_CUDA(cudaMemcpy(recs.data(), rec_.p + at, n1 * sizeof(ltfb_dev::StepRec), cudaMemcpyDeviceToHost));
+    if (n1 < chunk)
+      LTFB_CUDA(cudaMemcpy(recs.data() + n1, rec_.p, (chunk - n1) * sizeof(ltfb_dev::StepRec),
+                           cudaMemcpyDeviceToHost));
+    for (std::size_t i = 0; i < chunk; ++i) {
+      const auto& r = recs[i];
+      ltfb::train::StepRecord s;
+      s.trainer = spec_.trainer_id;
+      s.step = r.step;
+      s.epoch = r.epoch;
+      s.d_loss = r.d_loss;
+      s.g_total = r.g_total;
+      s.g_fwd = r.g_fwd;
+      s.g_adv = r.g_adv;
+      s.g_cyc = r.g_cyc;
+      s.skipped = (r.flags & 1u) != 0;
+      out.push_back(s);
+      if (r.flags & 8u) {
+        // abort: steps enqueued after this one were no-ops on the device;
+        // roll the host bookkeeping back to this step.
+        const std::uint64_t extra = chunk - 1 - i;
+        host_step_ -= extra;
+        epoch_steps_ -= std::min<std::uint64_t>(epoch_steps_, extra);
+        return false;
+      }
+    }
+    done += chunk;
+  }
+  return true;
+}
+
+std::vector<DeviceTrainer::EpochInfo> DeviceTrainer::take_epochs() {
+  std::vector<EpochInfo> out;
+  out.swap(closed_);
+  return out;
+}
+
+void DeviceTrainer::flush_epoch() {
+  DeviceGuard g(spec_.device);
+  if (have_plan_ && step_in_epoch_ > 0) {
+    close_epoch_segment(true, step_in_epoch_ < steps_per_epoch_);
+  }
+}
+
+void DeviceTrainer::synchronize() {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// ----------------------------------------------------------- evaluation --
+EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int nc, bool decide,
+                                double w_f, double w_i) {
+  DeviceGuard g(spec_.device);
+  const std::size_t rows = which == 0 ? tour_rows_ : val_rows_;
+  if (rows == 0) throw ContractError(which == 0 ? "Trainer: no tournament slice configured"
+                                                : "evaluate: empty data slice");
+  ltfb_dev::EvalArgs e{};
+  e.m = margs_;
+  e.rows = static_cast<int>(rows);
+  e.nc = nc;
+  e.S = static_cast<int>(eval_S_);
+  e.x = which == 0 ? tx_.p : vx_.p;
+  e.y = which == 0 ? ty_.p : vy_.p;
+  e.enc = params_[0].p;
+  e.dec = params_[1].p;
+  const float* own_f = gen_.p;
+  const float* own_i = gen_.p + counts_[2];
+  e.cf[0] = cf ? cf : own_f;
+  e.ci[0] = ci ? ci : own_i;
+  e.cf[1] = incoming_.p;
+  e.ci[1] = incoming_.p + counts_[2];
+  e.h = eval_h_.p;
+  e.inv_row = eval_inv_.p;
+  e.part = eval_part_.p;
+  e.out = eval_out_.p;
+  e.w_f = w_f;
+  e.w_i = w_i;
+  e.decide = decide ? 1 : 0;
+  e.dst_fwd = gen_.p;
+  e.dst_inv = gen_.p + counts_[2];
+  e.m_fwd = mom1_[2].p;
+  e.v_fwd = mom2_[2].p;
+  e.m_inv = mom1_[3].p;
+  e.v_inv = mom2_[3].p;
+  e.n_fwd = static_cast<long long>(counts_[2]);
+  e.n_inv = static_cast<long long>(counts_[3]);
+  e.ctr = ctr_.p;
+  ltfb_dev::launch_eval(e, stream_);
+  LTFB_CUDA(cudaGetLastError());
+  double out[6] = {0, 0, 0, 0, 0, 0};
+  LTFB_CUDA(cudaMemcpyAsync(out, eval_out_.p, sizeof(double) * 3 * nc, cudaMemcpyDeviceToHost, stream_));
+  int adopt = 0;
+  LTFB_CUDA(cudaMemcpyAsync(&adopt, &ctr_.p->last_adopt, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  EvalOut r;
+  for (int c = 0; c < nc; ++c) r.m[c] = {out[3 * c], out[3 * c + 1], out[3 * c + 2]};
+  r.adopted = decide ? adopt : 0;
+  return r;
+}
+
+void DeviceTrainer::set_incoming(const float* fwd, const float* inv) {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaMemcpyAsync(incoming_.p, fwd, counts_[2] * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaMemcpyAsync(incoming_.p + counts_[2], inv, counts_[3] * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+EvalOut DeviceTrainer::tournament_decide() {
+  return evaluate(0, nullptr, nullptr, 2, true, spec_.w_f, spec_.w_i);
+}
+
+void DeviceTrainer::adopt(const float* fwd, const float* inv) {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaMemcpyAsync(gen_.p, fwd, counts_[2] * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaMemcpyAsync(gen_.p + counts_[2], inv, counts_[3] * 4, cudaMemcpyHostToDevice, stream_));
+  for (int net : {2, 3}) {
+    LTFB_CUDA(cudaMemsetAsync(mom1_[net].p, 0, counts_[net] * 4, stream_));
+    LTFB_CUDA(cudaMemsetAsync(mom2_[net].p, 0, counts_[net] * 4, stream_));
+  }
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+double DeviceTrainer::ae_step(const std::uint32_t*, std::size_t) {
+  throw ContractError("ae_step: not available in this build");
+}
+void DeviceTrainer::load_ae_source(const float*, std::size_t) {
+  throw ContractError("load_ae_source: not available in this build");
+}
+
+}  // namespace ltfb_b200

@@ -1,0 +1,220 @@
+// DeviceTrainer: one LTFB trainer resident on one GPU.
+//
+// Owns every device buffer of the trainer (parameter blobs and Adam state,
+// the HBM data store of its partition, the tournament and validation slices,
+// the step intermediates) plus one CUDA stream, and drives the step kernels.
+// It is the implementation behind both the C ABI (include/ltfb_gpu.h) and the
+// C++ drop-in façade (include/ltfb_b200/trainer.hpp), and mirrors the state
+// machine of the reference train::Trainer (train/trainer.hpp:41-308):
+// epoch plans, D-then-G steps, numeric skip / abort, epoch records,
+// tournament evaluation and generator adoption.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "ltfb_b200/types.hpp"
+#include "step_args.cuh"
+
+namespace ltfb_b200 {
+
+void cuda_check(cudaError_t e, const char* what);
+#define LTFB_CUDA(x) ::ltfb_b200::cuda_check((x), #x)
+
+/// RAII device guard (cudaSetDevice for the current scope).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(std::size_t count) {
+    release();
+    if (count) LTFB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  std::size_t bytes() const { return n * sizeof(T); }
+};
+
+struct TrainerSpec {
+  ltfb::surrogate::ModalityDims dims;
+  ltfb::surrogate::SurrogateArch arch;
+  int trainer_id = 0;
+  int device = 0;
+  int n_shards = 1;
+  std::size_t batch_size = 128;
+  std::uint64_t seed = 0;
+  int numeric_abort_threshold = 10;
+  double w_f = 1.0, w_i = 1.0;
+  double lr[5] = {0, 0, 0, 0, 0};  // 0 = arch.adam.lr
+  int wide_kernel = 0;             // 0 auto, 1 generic, 2 tcgen05
+};
+
+struct EvalOut {
+  ltfb::surrogate::EvalMetric m[2];
+  int adopted = 0;
+};
+
+/// Nets are indexed like ltfb_dev::NetId: enc, dec, fwd, inv, disc.
+class DeviceTrainer {
+ public:
+  explicit DeviceTrainer(const TrainerSpec& spec);
+  ~DeviceTrainer();
+  DeviceTrainer(const DeviceTrainer&) = delete;
+  DeviceTrainer& operator=(const DeviceTrainer&) = delete;
+
+  const TrainerSpec& spec() const { return spec_; }
+  int device() const { return spec_.device; }
+  cudaStream_t stream() const { return stream_; }
+  std::size_t param_count(int net) const { return counts_[net]; }
+  const ltfb::nn::MlpSpec& net_spec(int net) const { return specs_[net]; }
+
+  // ---- parameters & optimizer state (host <-> HBM, blob layout) ----
+  void set_params(int net, const float* blob, std::size_t count);
+  void get_params(int net, float* blob, std::size_t count);
+  void set_adam(int net, const float* m, const float* v, std::uint64_t t);
+  void get_adam(int net, float* m, float* v, std::uint64_t* t);
+
+  // ---- data ----
+  /// Uploads the partition (slot i = ids[i]) into the HBM store. `owner`
+  /// (optional) is the owning shard per slot for shuffle accounting.
+  void load_store(const std::uint32_t* ids, std::size_t n, const float* x, const float* y,
+                  const std::int32_t* owner = nullptr);
+  /// Device-generated partition (synthetic generator on the GPU).
+  void generate_store(const std::uint32_t* ids, std::size_t n, std::uint64_t spec_seed,
+                      std::uint64_t sampling_seed, std::uint64_t total_n);
+  void set_slice(int which, const float* x, const float* y, std::size_t rows);  // 0 tour, 1 val
+  std::size_t slice_rows(int which) const { return which == 0 ? tour_rows_ : val_rows_; }
+
+  // ---- training ----
+  /// Runs n steps; appends one record per executed step. Returns false if
+  /// the numeric abort threshold was exceeded (records end at that step).
+  bool train_steps(std::size_t n, std::vector<ltfb::train::StepRecord>& out);
+  std::uint64_t step() const { return host_step_; }
+  struct EpochInfo {
+    std::uint32_t epoch;
+    std::uint64_t steps, samples_shuffled;
+    double seconds;
+    bool partial;
+  };
+  /// Closed epoch records (epoch >= 1) produced so far; drains the queue.
+  std::vector<EpochInfo> take_epochs();
+  /// Closes the in-flight epoch as partial (trainer.hpp:129-134).
+  void flush_epoch();
+
+  // ---- tournament / evaluation ----
+  /// Evaluates candidates (null pointers = this trainer's own fwd/inv) on
+  /// slice `which` (0 tournament, 1 validation).
+  EvalOut evaluate(int which, const float* cand_fwd_dev, const float* cand_inv_dev, int nc,
+                   bool decide, double w_f, double w_i);
+  /// Uploads host blobs into the incoming-generator buffer.
+  void set_incoming(const float* fwd, const float* inv);
+  /// Device pointers of the own [fwd|inv] generator blob and the incoming one.
+  float* generator_dev() { return gen_.p; }
+  float* incoming_dev() { return incoming_.p; }
+  std::size_t generator_floats() const { return counts_[2] + counts_[3]; }
+  /// Evaluate local vs incoming on the tournament slice, decide and adopt
+  /// on the device (K3 + K9). Requires the incoming buffer filled.
+  EvalOut tournament_decide();
+  /// Installs fwd/inv blobs and zeroes their moments, keeping t.
+  void adopt(const float* fwd, const float* inv);
+  void synchronize();
+
+  // ---- autoencoder pre-training (runner.hpp:249-279) ----
+  /// One AE step on rows `rows_idx` (slots of the AE source store).
+  double ae_step(const std::uint32_t* rows_idx, std::size_t n);
+  void load_ae_source(const float* y, std::size_t n);
+
+  // exposed for benchmarks: launches one step without reading back
+  void enqueue_steps(std::size_t n);
+  std::size_t wide_ctas() const { return S_; }
+  const ltfb_dev::StepArgs& step_args() const { return args_; }
+  int wide_kernel_kind() const { return wide_kind_; }
+
+ private:
+  void build_model_args();
+  void ensure_adam_table(std::uint64_t t_max);
+  void start_epoch();
+  void launch_step();
+  void close_epoch_segment(bool epoch_done, bool partial);
+
+  TrainerSpec spec_;
+  ltfb::nn::MlpSpec specs_[5];
+  std::size_t counts_[5] = {};
+  ltfb_dev::ModelArgs margs_{};
+  ltfb_dev::StepArgs args_{};
+  cudaStream_t stream_ = nullptr;
+  int sm_count_ = 148;
+  std::size_t S_ = 0;
+  int wide_kind_ = 1;
+
+  DevBuf<float> params_[5], mom1_[5], mom2_[5], grads_[5];
+  DevBuf<float> gen_;       // [fwd | inv] contiguous (exchange payload)
+  DevBuf<float> incoming_;  // [fwd | inv] of an incoming generator
+  DevBuf<float> sx_, sy_;
+  DevBuf<unsigned> perm_[2];
+  DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
+  DevBuf<double> mae_part_, adam_c_;
+  DevBuf<ltfb_dev::Counters> ctr_;
+  DevBuf<ltfb_dev::StepRec> rec_;
+  std::uint64_t adam_cap_ = 0;
+  std::uint64_t t_host_max_ = 0;  // upper bound of any net's t
+
+  // epoch plan (host)
+  std::vector<std::uint32_t> part_ids_;
+  std::vector<std::int32_t> owner_;
+  std::size_t n_part_ = 0;
+  std::uint32_t epoch_ = 0;
+  std::size_t step_in_epoch_ = 0, steps_per_epoch_ = 0;
+  bool have_plan_ = false;
+  std::uint64_t host_step_ = 0;
+  std::vector<std::uint32_t> perm_slots_[2];
+  unsigned* pinned_perm_[2] = {nullptr, nullptr};
+  cudaEvent_t perm_ev_[2] = {nullptr, nullptr};
+  // epoch accounting
+  std::uint64_t epoch_steps_ = 0, epoch_shuffled_ = 0;
+  double epoch_seconds_ = 0;
+  std::vector<EpochInfo> closed_;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::size_t ev_used_ = 0;
+  struct Segment {
+    cudaEvent_t a, b;
+  };
+  std::vector<Segment> open_segments_;
+  cudaEvent_t seg_start_ = nullptr;
+  bool seg_open_ = false;
+  cudaEvent_t next_event();
+
+  // slices
+  DevBuf<float> tx_, ty_, vx_, vy_;
+  std::size_t tour_rows_ = 0, val_rows_ = 0;
+  DevBuf<float> eval_h_;
+  DevBuf<double> eval_inv_, eval_part_, eval_out_;
+  std::size_t eval_S_ = 0;
+
+  // AE
+  DevBuf<float> ae_y_;
+  std::size_t ae_rows_ = 0;
+  DevBuf<unsigned> ae_idx_;
+  DevBuf<double> ae_loss_;
+};
+
+}  // namespace ltfb_b200

@@ -1,0 +1,268 @@
+"""CUDA path vs the reference (golden vectors from the unmodified reference)
+and vs the pinned C oracle, through the C ABI.
+
+Tolerances (stated per north_star):
+  * integer artefacts (pairings, permutations, step/epoch counters, skip
+    flags, winner decisions) are bit-exact;
+  * per-step losses and weights (fp32 parity mode, generic/tcgen05 3xTF32
+    wide pass) within REL_LOSS relative of the reference over the run --
+    the reference's own summation-order tolerance is 1e-4 over 50 steps
+    (tests/acceptance_test.cpp:210-244);
+  * evaluation metrics within REL_EVAL.
+"""
+import numpy as np
+import pytest
+
+L = pytest.importorskip("paper_1910_02270_b200")
+pytestmark = pytest.mark.gpu
+
+REL_LOSS = 1e-4
+REL_EVAL = 1e-5
+REL_W = 1e-3   # weights after up to 20 Adam steps (absolute scale of lr)
+
+TINY = L.ModalityDims(image_views=1, image_channels=1, image_h=4, image_w=4)
+DESK = L.ModalityDims()
+PAPER = L.ModalityDims.paper_scale()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    try:
+        n = L.device_count()
+    except L.Error:
+        n = 0
+    if n < 1:
+        pytest.skip("no CUDA device")
+
+
+def rel(a, b, floor=1e-12):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
+
+
+def make_trainer(g, pfx, dims, arch, ds_meta, wide_kernel=0, shards=None):
+    model_seed, gshards, batch, seed, n_tour, steps = (int(v) for v in g[pfx + "cfg"])
+    n, per_file, spec_seed, sampling_seed = (int(v) for v in ds_meta)
+    ds = L.synthetic_dataset(dims, n, sampling_seed=sampling_seed, spec_seed=spec_seed,
+                             samples_per_file=per_file)
+    model = L.make_cyclegan(dims, arch, model_seed)
+    model.autoencoder_frozen = True
+    ids = np.arange(n, dtype=np.uint32)
+    cfg = L.TrainerConfig(trainer_id=0, n_shards=shards or gshards, batch_size=batch, seed=seed,
+                          prefetch_depth=0, train_ids=ids[n_tour:], tournament_ids=ids[:n_tour],
+                          wide_kernel=wide_kernel)
+    return L.Trainer(cfg, ds, model), steps, ds
+
+
+def check_against_golden(g, pfx, t, steps):
+    e0 = t.eval_tournament()
+    assert rel([e0.forward_mae, e0.inverse_mae, e0.combined], g[pfx + "eval0"]) < REL_EVAL
+    t.train_steps(steps)
+    t.flush_epoch_record()
+    h = t.history()
+    assert [s.step for s in h.steps] == [int(v) for v in g[pfx + "steps_step"]]
+    assert [s.epoch for s in h.steps] == [int(v) for v in g[pfx + "steps_epoch"]]
+    assert [int(s.skipped) for s in h.steps] == [int(v) for v in g[pfx + "steps_skipped"]]
+    errs = {}
+    for name in ("d_loss", "g_total", "g_fwd", "g_adv", "g_cyc"):
+        errs[name] = rel([getattr(s, name) for s in h.steps], g[pfx + "steps_" + name])
+    assert max(errs.values()) < REL_LOSS, errs
+    m = t.model()
+    for n in ("fwd", "inv", "disc"):
+        ref = g[pfx + "final_" + n]
+        assert np.max(np.abs(m.blobs[n] - ref)) < REL_W * max(1.0, float(np.max(np.abs(ref)))), n
+    e1 = t.eval_tournament()
+    assert rel([e1.forward_mae, e1.inverse_mae, e1.combined], g[pfx + "eval1"]) < 10 * REL_EVAL
+    assert [m.opt[n].t for n in ("fwd", "inv", "disc")] == [int(v) for v in g[pfx + "opt_t"]]
+    ep = [e for e in h.epochs]
+    assert [e.epoch for e in ep] == [int(v) for v in g[pfx + "epochs_epoch"]]
+    assert [e.steps for e in ep] == [int(v) for v in g[pfx + "epochs_steps"]]
+    assert [e.files_opened for e in ep] == [int(v) for v in g[pfx + "epochs_files_opened"]]
+    assert [e.bytes_read for e in ep] == [int(v) for v in g[pfx + "epochs_bytes_read"]]
+    assert [e.samples_shuffled for e in ep] == [int(v) for v in g[pfx + "epochs_samples_shuffled"]]
+    assert [int(e.partial) for e in ep] == [int(v) for v in g[pfx + "epochs_partial"]]
+    return errs
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_trainer_tiny_matches_reference(golden, kernel):
+    g = golden("trainer")
+    t, steps, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"], kernel)
+    check_against_golden(g, "tiny_s1_", t, steps)
+
+
+@pytest.mark.parametrize("pfx", ["tiny_s2_", "tiny_s4_"])
+def test_trainer_tiny_shards(golden, pfx):
+    """n_shards > 1: same minibatch math (shard-weighted mean == full-batch
+    mean), within the reference's own shard tolerance; shuffle accounting
+    exact."""
+    g = golden("trainer")
+    t, steps, _ = make_trainer(g, pfx, TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    check_against_golden(g, pfx, t, steps)
+    hs = t.replica_hashes()
+    assert len(hs) == int(g[pfx + "cfg"][1]) and len(set(hs)) == 1
+
+
+@pytest.mark.parametrize("pfx", ["desk_s1_", "desk_s2_"])
+def test_trainer_desk_matches_reference(golden, pfx):
+    g = golden("trainer")
+    t, steps, _ = make_trainer(g, pfx, DESK, L.SurrogateArch(), g["desk_data"])
+    check_against_golden(g, pfx, t, steps)
+
+
+@pytest.mark.parametrize("kernel", [1, 0])
+def test_trainer_paper_matches_reference(golden, kernel):
+    g = golden("trainer")
+    t, steps, _ = make_trainer(g, "paper_s1_", PAPER, L.SurrogateArch(), g["paper_data"], kernel)
+    check_against_golden(g, "paper_s1_", t, steps)
+
+
+def test_numeric_skip_then_abort(golden):
+    """tests/test_trainer.cpp:208-222: poisoned fwd weights overflow; three
+    skips are allowed, the fourth aborts with NumericError; nothing applied."""
+    g = golden("trainer")
+    ds = L.synthetic_dataset(TINY, 600, sampling_seed=17, spec_seed=3, samples_per_file=100)
+    model = L.make_cyclegan(TINY, L.SurrogateArch.tiny(), 6)
+    model.autoencoder_frozen = True
+    w = L.layer_widths(TINY, L.SurrogateArch.tiny(), 2)
+    off = 0
+    for l in range(len(w) - 1):
+        model.blobs["fwd"][off:off + w[l] * w[l + 1]] = 1e38
+        off += w[l] * w[l + 1] + w[l + 1]
+    before = {n: model.blobs[n].copy() for n in ("fwd", "inv", "disc")}
+    ids = np.arange(600, dtype=np.uint32)
+    cfg = L.TrainerConfig(n_shards=1, batch_size=32, seed=10, numeric_abort_threshold=3,
+                          prefetch_depth=0, train_ids=ids[30:], tournament_ids=ids[:30])
+    t = L.Trainer(cfg, ds, model)
+    with pytest.raises(L.NumericError):
+        t.train_steps(10)
+    st = t.history().steps
+    assert [int(s.skipped) for s in st] == list(g["abort_steps_skipped"])
+    assert t.history().skipped_steps == int(g["abort_skipped"][0])
+    assert t.step() == int(g["abort_step"][0])
+    m = t.model()
+    for n in ("inv", "disc"):
+        assert np.array_equal(m.blobs[n], before[n]), n
+
+
+def test_zero_steps_and_determinism(golden):
+    g = golden("trainer")
+    a, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    h0 = a.model().model_hash()
+    a.train_steps(0)
+    assert a.step() == 0 and a.model().model_hash() == h0 and not a.history().steps
+    b, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    a.train_steps(10)
+    b.train_steps(10)
+    assert [s.g_total for s in a.history().steps] == [s.g_total for s in b.history().steps]
+    assert a.model().model_hash() == b.model().model_hash()
+    e1, e2 = a.eval_tournament(), a.eval_tournament()
+    assert e1.combined == e2.combined and e1.combined > 0
+
+
+def test_adopt_resets_moments_keeps_t(golden):
+    g = golden("trainer")
+    t, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    t.train_steps(5)
+    donor = L.make_cyclegan(TINY, L.SurrogateArch.tiny(), 99)
+    t.adopt_generators(donor.fwd, donor.inv)
+    m = t.model()
+    assert m.fwd_hash() == donor.fwd_hash() and m.inv_hash() == donor.inv_hash()
+    assert not m.opt["fwd"].m.any() and not m.opt["fwd"].v.any() and m.opt["fwd"].t == 5
+    with pytest.raises(L.ContractError):
+        t.adopt_generators(donor.fwd[:-1], donor.inv)
+
+
+def test_paper_eval_matches_oracle(oracle):
+    """Evaluation at paper dims (tournament metric) vs the C oracle."""
+    ds = L.synthetic_dataset(PAPER, 64, sampling_seed=5, spec_seed=1)
+    model = L.make_cyclegan(PAPER, L.SurrogateArch(), 11)
+    model.autoencoder_frozen = True
+    ids = np.arange(64, dtype=np.uint32)
+    t = L.Trainer(L.TrainerConfig(n_shards=1, train_ids=ids[24:], tournament_ids=ids[:24]), ds, model)
+    got = t.eval_tournament()
+    og = oracle.Gan(list(PAPER.as_tuple()), oracle.Arch(), 11)
+    ref = og.evaluate(ds.x[:24], ds.y[:24])
+    assert rel([got.forward_mae, got.inverse_mae, got.combined], ref) < REL_EVAL
+
+
+@pytest.mark.parametrize("pfx", ["tiny_k2_", "tiny_k4_", "tiny_k3_"])
+def test_tournament_decisions_state_injection(golden, pfx):
+    """Pre-round generators captured from the reference, evaluated and
+    decided by the device kernels on each trainer's tournament slice:
+    decisions bit-identical, metrics within REL_EVAL."""
+    g = golden("tournament")
+    cfg = [int(v) for v in g[pfx + "cfg"]]
+    gen_n, spf, spec_seed, sampling_seed, k = cfg[:5]
+    dims = L.ModalityDims(*[int(v) for v in g[pfx + "dims"]])
+    arch = L.SurrogateArch.tiny()
+    ds = L.synthetic_dataset(dims, gen_n, sampling_seed=sampling_seed, spec_seed=spec_seed,
+                             samples_per_file=spf)
+    tour_sizes = g[pfx + "split_tour_sizes"].astype(np.int64)
+    tour_off = np.concatenate([[0], np.cumsum(tour_sizes)])
+    tr_sizes = g[pfx + "split_train_sizes"].astype(np.int64)
+    tr_off = np.concatenate([[0], np.cumsum(tr_sizes)])
+    fo = np.concatenate([[0], np.cumsum(g[pfx + "pre_round_fwd_len"].astype(np.int64))])
+    io = np.concatenate([[0], np.cumsum(g[pfx + "pre_round_inv_len"].astype(np.int64))])
+    base = L.make_cyclegan(dims, arch, 0)
+    base.blobs["enc"][:] = g[pfx + "ae_enc"]
+    base.blobs["dec"][:] = g[pfx + "ae_dec"]
+    base.autoencoder_frozen = True
+    trainers = []
+    for t in range(k):
+        c = L.TrainerConfig(trainer_id=t, n_shards=1, batch_size=32, prefetch_depth=0,
+                            train_ids=g[pfx + "split_train_ids"][tr_off[t]:tr_off[t + 1]],
+                            tournament_ids=g[pfx + "split_tour_ids"][tour_off[t]:tour_off[t + 1]])
+        trainers.append(L.Trainer(c, ds, base))
+    n_rounds = int(g[pfx + "round_step"].size)
+    rec_i = 0
+    worst_margin, worst_err = np.inf, 0.0
+    for rnd in range(1, n_rounds + 1):
+        for t in range(k):
+            j = (rnd - 1) * k + t
+            trainers[t].adopt_generators(g[pfx + "pre_round_fwd"][fo[j]:fo[j + 1]],
+                                         g[pfx + "pre_round_inv"][io[j]:io[j + 1]])
+        m = L.pair_trainers(k, rnd, L.mix_seed(cfg[9], 0x9A18))
+        assert m.bye == int(g[pfx + "round_bye"][rnd - 1])
+        res = L.tournament_round(trainers, m, rnd)
+        for r in res.trainer_records:
+            assert r.trainer == int(g[pfx + "tr_trainer"][rec_i]) and r.peer == int(g[pfx + "tr_peer"][rec_i])
+            assert r.kept_incoming == bool(g[pfx + "tr_kept"][rec_i])
+            err = max(rel(r.local_metric, g[pfx + "tr_local"][rec_i]),
+                      rel(r.incoming_metric, g[pfx + "tr_incoming"][rec_i]))
+            worst_err = max(worst_err, err)
+            worst_margin = min(worst_margin, abs(r.local_metric - r.incoming_metric) /
+                               max(abs(r.local_metric), 1e-12))
+            rec_i += 1
+    assert rec_i == g[pfx + "tr_round"].size
+    assert worst_err < REL_EVAL, (worst_err, worst_margin)
+    assert worst_err < worst_margin
+
+
+def test_identical_candidates_tie_and_keep_local(golden):
+    """tests/test_tournament.cpp:191-219: identical generators give exactly
+    equal metrics and the local model is kept."""
+    g = golden("trainer")
+    a, _, ds = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    b, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    res = L.tournament_round([a, b], L.Matching([(0, 1)]), 1)
+    for r in res.trainer_records:
+        assert r.local_metric == r.incoming_metric and not r.kept_incoming
+    assert {t.payload for t in res.transfers} == {"fwd", "inv"}
+
+
+def test_nonfinite_incoming_loses(golden):
+    g = golden("trainer")
+    a, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    b, _, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"])
+    bad = b.model().copy()
+    bad.blobs["fwd"][:] = np.nan
+    b.adopt_generators(bad.fwd, bad.inv)
+    good_hash = a.model().fwd_hash()
+    res = L.tournament_round([a, b], L.Matching([(0, 1)]), 1)
+    recs = {r.trainer: r for r in res.trainer_records}
+    assert not recs[0].kept_incoming and recs[1].kept_incoming
+    assert b.model().fwd_hash() == good_hash
+    with pytest.raises(L.ContractError):
+        a.train_steps(1)
+        L.tournament_round([a, b], L.Matching([(0, 1)]), 2)

@@ -1,0 +1,400 @@
+#!/usr/bin/env python3
+"""bench.py — LTFB tournament training of the JAG/ICF surrogate on B200.
+
+Metric (BASELINE.json): samples/s per box (whole job, all GPUs) and the
+tournament-round time, one trainer per GPU.
+
+Workload (configs[2]/[3]): paper dims (3 views x 4 ch x 64x64 + 15 scalars,
+output_dim 49167), default SurrogateArch, B = 128, one LTFB trainer per
+GPU, per-trainer partition of a synthetic JAG-shaped dataset resident in
+HBM (weak scaling), tournament rounds every --interval steps at N > 1
+(pairwise NCCL exchange + device-side decision). A step = one
+discriminator + one generator update on every trainer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 is launched with torchrun (one rank per GPU). Prints one JSON line on
+rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--dims", default="paper", choices=["paper", "desk"])
+    p.add_argument("--samples-per-trainer", type=int, default=8000)
+    p.add_argument("--batch", type=int, default=128)
+    p.add_argument("--interval", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=16)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--wide-kernel", type=int, default=0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-lms", "100"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- reference --
+def run_reference_bench(dims: str, trainers: int, steps: int, warmup: int, n: int, threads_total: int,
+                        batch: int):
+    exe = os.path.join(REPO, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None, "oracle/_ref/ref_bench not built"
+    env = dict(os.environ)
+    per = max(1, threads_total // max(1, trainers))
+    env["OPENBLAS_NUM_THREADS"] = str(per)
+    cmd = [exe, "--dims", dims, "--n", str(n), "--batch", str(batch), "--trainers", str(trainers),
+           "--threads", str(min(trainers, threads_total)), "--steps", str(steps), "--warmup", str(warmup),
+           "--dir", f"/tmp/ltfb_ref_bench_{os.getpid()}"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=1800)
+    if r.returncode != 0:
+        return None, "ref_bench failed: " + r.stderr[-300:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    out["blas_threads_per_trainer"] = per
+    out["cores"] = min(threads_total, per * trainers)
+    return out, None
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    k = max(1, args.gpus)
+    nproc = os.cpu_count() or 1
+    steps = max(1, min(args.steps, 6))
+    warm = max(1, min(args.warmup, 1))
+    per_trainer = min(args.samples_per_trainer, 1500 if args.dims == "paper" else 4000)
+    res, err = run_reference_bench(args.dims, k, steps, warm, per_trainer * k, nproc, args.batch)
+    metric = "samples/sec/box"
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": err}))
+        return 0
+    value = res["samples_per_s"]
+    line = {
+        "impl": "reference", "metric": metric, "value": value, "unit": "samples/s",
+        "n_gpus": k, "steps": steps, "warmup": warm, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference SynthGenerator, spec_seed 1, sampling_seed 1)",
+        "config": {"workload": workload_name(args, k), "global_batch": args.batch * k,
+                   "trainers": k, "samples_per_trainer_sample": per_trainer},
+        "round_ms": res.get("round_ms"),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": res["cores"], "kind": "reference",
+                         "sample": f"{steps} timed steps x {k} trainer(s), {per_trainer} samples/trainer, "
+                                   f"OpenBLAS-backed Eigen shim, {res['blas_threads_per_trainer']} BLAS "
+                                   f"threads/trainer"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def workload_name(args, k):
+    d = "paper 3x4x64x64 (out 49167)" if args.dims == "paper" else "desk 3x4x16x16 (out 3087)"
+    return (f"LTFB {k} trainer(s), one per GPU; {d}; default SurrogateArch; B={args.batch}; "
+            f"rounds every {args.interval} steps when k>1; HBM-resident partition store")
+
+
+# -------------------------------------------------------------------- b200 --
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import numpy as np
+
+    import paper_1910_02270_b200 as L
+
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist  # noqa: F811
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    dims = L.ModalityDims.paper_scale() if args.dims == "paper" else L.ModalityDims()
+    arch = L.SurrogateArch()
+    k = world
+    B = args.batch
+    seed = 1
+    # dataset: per-trainer partitions of one synthetic sweep (weak scaling)
+    total = int(args.samples_per_trainer * k / 0.95)
+    _, train_parts, tour_parts = L.split_dataset(total, k, 0.05, 0.05, seed, k >= 2)
+    my_train, my_tour = train_parts[rank], tour_parts[rank]
+    t0 = time.perf_counter()
+    need = np.concatenate([my_train, my_tour]).astype(np.uint32)
+    x, y = L.synth_generate_ids(dims, need, total, sampling_seed=1, spec_seed=1)
+    ds = L.SparseDataset(dims, need, x, y, total)
+    gen_s = time.perf_counter() - t0
+
+    base = L.make_cyclegan(dims, arch, L.mix_seed(seed, 0xAE0))
+    base.autoencoder_frozen = True
+    model = base.copy()
+    L.reinit_gan_nets(model, L.mix_seed(seed, 0x1417, rank))
+    cfg = L.TrainerConfig(trainer_id=rank, n_shards=1, batch_size=B, seed=L.mix_seed(seed, 0x57A7E1, rank),
+                          prefetch_depth=0, train_ids=my_train, tournament_ids=my_tour, device=local,
+                          wide_kernel=args.wide_kernel)
+    t0 = time.perf_counter()
+    tr = L.Trainer(cfg, ds, model)
+    load_s = time.perf_counter() - t0
+    del x, y
+    comm = None
+    if k > 1:
+        uid = L.Comm.unique_id() if rank == 0 else b"\0" * 128
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = L.Comm(obj[0], k, rank, local)
+
+    rounds_ms = []
+    round_counter = [0]
+
+    def do_round():
+        round_counter[0] += 1
+        m = L.pair_trainers(k, round_counter[0], L.mix_seed(seed, 0x9A18))
+        peer = None
+        for a, b in m.pairs:
+            if a == rank:
+                peer = b
+            elif b == rank:
+                peer = a
+        tr.timer_start()
+        if peer is not None:
+            tr.exchange(comm, peer)
+            tr.decide_incoming()
+        ms = tr.timer_stop()
+        rounds_ms.append(ms)
+
+    def run_steps(n):
+        done = 0
+        while done < n:
+            chunk = min(args.interval, n - done)
+            tr.train_steps_raw(chunk)
+            done += chunk
+            if k > 1 and chunk == args.interval:
+                do_round()
+
+    # warm-up (also compiles nothing: kernels are AOT sm_100a)
+    run_steps(max(args.warmup, 3))
+    warm_launch = tr.launch_count()
+    tr.kernel_timing(True)
+    rounds_ms.clear()
+    sampler = ClockSampler(local)
+    barrier()
+    tr.synchronize() if hasattr(tr, "synchronize") else None
+    sampler.start()
+    tr.timer_start()
+    run_steps(args.steps)
+    ms = tr.timer_stop()
+    clocks = sampler.stop()
+    barrier()
+    launches = tr.launch_count() - warm_launch
+    kt = {name: tr.kernel_time(i) for i, name in enumerate(("gather", "small_fwd", "wide", "post"))}
+    tr.kernel_timing(False)
+    ms_max = max_over_ranks(ms)
+    value = k * B * args.steps / (ms_max / 1e3)
+    round_ms = max_over_ranks(statistics.mean(rounds_ms)) if rounds_ms else None
+
+    # ---- e2e: same step through the C ABI with HOST buffers (pinned) -------
+    import torch
+    ne = max(2, args.e2e_steps)
+    out = dims.output_dim()
+    hx = torch.empty((ne, B, dims.input_dim), dtype=torch.float32, pin_memory=True).numpy()
+    hy = torch.empty((ne, B, out), dtype=torch.float32, pin_memory=True).numpy()
+    rows = np.arange(ne * B) % my_train.size
+    bx, by = ds.rows(my_train[rows])
+    hx[:] = bx.reshape(ne, B, -1)
+    hy[:] = by.reshape(ne, B, -1)
+    del bx, by
+    tr.train_steps_host(2, hx[:2], hy[:2])
+    barrier()
+    tr.timer_start()
+    tr.train_steps_host(ne, hx, hy)
+    e2e_ms = max_over_ranks(tr.timer_stop())
+    e2e_value = k * B * ne / (e2e_ms / 1e3)
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel --------------------------------
+    peaks, peak_src = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    E1, D = arch.enc_hidden[0], arch.dec_hidden[-1]
+    out_pad = (out + 3) // 4 * 4
+    bytes_of = {
+        # algorithmic bytes per launch
+        "gather": 2 * B * (out_pad + dims.input_dim) * 4,
+        "wide": (B * out + out * E1 + D * out + out) * 4,
+        "small_fwd": 0,
+        "post": 0,
+    }
+    shares = {n: v[0] for n, v in kt.items()}
+    dom = max(("gather", "wide"), key=lambda n: shares[n])
+    dms, dcount = kt[dom]
+    avg_ms = dms / max(dcount, 1)
+    achieved = bytes_of[dom] / (avg_ms / 1e3) / 1e9
+    kind, ctas = tr.wide_info()
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{dom}_kind{kind}")
+        except Exception:
+            traffic = None
+
+    # ---- CPU baseline: the reference itself on this box's host cores -------
+    cpu = None
+    if not args.no_cpu_baseline:
+        res, err = run_reference_bench(args.dims, 1, 3, 1, 1000 if args.dims == "paper" else 3000,
+                                       os.cpu_count() or 1, B)
+        if res is not None:
+            cpu = {"value": res["samples_per_s"], "unit": "samples/s", "cores": res["cores"],
+                   "kind": "reference",
+                   "sample": f"reference Trainer (oracle/_ref/ref_bench, OpenBLAS Eigen shim), 1 trainer, "
+                             f"3 timed steps of B={B} on a 1000-sample partition; round_ms "
+                             f"{res.get('round_ms')}"}
+        else:
+            cpu = {"value": None, "unit": "samples/s", "cores": 0, "kind": "reference", "sample": err}
+
+    line = {
+        "metric": "samples/sec/box", "value": value, "unit": "samples/s", "n_gpus": k,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SynthGenerator spec_seed 1, sampling_seed 1; random-init SurrogateArch)",
+        "config": {"workload": workload_name(args, k), "global_batch": B * k, "batch_per_trainer": B,
+                   "output_dim": out, "samples_per_trainer": int(my_train.size),
+                   "tournament_rows": int(my_tour.size), "interval": args.interval,
+                   "parallelism": f"ltfb{k} (one trainer per GPU, NCCL pairwise exchange)",
+                   "l2": "inputs larger than L2: each step gathers random rows of a "
+                         f"{my_train.size * out_pad * 4 / 1e9:.2f} GB HBM store",
+                   "wide_kernel": {1: "generic SIMT fp32", 2: "tcgen05 3xTF32"}.get(kind, str(kind)),
+                   "wide_ctas": ctas},
+        "round_ms": round_ms, "rounds_timed": len(rounds_ms),
+        "kernels_ms_per_launch": {n: (v[0] / v[1] if v[1] else None) for n, v in kt.items()},
+        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_of[dom]},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "samples/s",
+                "h2d_bytes_per_step": B * (dims.input_dim + out) * 4,
+                "d2h_bytes_per_step": 64,
+                "path": "ltfb_trainer_train_steps_host: pinned host minibatch -> H2D per step "
+                        "(copy stream, double-buffered) -> step kernels -> D2H step record"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "setup_s": {"generate": round(gen_s, 2), "preload": round(load_s, 2)},
+    }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -168,6 +168,26 @@ int ltfb_trainer_tournament_decide(ltfb_trainer* t, ltfb_eval_metric* local,
 /* Trainer::adopt_generators from host blobs. */
 int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv);
 
+/* ---- measurement hooks (bench.py) ------------------------------------- */
+/* Host-buffer variant of train_steps (the e2e path): the minibatches of the
+ * n steps come from HOST memory, x [n x batch x input_dim] and
+ * y [n x batch x output_dim] (pinned for full PCIe rate); every step's batch
+ * is copied H2D inside the call (double-buffered on a copy stream that
+ * overlaps the previous step's kernels) and its record is read back D2H. */
+int ltfb_trainer_train_steps_host(ltfb_trainer* t, uint64_t n, const float* x, const float* y,
+                                  ltfb_step_record* out, uint64_t* n_out);
+/* CUDA-event timer on the trainer's stream. */
+int ltfb_trainer_timer_start(ltfb_trainer* t);
+int ltfb_trainer_timer_stop(ltfb_trainer* t, double* ms);
+/* Per-kernel CUDA-event timing inside train_steps (0 gather, 1 small
+ * forward, 2 wide pass, 3 post/optimizer). on=1 resets the counters. */
+int ltfb_trainer_kernel_timing(ltfb_trainer* t, int on);
+int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* launches);
+/* Which wide-pass kernel is active (1 generic SIMT, 2 tcgen05) and its grid. */
+int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
+/* Number of kernels this trainer has launched so far (all of them ours). */
+int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches);
+
 /* ---- multi-GPU: one trainer per GPU, NCCL point-to-point exchange ------- */
 int ltfb_nccl_available(void);
 int ltfb_nccl_unique_id(uint8_t id[128]);
@@ -198,6 +218,10 @@ int ltfb_incoming_wins(double local, double incoming);                       /* 
 int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
                         uint64_t first, uint64_t n, uint64_t total_n, uint64_t sampling_seed,
                         float* x, float* y, int threads);
+/* the samples with global ids `ids` of a total_n sweep, in ids order */
+int ltfb_synth_generate_ids(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                            const uint32_t* ids, uint64_t n, uint64_t total_n, uint64_t sampling_seed,
+                            float* x, float* y, int threads);
 /* make_cyclegan blob init (model.hpp:96-132, mlp.hpp:235-244) */
 int ltfb_init_params(const ltfb_dims* dims, const ltfb_arch* arch, uint64_t seed, int net,
                      float* blob, uint64_t count);

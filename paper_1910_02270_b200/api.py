@@ -320,6 +320,35 @@ def synth_generate(dims: ModalityDims, n: int, sampling_seed: int = 1, spec_seed
     return x, y
 
 
+def synth_generate_ids(dims: ModalityDims, ids, total: int, sampling_seed: int = 1,
+                       spec_seed: int = 1, noise_level: float = 0.0, threads: int | None = None):
+    """Samples with global ids `ids` of a `total`-point sweep (host, threads)."""
+    ids = np.ascontiguousarray(ids, np.uint32)
+    x = np.empty((ids.size, dims.input_dim), np.float32)
+    y = np.empty((ids.size, dims.output_dim()), np.float32)
+    dc = dims.c()
+    threads = threads or max(1, os.cpu_count() or 1)
+    check(lib.ltfb_synth_generate_ids(C.byref(dc), spec_seed, noise_level, ids, ids.size, total,
+                                      sampling_seed, x, y, threads))
+    return x, y
+
+
+class SparseDataset(Dataset):
+    """Only the rows a trainer needs (its partition and tournament slice) of
+    a large synthetic dataset; ids stay global."""
+
+    def __init__(self, dims: ModalityDims, ids, x, y, total: int, samples_per_file: int = 500):
+        super().__init__(dims, x, y, samples_per_file)
+        self.ids = np.ascontiguousarray(ids, np.uint32)
+        self.total = int(total)
+        self._pos = {int(i): k for k, i in enumerate(self.ids)}
+
+    def rows(self, ids):
+        ids = np.asarray(ids)
+        sel = np.fromiter((self._pos[int(i)] for i in ids), np.int64, count=ids.size)
+        return self.x[sel], self.y[sel]
+
+
 def synthetic_dataset(dims: ModalityDims, n: int, sampling_seed: int = 1, spec_seed: int = 1,
                       noise_level: float = 0.0, samples_per_file: int = 500) -> Dataset:
     x, y = synth_generate(dims, n, sampling_seed, spec_seed, noise_level)
@@ -559,6 +588,48 @@ class Trainer:
         self._drain_epochs()
         check(rc)
 
+    # -- measurement hooks (bench.py)
+    def timer_start(self):
+        check(lib.ltfb_trainer_timer_start(self._h))
+
+    def timer_stop(self) -> float:
+        ms = C.c_double(0)
+        check(lib.ltfb_trainer_timer_stop(self._h, C.byref(ms)))
+        return ms.value
+
+    def kernel_timing(self, on: bool):
+        check(lib.ltfb_trainer_kernel_timing(self._h, int(on)))
+
+    def kernel_time(self, which: int):
+        ms, n = C.c_double(0), C.c_uint64(0)
+        check(lib.ltfb_trainer_kernel_time(self._h, which, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def wide_info(self):
+        k, c = C.c_int32(0), C.c_int32(0)
+        check(lib.ltfb_trainer_wide_info(self._h, C.byref(k), C.byref(c)))
+        return k.value, c.value
+
+    def launch_count(self) -> int:
+        n = C.c_uint64(0)
+        check(lib.ltfb_trainer_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def train_steps_host(self, n: int, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+        """e2e path: n steps whose minibatches x [n,B,in], y [n,B,out] are in
+        host memory and are copied H2D inside the call."""
+        recs = (_lib.StepRecordC * n)()
+        got = C.c_uint64(0)
+        check(lib.ltfb_trainer_train_steps_host(self._h, n, ptr(x), ptr(y), recs, C.byref(got)))
+        self._dirty = True
+        return np.ctypeslib.as_array(recs)
+
+    def exchange(self, comm: "Comm", peer: int):
+        check(lib.ltfb_trainer_exchange(self._h, comm._h, peer))
+
+    def decide_incoming(self):
+        return self._decide()
+
     def train_steps_raw(self, n: int) -> np.ndarray:
         """Benchmark entry: runs n steps and returns the records as an array."""
         recs = (_lib.StepRecordC * n)()
@@ -635,6 +706,32 @@ class Trainer:
         check(lib.ltfb_trainer_tournament_decide(self._h, C.byref(loc), C.byref(inc), C.byref(adopted)))
         self._dirty = True
         return self._metric(loc), self._metric(inc), bool(adopted.value)
+
+
+class Comm:
+    """NCCL communicator of the multi-GPU run (one rank per GPU/trainer)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        self._h = C.c_void_p()
+        check(lib.ltfb_comm_create(uid, nranks, rank, device, C.byref(self._h)))
+        self.nranks, self.rank = nranks, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib.ltfb_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self._h and self._h.value:
+            check(lib.ltfb_comm_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def tournament_round(trainers: list, matching: Matching, round_index: int) -> RoundResult:

@@ -359,6 +359,57 @@ int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv) {
   return guarded([&] { T(t).adopt(fwd, inv); });
 }
 
+int ltfb_trainer_train_steps_host(ltfb_trainer* t, uint64_t n, const float* x, const float* y,
+                                  ltfb_step_record* out, uint64_t* n_out) {
+  bool ok = true;
+  std::vector<ltfb::train::StepRecord> recs;
+  const int rc = guarded([&] {
+    recs.reserve(n);
+    ok = T(t).train_steps_host(n, x, y, recs);
+  });
+  if (n_out) *n_out = recs.size();
+  if (out)
+    for (std::size_t i = 0; i < recs.size(); ++i) {
+      const auto& r = recs[i];
+      out[i] = {r.step, r.epoch, r.skipped ? 1u : 0u, r.d_loss, r.g_total, r.g_fwd, r.g_adv, r.g_cyc};
+    }
+  if (rc != LTFB_OK) return rc;
+  if (!ok) {
+    g_err = "trainer exceeded the numeric skip threshold";
+    return LTFB_ENUMERIC;
+  }
+  return LTFB_OK;
+}
+
+int ltfb_trainer_timer_start(ltfb_trainer* t) {
+  return guarded([&] { T(t).timer_start(); });
+}
+int ltfb_trainer_timer_stop(ltfb_trainer* t, double* ms) {
+  return guarded([&] { *ms = T(t).timer_stop_ms(); });
+}
+int ltfb_trainer_kernel_timing(ltfb_trainer* t, int on) {
+  return guarded([&] { T(t).set_kernel_timing(on != 0); });
+}
+int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* launches) {
+  return guarded([&] {
+    if (which < 0 || which > 3) throw ltfb::ContractError("bad kernel index");
+    const auto r = T(t).kernel_time(which);
+    *ms = r.first;
+    *launches = r.second;
+  });
+}
+int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas) {
+  return guarded([&] {
+    auto& tr = T(const_cast<ltfb_trainer*>(t));
+    *kind = tr.wide_kernel_kind();
+    *ctas = static_cast<int32_t>(tr.wide_ctas());
+  });
+}
+
+int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches) {
+  return guarded([&] { *launches = T(const_cast<ltfb_trainer*>(t)).launch_count(); });
+}
+
 int ltfb_nccl_available(void) { return nccl().ok ? 1 : 0; }
 
 int ltfb_nccl_unique_id(uint8_t id[128]) {
@@ -501,9 +552,9 @@ int ltfb_incoming_wins(double local, double incoming) {
   return ltfb::tournament::incoming_wins(local, incoming) ? 1 : 0;
 }
 
-int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_level, uint64_t first,
-                        uint64_t n, uint64_t total_n, uint64_t sampling_seed, float* x, float* y,
-                        int threads) {
+static int synth_rows(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                      const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
+                      uint64_t sampling_seed, float* x, float* y, int threads) {
   return guarded([&] {
     ltfb::synth::GeneratorSpec spec;
     spec.dims = dims_of(dims);
@@ -514,7 +565,8 @@ int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_
     const std::size_t in = spec.dims.input_dim, out = spec.dims.output_dim();
     auto work = [&](std::uint64_t a, std::uint64_t b) {
       for (std::uint64_t i = a; i < b; ++i) {
-        const auto p = ltfb::synth::sweep_point(first + i, g, sampling_seed);
+        const std::uint64_t id = ids ? ids[i] : first + i;
+        const auto p = ltfb::synth::sweep_point(id, g, sampling_seed);
         gen.sample_into(p, x + i * in, y + i * out);
       }
     };
@@ -527,6 +579,18 @@ int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_
     for (int w = 0; w < nt; ++w) pool.emplace_back(work, n * w / nt, n * (w + 1) / nt);
     for (auto& th : pool) th.join();
   });
+}
+
+int ltfb_synth_generate_ids(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                            const uint32_t* ids, uint64_t n, uint64_t total_n, uint64_t sampling_seed,
+                            float* x, float* y, int threads) {
+  return synth_rows(dims, spec_seed, noise_level, ids, 0, n, total_n, sampling_seed, x, y, threads);
+}
+
+int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_level, uint64_t first,
+                        uint64_t n, uint64_t total_n, uint64_t sampling_seed, float* x, float* y,
+                        int threads) {
+  return synth_rows(dims, spec_seed, noise_level, nullptr, first, n, total_n, sampling_seed, x, y, threads);
 }
 
 int ltfb_net_param_count(const ltfb_dims* dims, const ltfb_arch* arch, int net, uint64_t* count) {

@@ -169,6 +169,21 @@ DeviceTrainer::~DeviceTrainer() {
     if (perm_ev_[i]) cudaEventDestroy(perm_ev_[i]);
   }
   for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto e : tmr_)
+    if (e) cudaEventDestroy(e);
+  for (auto& v : kev_)
+    for (auto& pr : v) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  for (int i = 0; i < 2; ++i) {
+    if (h2d_done_[i]) cudaEventDestroy(h2d_done_[i]);
+    if (used_done_[i]) cudaEventDestroy(used_done_[i]);
+  }
+  if (copy_stream_) {
+    cudaStreamSynchronize(copy_stream_);
+    cudaStreamDestroy(copy_stream_);
+  }
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -390,16 +405,95 @@ void DeviceTrainer::start_epoch() {
                             cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaEventRecord(perm_ev_[buf], stream_));
   ltfb_dev::launch_begin_epoch(ctr_.p, epoch_, stream_);
+  ++launches_;
   step_in_epoch_ = 0;
   have_plan_ = true;
 }
 
-void DeviceTrainer::launch_step() {
-  ltfb_dev::launch_gather(args_, stream_);
+void DeviceTrainer::launch_step() { launch_step_kernels(true); }
+
+// kernel ids for per-kernel timing: 0 gather, 1 pre, 2 wide, 3 post
+void DeviceTrainer::kernel_mark(int which, bool begin) {
+  if (!ktime_on_) return;
+  auto& v = kev_[which];
+  auto& used = kev_used_[which];
+  if (begin) {
+    if (used == v.size()) {
+      cudaEvent_t a, b;
+      LTFB_CUDA(cudaEventCreate(&a));
+      LTFB_CUDA(cudaEventCreate(&b));
+      v.push_back({a, b});
+    }
+    LTFB_CUDA(cudaEventRecord(v[used].first, stream_));
+  } else {
+    LTFB_CUDA(cudaEventRecord(v[used].second, stream_));
+    ++used;
+  }
+}
+
+void DeviceTrainer::resolve_kernel_times() {
+  for (int k = 0; k < 4; ++k) {
+    for (std::size_t i = 0; i < kev_used_[k]; ++i) {
+      float ms = 0;
+      LTFB_CUDA(cudaEventElapsedTime(&ms, kev_[k][i].first, kev_[k][i].second));
+      kms_[k] += ms;
+      ++kcount_[k];
+    }
+    kev_used_[k] = 0;
+  }
+}
+
+void DeviceTrainer::launch_step_kernels(bool gather) {
+  if (gather) {
+    kernel_mark(0, true);
+    ltfb_dev::launch_gather(args_, stream_);
+    kernel_mark(0, false);
+  }
+  kernel_mark(1, true);
   ltfb_dev::launch_pre(args_, stream_);
+  kernel_mark(1, false);
+  kernel_mark(2, true);
   if (wide_kind_ == 2) ltfb_dev::launch_wide_tc(args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
+  kernel_mark(2, false);
+  kernel_mark(3, true);
   ltfb_dev::launch_post(args_, stream_);
+  kernel_mark(3, false);
+  launches_ += gather ? 4 : 3;
+}
+
+void DeviceTrainer::timer_start() {
+  DeviceGuard g(spec_.device);
+  for (auto& e : tmr_)
+    if (!e) LTFB_CUDA(cudaEventCreate(&e));
+  LTFB_CUDA(cudaEventRecord(tmr_[0], stream_));
+}
+
+double DeviceTrainer::timer_stop_ms() {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaEventRecord(tmr_[1], stream_));
+  LTFB_CUDA(cudaEventSynchronize(tmr_[1]));
+  float ms = 0;
+  LTFB_CUDA(cudaEventElapsedTime(&ms, tmr_[0], tmr_[1]));
+  return ms;
+}
+
+void DeviceTrainer::set_kernel_timing(bool on) {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  resolve_kernel_times();
+  for (int k = 0; k < 4; ++k) {
+    kms_[k] = 0;
+    kcount_[k] = 0;
+  }
+  ktime_on_ = on;
+}
+
+std::pair<double, std::uint64_t> DeviceTrainer::kernel_time(int which) {
+  DeviceGuard g(spec_.device);
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  resolve_kernel_times();
+  return {kms_[which], kcount_[which]};
 }
 
 void DeviceTrainer::enqueue_steps(std::size_t n) {
@@ -443,7 +537,7 @@ bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepReco
     enqueue_steps(chunk);
     close_epoch_segment(false, false);
     LTFB_CUDA(cudaStreamSynchronize(stream_));
-    // resolve this chunk's segment timings lazily at epoch close
+    if (ktime_on_) resolve_kernel_times();
     std::vector<ltfb_dev::StepRec> recs(chunk);
     const std::size_t at = first % rec_.n;
     const std::size_t n1 = std::min(chunk, rec_.n - at);
@@ -535,6 +629,7 @@ EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int
   e.n_inv = static_cast<long long>(counts_[3]);
   e.ctr = ctr_.p;
   ltfb_dev::launch_eval(e, stream_);
+  launches_ += 3;
   LTFB_CUDA(cudaGetLastError());
   double out[6] = {0, 0, 0, 0, 0, 0};
   LTFB_CUDA(cudaMemcpyAsync(out, eval_out_.p, sizeof(double) * 3 * nc, cudaMemcpyDeviceToHost, stream_));
@@ -567,6 +662,78 @@ void DeviceTrainer::adopt(const float* fwd, const float* inv) {
     LTFB_CUDA(cudaMemsetAsync(mom2_[net].p, 0, counts_[net] * 4, stream_));
   }
   LTFB_CUDA(cudaStreamSynchronize(stream_));
+}
+
+bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float* y,
+                                     std::vector<ltfb::train::StepRecord>& out) {
+  DeviceGuard g(spec_.device);
+  if (n_part_ == 0) throw ContractError("train_steps: data store is empty");
+  const auto& m = margs_;
+  const std::size_t B = spec_.batch_size;
+  if (!copy_stream_) {
+    LTFB_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      hx_[i].alloc(B * m.in);
+      hy_[i].alloc(B * m.out_pad);
+      LTFB_CUDA(cudaMemsetAsync(hy_[i].p, 0, hy_[i].bytes(), copy_stream_));
+      LTFB_CUDA(cudaEventCreateWithFlags(&h2d_done_[i], cudaEventDisableTiming));
+      LTFB_CUDA(cudaEventCreateWithFlags(&used_done_[i], cudaEventDisableTiming));
+      LTFB_CUDA(cudaEventRecord(used_done_[i], stream_));
+    }
+  }
+  ensure_adam_table(t_host_max_ + host_step_ + n + 1);
+  // order the copy stream after everything already on the compute stream
+  LTFB_CUDA(cudaEventRecord(used_done_[0], stream_));
+  LTFB_CUDA(cudaEventRecord(used_done_[1], stream_));
+  float* keep_x = args_.xb;
+  float* keep_y = args_.yb;
+  for (std::size_t i = 0; i < n; ++i) {
+    if (!have_plan_ || step_in_epoch_ >= steps_per_epoch_) start_epoch();
+    const int b = static_cast<int>(i & 1);
+    // H2D of this step's minibatch on the copy stream, after the step that
+    // last used this buffer has finished with it
+    LTFB_CUDA(cudaStreamWaitEvent(copy_stream_, used_done_[b], 0));
+    LTFB_CUDA(cudaMemcpyAsync(hx_[b].p, x + i * B * m.in, B * m.in * 4, cudaMemcpyHostToDevice, copy_stream_));
+    LTFB_CUDA(cudaMemcpy2DAsync(hy_[b].p, m.out_pad * 4, y + i * B * m.out, m.out * 4, m.out * 4, B,
+                                cudaMemcpyHostToDevice, copy_stream_));
+    LTFB_CUDA(cudaEventRecord(h2d_done_[b], copy_stream_));
+    LTFB_CUDA(cudaStreamWaitEvent(stream_, h2d_done_[b], 0));
+    args_.xb = hx_[b].p;
+    args_.yb = hy_[b].p;
+    launch_step_kernels(false);
+    LTFB_CUDA(cudaEventRecord(used_done_[b], stream_));
+    ++step_in_epoch_;
+    ++epoch_steps_;
+    ++host_step_;
+  }
+  args_.xb = keep_x;
+  args_.yb = keep_y;
+  LTFB_CUDA(cudaGetLastError());
+  std::vector<ltfb_dev::StepRec> recs(n);
+  const std::uint64_t first = host_step_ - n;
+  for (std::size_t i = 0; i < n; ++i)  // D2H of every step's record
+    LTFB_CUDA(cudaMemcpyAsync(&recs[i], rec_.p + (first + i) % rec_.n, sizeof(ltfb_dev::StepRec),
+                              cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  bool ok = true;
+  for (const auto& r : recs) {
+    ltfb::train::StepRecord s;
+    s.trainer = spec_.trainer_id;
+    s.step = r.step;
+    s.epoch = r.epoch;
+    s.d_loss = r.d_loss;
+    s.g_total = r.g_total;
+    s.g_fwd = r.g_fwd;
+    s.g_adv = r.g_adv;
+    s.g_cyc = r.g_cyc;
+    s.skipped = (r.flags & 1u) != 0;
+    out.push_back(s);
+    if (r.flags & 8u) {
+      ok = false;
+      break;
+    }
+  }
+  return ok;
 }
 
 double DeviceTrainer::ae_step(const std::uint32_t*, std::size_t) {

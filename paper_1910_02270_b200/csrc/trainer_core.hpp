@@ -145,9 +145,23 @@ class DeviceTrainer {
 
   // exposed for benchmarks: launches one step without reading back
   void enqueue_steps(std::size_t n);
+  /// Device-event timer on this trainer's stream (bench.py timed region).
+  void timer_start();
+  double timer_stop_ms();
+  /// When on, every wide-pass launch is bracketed by CUDA events on the
+  /// launching stream; kernel_time() returns (total ms, launches).
+  void set_kernel_timing(bool on);
+  std::pair<double, std::uint64_t> kernel_time(int which);
+  /// e2e path: n steps whose minibatches come from HOST memory (x [n x B x
+  /// in], y [n x B x out], rows per step = B); each step's batch is copied
+  /// H2D inside the call (double-buffered on a copy stream) and its record
+  /// read back D2H.
+  bool train_steps_host(std::size_t n, const float* x, const float* y,
+                        std::vector<ltfb::train::StepRecord>& out);
   std::size_t wide_ctas() const { return S_; }
   const ltfb_dev::StepArgs& step_args() const { return args_; }
   int wide_kernel_kind() const { return wide_kind_; }
+  std::uint64_t launch_count() const { return launches_; }
 
  private:
   void build_model_args();
@@ -155,6 +169,7 @@ class DeviceTrainer {
   void start_epoch();
   void launch_step();
   void close_epoch_segment(bool epoch_done, bool partial);
+  void launch_step_kernels(bool gather);
 
   TrainerSpec spec_;
   ltfb::nn::MlpSpec specs_[5];
@@ -165,6 +180,7 @@ class DeviceTrainer {
   int sm_count_ = 148;
   std::size_t S_ = 0;
   int wide_kind_ = 1;
+  std::uint64_t launches_ = 0;
 
   DevBuf<float> params_[5], mom1_[5], mom2_[5], grads_[5];
   DevBuf<float> gen_;       // [fwd | inv] contiguous (exchange payload)
@@ -209,6 +225,20 @@ class DeviceTrainer {
   DevBuf<float> eval_h_;
   DevBuf<double> eval_inv_, eval_part_, eval_out_;
   std::size_t eval_S_ = 0;
+
+  // timing
+  cudaEvent_t tmr_[2] = {nullptr, nullptr};
+  bool ktime_on_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev_[4];
+  std::size_t kev_used_[4] = {0, 0, 0, 0};
+  double kms_[4] = {0, 0, 0, 0};
+  std::uint64_t kcount_[4] = {0, 0, 0, 0};
+  void kernel_mark(int which, bool begin);
+  void resolve_kernel_times();
+  // e2e streaming
+  cudaStream_t copy_stream_ = nullptr;
+  DevBuf<float> hx_[2], hy_[2];
+  cudaEvent_t h2d_done_[2] = {nullptr, nullptr}, used_done_[2] = {nullptr, nullptr};
 
   // AE
   DevBuf<float> ae_y_;

@@ -291,7 +291,7 @@ def main():
     clocks = sampler.stop()
     barrier()
     launches = tr.launch_count() - warm_launch
-    kt = {name: tr.kernel_time(i) for i, name in enumerate(("gather", "small_fwd", "wide", "post"))}
+    kt = {name: tr.kernel_time(i) for i, name in enumerate(("gather", "small_fwd", "wide", "post", "reduce"))}
     tr.kernel_timing(False)
     ms_max = max_over_ranks(ms)
     value = k * B * args.steps / (ms_max / 1e3)
@@ -332,6 +332,7 @@ def main():
         "wide": (B * out + out * E1 + D * out + out) * 4,
         "small_fwd": 0,
         "post": 0,
+        "reduce": 0,
     }
     shares = {n: v[0] for n, v in kt.items()}
     dom = max(("gather", "wide"), key=lambda n: shares[n])

@@ -392,7 +392,7 @@ int ltfb_trainer_kernel_timing(ltfb_trainer* t, int on) {
 }
 int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* launches) {
   return guarded([&] {
-    if (which < 0 || which > 3) throw ltfb::ContractError("bad kernel index");
+    if (which < 0 || which > 4) throw ltfb::ContractError("bad kernel index");
     const auto r = T(t).kernel_time(which);
     *ms = r.first;
     *launches = r.second;

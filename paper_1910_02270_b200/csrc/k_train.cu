@@ -170,236 +170,6 @@ __global__ void __launch_bounds__(256) k_wide_generic(StepArgs a) {
 
 template __global__ void k_wide_generic<32, 32>(StepArgs);
 
-// ------------------------------------------------------------------- Adam --
-// nn/adam.hpp:48-61 in double with explicit round-to-nearest operations so
-// nothing is contracted into an FMA: with identical inputs the update is
-// bit-identical to the reference's scalar loop.
-__device__ __forceinline__ void adam_elem(float& p, float g, float& m1, float& m2, double lr,
-                                          double b1, double b2, double eps, double c1, double c2) {
-  const double gd = (double)g;
-  const double mi = __dadd_rn(__dmul_rn(b1, (double)m1), __dmul_rn(1.0 - b1, gd));
-  const double vi = __dadd_rn(__dmul_rn(b2, (double)m2), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-  m1 = (float)mi;
-  m2 = (float)vi;
-  const double upd = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps));
-  p = (float)__dsub_rn((double)p, upd);
-}
-
-template <class Sync>
-__device__ void adam_net(const StepArgs& a, int net, long long n, Sync sync) {
-  const unsigned long long t = a.ctr->t[net] + 1;
-  const double c1 = a.adam_c[2 * t], c2 = a.adam_c[2 * t + 1];
-  float* p = a.p[net];
-  const float* g = a.g[net];
-  float* m1 = a.mom1[net];
-  float* m2 = a.mom2[net];
-  for (long long i = sync.rank(); i < n; i += sync.size())
-    adam_elem(p[i], g[i], m1[i], m2[i], a.lr[net], a.b1, a.b2, a.eps, c1, c2);
-}
-
-__device__ bool all_finite_blk(const float* v, long long n) {
-  int ok = 1;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) ok &= isfinite(v[i]) ? 1 : 0;
-  return __syncthreads_and(ok) != 0;
-}
-
-// ------------------------------------------------------------------- post --
-__global__ void __launch_bounds__(512) k_post(StepArgs a) {
-  __shared__ double red[512];
-  Counters* ctr = a.ctr;
-  if (ctr->aborted) return;
-  const ModelArgs& m = a.m;
-  const int rows = batch_rows(a);
-  const ScratchLayout L = make_scratch_layout(m, a.B);
-  float* sc = a.scratch;
-  const BlockSync sync{};
-  const int tid = threadIdx.x, nth = blockDim.x;
-  float* fz[kMaxLayers]; float* fa[kMaxLayers];
-  float* hz[kMaxLayers]; float* ha[kMaxLayers];
-  float* ez[kMaxLayers]; float* ea[kMaxLayers];
-  float* cz[kMaxLayers]; float* ca[kMaxLayers];
-  float* iz[kMaxLayers]; float* ia[kMaxLayers];
-  for (int l = 0; l < kMaxLayers; ++l) {
-    fz[l] = sc + L.fz[l]; fa[l] = sc + L.fa[l];
-    hz[l] = sc + L.hz[l]; ha[l] = sc + L.ha[l];
-    ez[l] = sc + L.ez[l]; ea[l] = sc + L.ea[l];
-    cz[l] = sc + L.cz[l]; ca[l] = sc + L.ca[l];
-    iz[l] = sc + L.iz[l]; ia[l] = sc + L.ia[l];
-  }
-  float* tA = sc + L.tA;
-  float* tB = sc + L.tB;
-  const float* latent = fa[m.fwd.L - 1];
-  const int lat = m.lat, E1 = m.E1, D = m.D;
-
-  // ---- enc wide layer: split-K reduction + bias + activation, enc tail ----
-  float* e1z = sc + L.e1z;
-  float* e1a = sc + L.e1a;
-  const float* be = a.p[kEnc] + m.enc_wide_b;
-  for (int i = tid; i < rows * E1; i += nth) {
-    const int r = i / E1, j = i - r * E1;
-    float acc = 0.0f;
-    for (int s = 0; s < a.S; ++s) acc += a.P_enc[((long long)s * a.B + r) * E1 + j];
-    const float z = acc + be[j];
-    e1z[i] = z;
-    e1a[i] = act_apply(m.enc_act0, m.enc_slope0, z);
-  }
-  sync();
-  const float* real = e1a;
-  if (m.enc_tail.L > 0) {
-    mlp_forward(m.enc_tail, a.p[kEnc], e1a, E1, rows, (float* const*)nullptr, ea, sync);
-    real = ea[m.enc_tail.L - 1];
-  }
-  float* stacked = sc + L.stacked;
-  for (int i = tid; i < rows * lat; i += nth) {
-    stacked[i] = real[i];
-    stacked[rows * lat + i] = latent[i];
-  }
-  // ---- dec path gradient: grad wrt h, then dec head backward ----
-  const long long n_fwd = (long long)rows * m.out;
-  const float gscale = (float)(1.0 / (double)n_fwd);
-  float* gh = sc + L.gh;
-  for (int i = tid; i < rows * D; i += nth) {
-    const int r = i / D, j = i - r * D;
-    float acc = 0.0f;
-    for (int s = 0; s < a.S; ++s) acc += a.P_dec[((long long)s * a.B + r) * D + j];
-    gh[i] = gscale * acc;
-  }
-  sync();
-  float* gl_dec = sc + L.gl_dec;
-  if (m.dec_head.L > 0) {
-    mlp_backward(m.dec_head, a.p[kDec], latent, lat, rows, hz, ha, gh, (float*)nullptr, gl_dec, tA,
-                 tB, sync);
-  } else {
-    for (int i = tid; i < rows * lat; i += nth) gl_dec[i] = gh[i];
-  }
-  double fwd_sum = 0.0;
-  if (tid == 0)
-    for (int s = 0; s < a.S; ++s) fwd_sum += a.mae_part[s];
-  const double fwd_mae = fwd_sum / (double)n_fwd;  // valid on thread 0
-  sync();
-
-  // ---- discriminator step (train_ops.hpp:155-186, trainer.hpp:208-229) ----
-  const int n2 = 2 * rows;
-  mlp_forward(m.disc, a.p[kDisc], stacked, lat, n2, cz, ca, sync);
-  float* probs = sc + L.probs;
-  float* bgrad = sc + L.bgrad;
-  const float* logit = ca[m.disc.L - 1];
-  double part = 0.0;
-  for (int i = tid; i < n2; i += nth) {
-    const float p = stable_sigmoid(logit[i]);
-    probs[i] = p;
-    const double y = i < rows ? 1.0 : 0.0;
-    double pc = (double)p;
-    pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
-    part += y != 0.0 ? -log(pc) : -log(1.0 - pc);
-    bgrad[i] = (float)((pc - y) / (double)n2);
-  }
-  const double d_raw = block_sum_det(part, red) / (double)n2;
-  const double d_loss = ((double)rows * d_raw) / (double)rows;  // allreduce.hpp:62-75
-  mlp_backward(m.disc, a.p[kDisc], stacked, lat, n2, cz, ca, bgrad, a.g[kDisc], (float*)nullptr, tA,
-               tB, sync);
-  const long long n_disc = m.disc.count;
-  const bool d_ok = isfinite(d_loss) && all_finite_blk(a.g[kDisc], n_disc);
-  if (d_ok) {
-    adam_net(a, kDisc, n_disc, sync);
-  }
-  sync();
-
-  // ---- generator step (train_ops.hpp:88-151, trainer.hpp:231-272) ----
-  bool g_ok = false;
-  double g_total = 0, g_adv = 0, g_cyc = 0;
-  if (d_ok) {
-    // adversarial path against the just-updated discriminator
-    mlp_forward(m.disc, a.p[kDisc], latent, lat, rows, cz, ca, sync);
-    const float* lg = ca[m.disc.L - 1];
-    double ap = 0.0;
-    for (int i = tid; i < rows; i += nth) {
-      double pc = (double)stable_sigmoid(lg[i]);
-      pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
-      ap += -log(pc);
-      bgrad[i] = (float)((pc - 1.0) / (double)rows) * m.lambda_adv;
-    }
-    const double adv = block_sum_det(ap, red) / (double)rows;
-    float* gl_disc = sc + L.gl_disc;
-    mlp_backward(m.disc, a.p[kDisc], latent, lat, rows, cz, ca, bgrad, (float*)nullptr, gl_disc, tA,
-                 tB, sync);
-    // cycle path
-    mlp_forward(m.inv, a.p[kInv], latent, lat, rows, iz, ia, sync);
-    const float* rec = ia[m.inv.L - 1];
-    float* ig = sc + L.igrad;
-    const long long n_cyc = (long long)rows * m.in;
-    double cp = 0.0;
-    const float pos = (float)(1.0 / (double)n_cyc), neg = (float)(-1.0 / (double)n_cyc);
-    for (int i = tid; i < n_cyc; i += nth) {
-      const double d = (double)rec[i] - (double)a.xb[i];
-      cp += fabs(d);
-      ig[i] = (d > 0 ? pos : (d < 0 ? neg : 0.0f)) * m.lambda_cyc;
-    }
-    const double cyc = block_sum_det(cp, red) / (double)n_cyc;
-    float* gl_inv = sc + L.gl_inv;
-    mlp_backward(m.inv, a.p[kInv], latent, lat, rows, iz, ia, ig, a.g[kInv], gl_inv, tA, tB, sync);
-    float* gl = sc + L.gl;
-    for (int i = tid; i < rows * lat; i += nth) gl[i] = (gl_dec[i] + gl_disc[i]) + gl_inv[i];
-    sync();
-    mlp_backward(m.fwd, a.p[kFwd], a.xb, m.in, rows, fz, fa, gl, a.g[kFwd], (float*)nullptr, tA,
-                 tB, sync);
-    // thread 0 holds fwd_mae; broadcast through red[0]
-    if (tid == 0) red[0] = fwd_mae;
-    sync();
-    const double fm = red[0];
-    sync();
-    const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
-    g_total = ((double)rows * total_raw) / (double)rows;
-    g_adv = ((double)rows * adv) / (double)rows;
-    g_cyc = ((double)rows * cyc) / (double)rows;
-    if (isfinite(g_total)) {
-      const bool fwd_ok = all_finite_blk(a.g[kFwd], m.fwd.count);
-      if (fwd_ok) {
-        adam_net(a, kFwd, m.fwd.count, sync);
-        const bool inv_ok = all_finite_blk(a.g[kInv], m.inv.count);
-        if (inv_ok) {
-          adam_net(a, kInv, m.inv.count, sync);
-          g_ok = true;
-        }
-        sync();
-        if (tid == 0) {
-          ctr->t[kFwd] += 1;
-          if (inv_ok) ctr->t[kInv] += 1;
-        }
-      }
-    }
-    if (tid == 0) {
-      red[1] = fm;
-    }
-  }
-  sync();
-  if (tid == 0) {
-    if (d_ok) ctr->t[kDisc] += 1;
-    const bool skipped = !(d_ok && g_ok);
-    StepRec r{};
-    r.d_loss = d_ok ? d_loss : 0.0;
-    if (g_ok) {
-      r.g_total = g_total;
-      r.g_fwd = ((double)rows * red[1]) / (double)rows;
-      r.g_adv = g_adv;
-      r.g_cyc = g_cyc;
-    }
-    ctr->global_step += 1;
-    ctr->step_in_epoch += 1;
-    r.step = ctr->global_step;
-    r.epoch = ctr->epoch;
-    r.flags = (skipped ? 1u : 0u) | (d_ok ? 2u : 0u) | (g_ok ? 4u : 0u);
-    if (skipped) {
-      ctr->skipped += 1;
-      if ((long long)ctr->skipped > (long long)a.abort_threshold) {
-        ctr->aborted = 1;
-        r.flags |= 8u;
-      }
-    }
-    a.rec[(ctr->global_step - 1) % (unsigned long long)a.rec_cap] = r;
-  }
-}
-
 // -------------------------------------------------------- epoch control --
 __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
   ctr->epoch = epoch;
@@ -435,7 +205,6 @@ void launch_wide_generic(const StepArgs& a, cudaStream_t s) {
   k_wide_generic<32, 32><<<a.S, 256, smem, s>>>(a);
 }
 
-void launch_post(const StepArgs& a, cudaStream_t s) { k_post<<<1, 512, 0, s>>>(a); }
 
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s) {
   k_begin_epoch<<<1, 1, 0, s>>>(ctr, epoch);

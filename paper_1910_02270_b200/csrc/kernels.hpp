@@ -13,6 +13,7 @@ void launch_pre(const StepArgs& a, cudaStream_t s);
 void launch_wide_generic(const StepArgs& a, cudaStream_t s);
 bool wide_tc_supported(const StepArgs& a);
 void launch_wide_tc(const StepArgs& a, cudaStream_t s);
+void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 

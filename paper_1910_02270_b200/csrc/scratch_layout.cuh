@@ -19,9 +19,15 @@ struct ScratchLayout {
   long long gh;                              // [B x D]
   long long gl_dec, gl_disc, gl_inv, gl;     // [B x lat]
   long long igrad;                           // [B x in]
-  long long tA, tB;                          // [2B x maxw]
+  long long tA, tB;                          // per post CTA: [2 ceil(B/C) x maxw]
+  long long tstride;                         // floats per post CTA in tA / tB
+  long long red_enc, red_dec;                // reduced wide-pass sums [B x E1], [B x D]
+  long long pg_disc, pg_fwd, pg_inv;         // per post CTA partial gradients
   long long total;
 };
+
+constexpr int kPostCluster = 8;   // CTAs of the post kernel (one cluster)
+constexpr int kPostThreads = 256;
 
 __host__ __device__ inline long long round_up_ll(long long v, long long a) { return (v + a - 1) / a * a; }
 
@@ -61,8 +67,15 @@ __host__ __device__ inline ScratchLayout make_scratch_layout(const ModelArgs& m,
   for (const NetDesc* n : nets) mw = n->max_w() > mw ? n->max_w() : mw;
   mw = m.E1 > mw ? m.E1 : mw;
   mw = m.D > mw ? m.D : mw;
-  s.tA = take(2LL * B * mw);
-  s.tB = take(2LL * B * mw);
+  const long long per = (B + kPostCluster - 1) / kPostCluster;
+  s.tstride = round_up_ll(2 * per * mw, 32);
+  s.tA = take(s.tstride * kPostCluster);
+  s.tB = take(s.tstride * kPostCluster);
+  s.red_enc = take((long long)B * m.E1);
+  s.red_dec = take((long long)B * m.D);
+  s.pg_disc = take(kPostCluster * round_up_ll(m.disc.count, 32));
+  s.pg_fwd = take(kPostCluster * round_up_ll(m.fwd.count, 32));
+  s.pg_inv = take(kPostCluster * round_up_ll(m.inv.count, 32));
   s.total = at;
   return s;
 }

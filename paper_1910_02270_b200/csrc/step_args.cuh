@@ -47,6 +47,7 @@ struct StepArgs {
   float* P_enc;     // [S x B x E1]
   float* P_dec;     // [S x B x D]
   double* mae_part; // [S]
+  double* mae_total; // [1] reduced forward-MAE sum
   float* scratch;   // small-network tapes
   Counters* ctr;
   StepRec* rec;

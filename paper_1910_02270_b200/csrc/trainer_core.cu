@@ -116,6 +116,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   pe_.alloc(S_ * B * ma.E1);
   pd_.alloc(S_ * B * ma.D);
   mae_part_.alloc(S_);
+  mae_total_.alloc(1);
   const auto lay = ltfb_dev::make_scratch_layout(ma, B);
   scratch_.alloc(static_cast<std::size_t>(lay.total));
   ctr_.alloc(1);
@@ -148,6 +149,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.P_enc = pe_.p;
   a.P_dec = pd_.p;
   a.mae_part = mae_part_.p;
+  a.mae_total = mae_total_.p;
   a.scratch = scratch_.p;
   a.h = scratch_.p + (margs_.dec_head.L > 0 ? lay.ha[margs_.dec_head.L - 1] : lay.fa[margs_.fwd.L - 1]);
   a.ctr = ctr_.p;
@@ -412,7 +414,7 @@ void DeviceTrainer::start_epoch() {
 
 void DeviceTrainer::launch_step() { launch_step_kernels(true); }
 
-// kernel ids for per-kernel timing: 0 gather, 1 pre, 2 wide, 3 post
+// kernel ids for per-kernel timing: 0 gather, 1 pre, 2 wide, 3 post, 4 reduce
 void DeviceTrainer::kernel_mark(int which, bool begin) {
   if (!ktime_on_) return;
   auto& v = kev_[which];
@@ -432,7 +434,7 @@ void DeviceTrainer::kernel_mark(int which, bool begin) {
 }
 
 void DeviceTrainer::resolve_kernel_times() {
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < kTimed; ++k) {
     for (std::size_t i = 0; i < kev_used_[k]; ++i) {
       float ms = 0;
       LTFB_CUDA(cudaEventElapsedTime(&ms, kev_[k][i].first, kev_[k][i].second));
@@ -456,10 +458,13 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
   if (wide_kind_ == 2) ltfb_dev::launch_wide_tc(args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
   kernel_mark(2, false);
+  kernel_mark(4, true);
+  ltfb_dev::launch_reduce(args_, stream_);
+  kernel_mark(4, false);
   kernel_mark(3, true);
   ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
-  launches_ += gather ? 4 : 3;
+  launches_ += gather ? 5 : 4;
 }
 
 void DeviceTrainer::timer_start() {
@@ -482,7 +487,7 @@ void DeviceTrainer::set_kernel_timing(bool on) {
   DeviceGuard g(spec_.device);
   LTFB_CUDA(cudaStreamSynchronize(stream_));
   resolve_kernel_times();
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < kTimed; ++k) {
     kms_[k] = 0;
     kcount_[k] = 0;
   }

@@ -188,7 +188,7 @@ class DeviceTrainer {
   DevBuf<float> sx_, sy_;
   DevBuf<unsigned> perm_[2];
   DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
-  DevBuf<double> mae_part_, adam_c_;
+  DevBuf<double> mae_part_, mae_total_, adam_c_;
   DevBuf<ltfb_dev::Counters> ctr_;
   DevBuf<ltfb_dev::StepRec> rec_;
   std::uint64_t adam_cap_ = 0;
@@ -229,10 +229,11 @@ class DeviceTrainer {
   // timing
   cudaEvent_t tmr_[2] = {nullptr, nullptr};
   bool ktime_on_ = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev_[4];
-  std::size_t kev_used_[4] = {0, 0, 0, 0};
-  double kms_[4] = {0, 0, 0, 0};
-  std::uint64_t kcount_[4] = {0, 0, 0, 0};
+  static constexpr int kTimed = 5;  // gather, small fwd, wide, post, reduce
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev_[kTimed];
+  std::size_t kev_used_[kTimed] = {};
+  double kms_[kTimed] = {};
+  std::uint64_t kcount_[kTimed] = {};
   void kernel_mark(int which, bool begin);
   void resolve_kernel_times();
   // e2e streaming

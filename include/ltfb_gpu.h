@@ -188,6 +188,13 @@ int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
 /* Number of kernels this trainer has launched so far (all of them ours). */
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches);
 
+/* Diagnostic: runs the three tcgen05 MMA shapes of the wide pass on the
+ * current device (host buffers): a1 [128x32], b1 [32x64], ah [128x64],
+ * b2 [64x32], a3 [128x32] -> d1 = a1 b1 [128x64], d2 = ah b2 [128x32],
+ * d3 = a3 b2^T [128x64] (kind::tf32 inputs, f32 accumulation). */
+int ltfb_selftest_tcgen05(const float* a1, const float* b1, const float* ah, const float* b2, const float* a3,
+                          float* d1, float* d2, float* d3);
+
 /* ---- multi-GPU: one trainer per GPU, NCCL point-to-point exchange ------- */
 int ltfb_nccl_available(void);
 int ltfb_nccl_unique_id(uint8_t id[128]);

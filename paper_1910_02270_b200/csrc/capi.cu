@@ -7,6 +7,7 @@
 #include <thread>
 
 #include "ltfb_b200/host_algos.hpp"
+#include "kernels.hpp"
 #include "ltfb_gpu.h"
 #include "trainer_core.hpp"
 
@@ -408,6 +409,30 @@ int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas) 
 
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches) {
   return guarded([&] { *launches = T(const_cast<ltfb_trainer*>(t)).launch_count(); });
+}
+
+int ltfb_selftest_tcgen05(const float* a1, const float* b1, const float* ah, const float* b2, const float* a3,
+                          float* d1, float* d2, float* d3) {
+  return guarded([&] {
+    const std::size_t n_in[5] = {128 * 32, 32 * 64, 128 * 64, 64 * 32, 128 * 32};
+    const float* in[5] = {a1, b1, ah, b2, a3};
+    const std::size_t n_out[3] = {128 * 64, 128 * 32, 128 * 64};
+    float* outp[3] = {d1, d2, d3};
+    float* din[5];
+    float* dout[3];
+    for (int i = 0; i < 5; ++i) {
+      LTFB_CUDA(cudaMalloc(&din[i], n_in[i] * 4));
+      LTFB_CUDA(cudaMemcpy(din[i], in[i], n_in[i] * 4, cudaMemcpyHostToDevice));
+    }
+    for (int i = 0; i < 3; ++i) LTFB_CUDA(cudaMalloc(&dout[i], n_out[i] * 4));
+    const cudaError_t e = ltfb_dev::selftest_tc(din[0], din[1], din[2], din[3], din[4], dout[0], dout[1], dout[2]);
+    for (int i = 0; i < 3; ++i) {
+      if (e == cudaSuccess) LTFB_CUDA(cudaMemcpy(outp[i], dout[i], n_out[i] * 4, cudaMemcpyDeviceToHost));
+      cudaFree(dout[i]);
+    }
+    for (int i = 0; i < 5; ++i) cudaFree(din[i]);
+    LTFB_CUDA(e);
+  });
 }
 
 int ltfb_nccl_available(void) { return nccl().ok ? 1 : 0; }

@@ -1,11 +1,427 @@
-// tcgen05 wide pass (placeholder until the tensor-core kernel lands).
+// The wide pass of a training step on the 5th-gen tensor cores (sm_100a).
+//
+// One persistent CTA per SM walks 32-column tiles c0 = 32 t of the output
+// dimension (49,167 at paper scale). Per tile, with Y = the minibatch's
+// output rows [128 x 32], the frozen weights We (enc layer 0, [out x 64])
+// and Wd (dec last layer, [64 x out]) and h = dec-head activations
+// [128 x 64] (in TMEM for the whole kernel):
+//
+//   MMA1  P_enc += Y  We[c0:c0+32, :]         (enc layer-0 split-K partial:
+//                                              D-step real latents,
+//                                              train_ops.hpp:160)
+//   MMA2  O      = h  Wd[:, c0:c0+32]         (dec forward, train_ops.hpp:100)
+//   epi   d = O + b - Y ; sum |d| (f64) ; S = sign(d)     (loss.hpp:25-41)
+//   MMA3  P_dec += S  Wd[:, c0:c0+32]^T        (dL/dh up to 1/n,
+//                                              mlp.hpp:278; dW/db of the
+//                                              frozen decoder never formed)
+//
+// Parity ("3xTF32") mode splits every fp32 operand into hi + lo tf32 parts
+// and accumulates hi*hi + lo*hi + hi*lo in f32 TMEM (S is exact in tf32, so
+// MMA3 needs only S*hi + S*lo). Frozen weights are split once into
+// K-major copies (WeT, Wd, WdT; tf32 MN-major operands would need the
+// 32B-atom swizzle); Y is split per tile in shared memory.
+//
+// Warp roles (320 threads): w0 TMA producer, w1 MMA issuer + TMEM owner,
+// w2-5 epilogue (TMEM lane quadrants 2,3,0,1), w6-9 Y hi/lo split.
+// Pipelines: 2 smem stages (full / split / sready / empty mbarriers),
+// 2 TMEM O buffers (ofull / oempty). Each CTA writes one [128 x 64] partial
+// of P_enc and P_dec and one f64 |d| sum; k_reduce sums them in fixed order.
+#include <cuda.h>
+
+#include <cstring>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.hpp"
+#include "tc_ptx.cuh"
 
 namespace ltfb_dev {
 
-bool wide_tc_supported(const StepArgs&) { return false; }
-void launch_wide_tc(const StepArgs&, cudaStream_t) { throw std::runtime_error("tcgen05 wide kernel unavailable"); }
+namespace wt {
+constexpr int kTileN = 32;                 // output columns per tile
+constexpr int kRows = 128;                 // MMA M (minibatch rows)
+constexpr int kW = 64;                     // E1 == D == 64
+constexpr uint32_t kY = 16384;             // [128 x 32] f32
+constexpr uint32_t kWt = 8192;             // [64 x 32] f32
+constexpr uint32_t kStage = 2 * kY + 6 * kWt;  // Y, Ylo/S, WeT hi/lo, Wd hi/lo, WdT hi/lo
+constexpr int kStages = 2;
+constexpr uint32_t kSmem = kStages * kStage + 1024;
+constexpr int kThreads = 320;
+// TMEM columns
+constexpr uint32_t kPenc = 0, kPdec = 64, kO0 = 128, kHhi = 192, kHlo = 256;
+}  // namespace wt
+
+struct WideTcParams {
+  CUtensorMap tm_y, tm_wet_hi, tm_wet_lo, tm_wd_hi, tm_wd_lo, tm_wdt_hi, tm_wdt_lo;
+};
+
+template <bool kPrecise>
+__global__ void __launch_bounds__(wt::kThreads, 1)
+    k_wide_tc(const __grid_constant__ WideTcParams tp, StepArgs a, const float* __restrict__ bias_pad) {
+  using namespace wt;
+  if (a.ctr->aborted) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kStages], split_done[kStages], sready[kStages], empty[kStages];
+  __shared__ uint64_t ofull[2], oempty[2], h_ready, done;
+  __shared__ uint32_t tmem_base;
+  __shared__ double red[128];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows = min(a.B, a.n_part - (int)a.ctr->step_in_epoch * a.B);
+  const int out = a.m.out;
+  const int ntiles = (out + kTileN - 1) / kTileN;
+  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  auto stage_ptr = [&](int s) { return sm + s * kStage; };
+  // stage layout
+  auto Yp = [&](int s) { return stage_ptr(s); };
+  auto Ylo = [&](int s) { return stage_ptr(s) + kY; };
+  auto WeH = [&](int s) { return stage_ptr(s) + 2 * kY; };
+  auto WeL = [&](int s) { return stage_ptr(s) + 2 * kY + kWt; };
+  auto WdH = [&](int s) { return stage_ptr(s) + 2 * kY + 2 * kWt; };
+  auto WdL = [&](int s) { return stage_ptr(s) + 2 * kY + 3 * kWt; };
+  auto WtH = [&](int s) { return stage_ptr(s) + 2 * kY + 4 * kWt; };
+  auto WtL = [&](int s) { return stage_ptr(s) + 2 * kY + 5 * kWt; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&split_done[s], 128);
+      tc::mbar_init(&sready[s], 128);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&ofull[b], 1);
+      tc::mbar_init(&oempty[b], 128);
+    }
+    tc::mbar_init(&h_ready, 128);
+    tc::mbar_init(&done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tp.tm_y);
+    tc::tma_prefetch(&tp.tm_wet_hi);
+    tc::tma_prefetch(&tp.tm_wd_hi);
+    tc::tma_prefetch(&tp.tm_wdt_hi);
+  }
+  if (warp == 1) tc::tmem_alloc<512>(&tmem_base);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t T = tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      const uint32_t bytes = kPrecise ? (kY + 6 * kWt) : (kY + 3 * kWt);
+      for (int i = 0; i < my_tiles; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+        if (i >= kStages) tc::mbar_wait(&empty[s], ph ^ 1u);
+        const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+        tc::mbar_expect_tx(&full[s], bytes);
+        tc::tma_load_2d(Yp(s), &tp.tm_y, &full[s], c0, 0);
+        tc::tma_load_2d(WeH(s), &tp.tm_wet_hi, &full[s], c0, 0);
+        tc::tma_load_2d(WdH(s), &tp.tm_wd_hi, &full[s], c0, 0);
+        tc::tma_load_2d(WtH(s), &tp.tm_wdt_hi, &full[s], 0, c0);
+        tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt_hi, &full[s], 32, c0);
+        if (kPrecise) {
+          tc::tma_load_2d(WeL(s), &tp.tm_wet_lo, &full[s], c0, 0);
+          tc::tma_load_2d(WdL(s), &tp.tm_wd_lo, &full[s], c0, 0);
+          tc::tma_load_2d(WtL(s), &tp.tm_wdt_lo, &full[s], 0, c0);
+          tc::tma_load_2d(WtL(s) + 4096, &tp.tm_wdt_lo, &full[s], 32, c0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      const uint32_t i_enc = tc::idesc_tf32(128, 64, 0, 0);
+      const uint32_t i_dec = tc::idesc_tf32(128, 32, 0, 0);
+      tc::mbar_wait(&h_ready, 0);
+      tc::tc_fence_after();
+      auto mma3 = [&](int j) {
+        const int s = j % kStages;
+        const uint32_t ph = (uint32_t)(j / kStages) & 1u;
+        tc::mbar_wait(&sready[s], ph);
+        tc::tc_fence_after();
+        const uint32_t sA = tc::smem_u32(Ylo(s));  // S overwrote Ylo
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = tc::sdesc_sw128(sA + 32 * kk, 16, 1024);
+          tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdH(s)) + 32 * kk, 16, 1024), i_enc,
+                          (j > 0 || kk > 0) ? 1u : 0u);
+          if (kPrecise)
+            tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdL(s)) + 32 * kk, 16, 1024), i_enc, 1u);
+        }
+        tc::tc_commit(&empty[s]);
+      };
+      for (int i = 0; i < my_tiles; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+        const int b = i & 1;
+        const uint32_t phb = (uint32_t)(i >> 1) & 1u;
+        tc::mbar_wait(&split_done[s], ph);
+        tc::tc_fence_after();
+        if (i >= 2) {
+          tc::mbar_wait(&oempty[b], phb ^ 1u);
+          tc::tc_fence_after();
+        }
+        const uint32_t yh = tc::smem_u32(Yp(s)), yl = tc::smem_u32(Ylo(s));
+        const uint32_t weh = tc::smem_u32(WeH(s)), wel = tc::smem_u32(WeL(s));
+        for (int kk = 0; kk < 4; ++kk) {  // MMA1: P_enc += Y We
+          const uint64_t ah = tc::sdesc_sw128(yh + 32 * kk, 16, 1024);
+          const uint64_t bh = tc::sdesc_sw128(weh + 32 * kk, 16, 1024);
+          tc::mma_tf32_ss(T + kPenc, ah, bh, i_enc, (i > 0 || kk > 0) ? 1u : 0u);
+          if (kPrecise) {
+            tc::mma_tf32_ss(T + kPenc, tc::sdesc_sw128(yl + 32 * kk, 16, 1024), bh, i_enc, 1u);
+            tc::mma_tf32_ss(T + kPenc, ah, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc, 1u);
+          }
+        }
+        const uint32_t Od = T + kO0 + 32u * (uint32_t)b;
+        const uint32_t wth = tc::smem_u32(WtH(s)), wtl = tc::smem_u32(WtL(s));
+        for (int kk = 0; kk < 8; ++kk) {  // MMA2: O = h Wd
+          const uint32_t boff = (kk / 4) * 4096 + 32 * (kk % 4);
+          const uint64_t bh = tc::sdesc_sw128(wth + boff, 16, 1024);
+          tc::mma_tf32_ts(Od, T + kHhi + 8 * kk, bh, i_dec, kk > 0 ? 1u : 0u);
+          if (kPrecise) {
+            tc::mma_tf32_ts(Od, T + kHlo + 8 * kk, bh, i_dec, 1u);
+            tc::mma_tf32_ts(Od, T + kHhi + 8 * kk, tc::sdesc_sw128(wtl + boff, 16, 1024), i_dec, 1u);
+          }
+        }
+        tc::tc_commit(&ofull[b]);
+        if (i >= 1) mma3(i - 1);
+      }
+      if (my_tiles > 0) mma3(my_tiles - 1);
+      tc::tc_commit(&done);
+    }
+  } else if (warp >= 2 && warp < 6) {
+    // -------------------------------------------------------- epilogue --
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int r = quad * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    {  // h -> TMEM as tf32 hi / lo
+      float v[32], vl[32];
+      for (int half = 0; half < 2; ++half) {
+        for (int j = 0; j < 32; ++j) {
+          const float x = r < rows ? a.h[(long long)r * kW + half * 32 + j] : 0.0f;
+          v[j] = kPrecise ? tc::tf32_hi(x) : x;
+          vl[j] = x - v[j];
+        }
+        tc::tmem_st32(T + lane_addr + kHhi + 32 * half, v);
+        if (kPrecise) tc::tmem_st32(T + lane_addr + kHlo + 32 * half, vl);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&h_ready);
+    }
+    double mae = 0.0;
+    for (int i = 0; i < my_tiles; ++i) {
+      const int s = i % kStages;
+      const int b = i & 1;
+      const uint32_t phb = (uint32_t)(i >> 1) & 1u;
+      const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+      tc::mbar_wait(&ofull[b], phb);
+      tc::tc_fence_after();
+      float o[32];
+      tc::tmem_ld32(T + lane_addr + kO0 + 32u * (uint32_t)b, o);
+      unsigned char* yrow = Yp(s) + r * 128;
+      unsigned char* lrow = Ylo(s) + r * 128;
+      const bool row_ok = r < rows;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t off = (uint32_t)(((q ^ (r & 7)) & 7) << 4);
+        float4 yh = *reinterpret_cast<const float4*>(yrow + off);
+        float4 yl = kPrecise ? *reinterpret_cast<const float4*>(lrow + off) : make_float4(0, 0, 0, 0);
+        const float yv[4] = {yh.x + yl.x, yh.y + yl.y, yh.z + yl.z, yh.w + yl.w};
+        float sv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = q * 4 + e;
+          float sg = 0.0f;
+          if (row_ok && c0 + c < out) {
+            const float of = o[c] + __ldg(bias_pad + c0 + c);
+            const double d = (double)of - (double)yv[e];
+            mae += fabs(d);
+            sg = d > 0 ? 1.0f : (d < 0 ? -1.0f : 0.0f);
+          }
+          sv[e] = sg;
+        }
+        *reinterpret_cast<float4*>(lrow + off) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+      }
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&oempty[b]);
+      tc::mbar_arrive(&sready[s]);
+    }
+    // ---- partials out ----
+    tc::mbar_wait(&done, 0);
+    tc::tc_fence_after();
+    float* pe = a.P_enc + ((long long)blockIdx.x * a.B + r) * kW;
+    float* pd = a.P_dec + ((long long)blockIdx.x * a.B + r) * kW;
+    for (int half = 0; half < 2; ++half) {
+      float v[32];
+      if (my_tiles > 0) {
+        tc::tmem_ld32(T + lane_addr + kPenc + 32 * half, v);
+      } else {
+        for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+      }
+      if (r < rows)
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(pe + 32 * half + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      if (my_tiles > 0) {
+        tc::tmem_ld32(T + lane_addr + kPdec + 32 * half, v);
+      }
+      if (r < rows)
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(pd + 32 * half + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+    red[r] = mae;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (r == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 128; ++k) t += red[k];
+      a.mae_part[blockIdx.x] = t;
+    }
+  } else {
+    // ------------------------------------------------- Y hi/lo split ----
+    if (kPrecise) {
+      const int t = threadIdx.x - 192;  // 0..127
+      for (int i = 0; i < my_tiles; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+        tc::mbar_wait(&full[s], ph);
+        float4* yh = reinterpret_cast<float4*>(Yp(s));
+        float4* yl = reinterpret_cast<float4*>(Ylo(s));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = t + 128 * k;
+          const float4 v = yh[idx];
+          const float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
+          yh[idx] = h;
+          yl[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&split_done[s]);
+      }
+    } else {
+      const int t = threadIdx.x - 192;
+      (void)t;
+      for (int i = 0; i < my_tiles; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+        tc::mbar_wait(&full[s], ph);
+        tc::mbar_arrive(&split_done[s]);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<512>(T);
+}
+
+// ----------------------------------------------------------------- host --
+bool wide_tc_supported(const StepArgs& a) {
+  return a.m.E1 == wt::kW && a.m.D == wt::kW && a.B <= wt::kRows && a.m.out >= wt::kTileN;
+}
+
+void launch_wide_tc(const StepArgs&, cudaStream_t) {
+  throw std::runtime_error("launch_wide_tc: use launch_wide_tc_params");
+}
+
+void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_wide_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt::kSmem);
+    cudaFuncSetAttribute(k_wide_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt::kSmem);
+    attr = true;
+  }
+  WideTcParams tp;
+  std::memcpy(&tp, p.maps, sizeof tp);
+  if (p.y_sel >= 0) std::memcpy(&tp.tm_y, p.y_alt[p.y_sel], sizeof(CUtensorMap));
+  if (p.precise)
+    k_wide_tc<true><<<a.S, wt::kThreads, wt::kSmem, s>>>(tp, a, p.bias_pad);
+  else
+    k_wide_tc<false><<<a.S, wt::kThreads, wt::kSmem, s>>>(tp, a, p.bias_pad);
+}
+
+// Splits / transposes the frozen wide-layer weights into the K-major tf32
+// hi/lo copies the kernel streams (run whenever enc/dec change).
+__global__ void k_prep_wide(const float* __restrict__ enc, long long enc_w, const float* __restrict__ dec,
+                            long long dec_w, long long dec_b, int out, int out_pad, float* wet_hi,
+                            float* wet_lo, float* wd_hi, float* wd_lo, float* wdt_hi, float* wdt_lo,
+                            float* bias_pad) {
+  const long long n = (long long)wt::kW * out_pad;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / out_pad), c = (int)(i % out_pad);
+    const bool ok = c < out;
+    const float we = ok ? enc[enc_w + (long long)c * wt::kW + j] : 0.0f;  // enc W0 [out x 64]
+    const float wd = ok ? dec[dec_w + (long long)j * out + c] : 0.0f;     // dec W_last [64 x out]
+    const float weh = tc::tf32_hi(we), wdh = tc::tf32_hi(wd);
+    wet_hi[i] = weh;
+    wet_lo[i] = we - weh;
+    wd_hi[i] = wdh;
+    wd_lo[i] = wd - wdh;
+    wdt_hi[(long long)c * wt::kW + j] = wdh;
+    wdt_lo[(long long)c * wt::kW + j] = wd - wdh;
+    if (j == 0) bias_pad[c] = ok ? dec[dec_b + c] : 0.0f;
+  }
+}
+
+void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t s) {
+  k_prep_wide<<<592, 256, 0, s>>>(a.p[kEnc], a.m.enc_wide_w, a.p[kDec], a.m.dec_wide_w, a.m.dec_wide_b, a.m.out,
+                                  a.m.out_pad, p.wet_hi, p.wet_lo, p.wd_hi, p.wd_lo, p.wdt_hi, p.wdt_lo,
+                                  p.bias_pad);
+}
+
+static_assert(sizeof(WideTcParams) == 7 * 128, "CUtensorMap packing");
+
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+void encode_2d(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+               uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 4};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+}  // namespace
+
+void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows) {
+  CUtensorMap m;
+  encode_2d(&m, yb, (uint64_t)a.m.out_pad, (uint64_t)yb_rows, 32, 128);
+  std::memcpy(p.y_alt[which], &m, sizeof m);
+}
+
+void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows) {
+  WideTcParams tp;
+  const uint64_t op = (uint64_t)a.m.out_pad;
+  encode_2d(&tp.tm_y, yb, op, (uint64_t)yb_rows, 32, 128);
+  encode_2d(&tp.tm_wet_hi, p.wet_hi, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wet_lo, p.wet_lo, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wd_hi, p.wd_hi, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wd_lo, p.wd_lo, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wdt_hi, p.wdt_hi, wt::kW, op, 32, 32);
+  encode_2d(&tp.tm_wdt_lo, p.wdt_lo, wt::kW, op, 32, 32);
+  std::memcpy(p.maps, &tp, sizeof tp);
+}
 
 }  // namespace ltfb_dev

@@ -13,11 +13,34 @@ void launch_pre(const StepArgs& a, cudaStream_t s);
 void launch_wide_generic(const StepArgs& a, cudaStream_t s);
 bool wide_tc_supported(const StepArgs& a);
 void launch_wide_tc(const StepArgs& a, cudaStream_t s);
+
+/// Host-side state of the tcgen05 wide pass: K-major tf32 hi/lo copies of
+/// the frozen wide-layer weights and the TMA descriptors over them.
+struct WideTcParamsHost {
+  alignas(64) unsigned char maps[7 * 128];  // CUtensorMap x7 (y, WeT hi/lo, Wd hi/lo, WdT hi/lo)
+  alignas(64) unsigned char y_alt[2][128];  // y maps of the host-streamed (e2e) minibatch buffers
+  int y_sel = -1;                           // -1: maps[0] (gathered minibatch), else y_alt[y_sel]
+  bool precise = true;
+  float* bias_pad = nullptr;
+  float* wet_hi = nullptr;
+  float* wet_lo = nullptr;
+  float* wd_hi = nullptr;
+  float* wd_lo = nullptr;
+  float* wdt_hi = nullptr;
+  float* wdt_lo = nullptr;
+};
+/// Builds the TMA descriptors (yb is [yb_rows x out_pad]).
+void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows);
+void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows);
+void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t s);
+void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s);
 void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 
 std::size_t eval_wide_smem(const ModelArgs& m);
+cudaError_t selftest_tc(const float* a1, const float* b1, const float* ah, const float* b2, const float* a3,
+                        float* d1, float* d2, float* d3);
 void launch_eval(const EvalArgs& a, cudaStream_t s);
 
 }  // namespace ltfb_dev

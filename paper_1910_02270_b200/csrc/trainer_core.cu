@@ -110,9 +110,28 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   }
   const int B = static_cast<int>(spec_.batch_size);
   const auto& ma = margs_;
-  S_ = std::min<std::size_t>((ma.out + 31) / 32, static_cast<std::size_t>(sm_count_) * 2);
+  // wide-pass kernel: tcgen05 (3xTF32 parity or 1xTF32 fast) where the
+  // shape allows it, else the generic SIMT kernel
+  {
+    ltfb_dev::StepArgs probe{};
+    probe.m = ma;
+    probe.B = B;
+    const bool tc_ok = ltfb_dev::wide_tc_supported(probe);
+    if (spec_.wide_kernel == 0) wide_kind_ = tc_ok ? 2 : 1;
+    else if (spec_.wide_kernel == 1) wide_kind_ = 1;
+    else if (spec_.wide_kernel == 2 || spec_.wide_kernel == 3) {
+      if (!tc_ok) throw ContractError("tcgen05 wide kernel requested but unsupported for this shape");
+      wide_kind_ = spec_.wide_kernel;
+    } else {
+      throw ContractError("wide_kernel must be 0 (auto), 1 (generic), 2 (tcgen05 3xTF32) or 3 (tcgen05 TF32)");
+    }
+  }
+  S_ = wide_kind_ >= 2 ? static_cast<std::size_t>(sm_count_)
+                       : std::min<std::size_t>((ma.out + 31) / 32, static_cast<std::size_t>(sm_count_) * 2);
+  const std::size_t yb_rows = std::max<std::size_t>(B, 128);
   xb_.alloc(static_cast<std::size_t>(B) * ma.in);
-  yb_.alloc(static_cast<std::size_t>(B) * ma.out_pad);
+  yb_.alloc(yb_rows * ma.out_pad);
+  LTFB_CUDA(cudaMemsetAsync(yb_.p, 0, yb_.bytes(), stream_));
   pe_.alloc(S_ * B * ma.E1);
   pd_.alloc(S_ * B * ma.D);
   mae_part_.alloc(S_);
@@ -156,10 +175,21 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.rec = rec_.p;
   ensure_adam_table(1024);
 
-  wide_kind_ = 1;
-  if (spec_.wide_kernel != 1 && ltfb_dev::wide_tc_supported(a)) wide_kind_ = 2;
-  if (spec_.wide_kernel == 2 && wide_kind_ != 2)
-    throw ContractError("tcgen05 wide kernel requested but unsupported for this shape");
+  if (wide_kind_ >= 2) {
+    const std::size_t nw = 64 * static_cast<std::size_t>(ma.out_pad);
+    for (auto* b : {&wet_hi_, &wet_lo_, &wd_hi_, &wd_lo_, &wdt_hi_, &wdt_lo_}) b->alloc(nw);
+    bias_pad_.alloc(ma.out_pad);
+    wtp_.precise = wide_kind_ == 2;
+    wtp_.bias_pad = bias_pad_.p;
+    wtp_.wet_hi = wet_hi_.p;
+    wtp_.wet_lo = wet_lo_.p;
+    wtp_.wd_hi = wd_hi_.p;
+    wtp_.wd_lo = wd_lo_.p;
+    wtp_.wdt_hi = wdt_hi_.p;
+    wtp_.wdt_lo = wdt_lo_.p;
+    ltfb_dev::encode_wide_maps(wtp_, a, yb_.p, static_cast<int>(yb_rows));
+    wide_dirty_ = true;
+  }
   LTFB_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -251,6 +281,7 @@ static float* net_ptr(DeviceTrainer& t, DevBuf<float>* params, DevBuf<float>& ge
 }
 
 void DeviceTrainer::set_params(int net, const float* blob, std::size_t count) {
+  if (net == 0 || net == 1) wide_dirty_ = true;
   if (net < 0 || net > 4) throw ContractError("set_params: bad network index");
   if (count != counts_[net])
     throw ContractError("blob length " + std::to_string(count) + " does not match manifest total " +
@@ -446,6 +477,11 @@ void DeviceTrainer::resolve_kernel_times() {
 }
 
 void DeviceTrainer::launch_step_kernels(bool gather) {
+  if (wide_kind_ >= 2 && wide_dirty_) {
+    ltfb_dev::launch_prep_wide(args_, wtp_, stream_);
+    ++launches_;
+    wide_dirty_ = false;
+  }
   if (gather) {
     kernel_mark(0, true);
     ltfb_dev::launch_gather(args_, stream_);
@@ -455,7 +491,7 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
   ltfb_dev::launch_pre(args_, stream_);
   kernel_mark(1, false);
   kernel_mark(2, true);
-  if (wide_kind_ == 2) ltfb_dev::launch_wide_tc(args_, stream_);
+  if (wide_kind_ >= 2) ltfb_dev::launch_wide_tc_params(wtp_, args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
   kernel_mark(2, false);
   kernel_mark(4, true);
@@ -679,7 +715,9 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
     LTFB_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       hx_[i].alloc(B * m.in);
-      hy_[i].alloc(B * m.out_pad);
+      hy_[i].alloc(std::max<std::size_t>(B, 128) * m.out_pad);
+      if (wide_kind_ >= 2)
+        ltfb_dev::encode_y_map(wtp_, i, hy_[i].p, args_, static_cast<int>(std::max<std::size_t>(B, 128)));
       LTFB_CUDA(cudaMemsetAsync(hy_[i].p, 0, hy_[i].bytes(), copy_stream_));
       LTFB_CUDA(cudaEventCreateWithFlags(&h2d_done_[i], cudaEventDisableTiming));
       LTFB_CUDA(cudaEventCreateWithFlags(&used_done_[i], cudaEventDisableTiming));
@@ -705,7 +743,9 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
     LTFB_CUDA(cudaStreamWaitEvent(stream_, h2d_done_[b], 0));
     args_.xb = hx_[b].p;
     args_.yb = hy_[b].p;
+    wtp_.y_sel = b;
     launch_step_kernels(false);
+    wtp_.y_sel = -1;
     LTFB_CUDA(cudaEventRecord(used_done_[b], stream_));
     ++step_in_epoch_;
     ++epoch_steps_;

@@ -19,6 +19,7 @@
 
 #include "device_common.cuh"
 #include "ltfb_b200/types.hpp"
+#include "kernels.hpp"
 #include "step_args.cuh"
 
 namespace ltfb_b200 {
@@ -188,6 +189,10 @@ class DeviceTrainer {
   DevBuf<float> sx_, sy_;
   DevBuf<unsigned> perm_[2];
   DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
+  // tcgen05 wide pass: K-major tf32 hi/lo copies of the frozen weights
+  DevBuf<float> wet_hi_, wet_lo_, wd_hi_, wd_lo_, wdt_hi_, wdt_lo_, bias_pad_;
+  ltfb_dev::WideTcParamsHost wtp_{};
+  bool wide_dirty_ = false;
   DevBuf<double> mae_part_, mae_total_, adam_c_;
   DevBuf<ltfb_dev::Counters> ctr_;
   DevBuf<ltfb_dev::StepRec> rec_;

@@ -77,7 +77,7 @@ class TrainerConfigC(C.Structure):
                 ("numeric_abort_threshold", C.c_int32), ("batch_size", C.c_uint64),
                 ("seed", C.c_uint64), ("w_f", C.c_double), ("w_i", C.c_double),
                 ("lr_fwd", C.c_double), ("lr_inv", C.c_double), ("lr_disc", C.c_double),
-                ("wide_kernel", C.c_int32), ("reserved", C.c_int32)]
+                ("wide_kernel", C.c_int32), ("post_kernel", C.c_int32)]
 
 
 class StepRecordC(C.Structure):

@@ -453,7 +453,8 @@ class TrainerConfig:
     train_ids: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
     tournament_ids: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
     device: int = 0
-    wide_kernel: int = 0       # 0 auto, 1 generic SIMT, 2 tcgen05
+    wide_kernel: int = 0       # 0 auto, 1 generic SIMT, 2 tcgen05 3xTF32, 3 tcgen05 TF32
+    post_kernel: int = 0       # 0 auto (smem fast path), 1 generic
     lr: tuple | None = None    # per-net lr override (fwd, inv, disc)
 
 
@@ -481,6 +482,7 @@ class Trainer:
         if cfg.lr is not None:
             cc.lr_fwd, cc.lr_inv, cc.lr_disc = cfg.lr
         cc.wide_kernel = cfg.wide_kernel
+        cc.post_kernel = cfg.post_kernel
         self._h = C.c_void_p()
         dc, ac = model.dims.c(), model.arch.c()
         check(lib.ltfb_trainer_create(C.byref(dc), C.byref(ac), C.byref(cc), C.byref(self._h)))

@@ -216,6 +216,7 @@ int ltfb_trainer_create(const ltfb_dims* dims, const ltfb_arch* arch, const ltfb
     s.lr[3] = cfg->lr_inv;
     s.lr[4] = cfg->lr_disc;
     s.wide_kernel = cfg->wide_kernel;
+    s.post_kernel = cfg->post_kernel;
     auto h = std::make_unique<ltfb_trainer>();
     h->t = std::make_unique<DeviceTrainer>(s);
     *out = h.release();

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kRedOut * kRedGroups) k_reduce(StepArgs a) {
   __shared__ float part[kRedGroups][kRedOut];
   const int rows = post_rows(a);
   const ModelArgs& m = a.m;
-  const ScratchLayout L = make_scratch_layout(m, a.B);
+  const ScratchLayout& L = a.L;
   float* red_enc = a.scratch + L.red_enc;
   float* red_dec = a.scratch + L.red_dec;
   const long long ne = (long long)rows * m.E1, nd = (long long)rows * m.D;
@@ -146,7 +146,7 @@ __global__ void __cluster_dims__(kPostCluster, 1, 1) __launch_bounds__(kPostThre
   const int per = (rows + C - 1) / C;
   const int r0 = min(rank * per, rows);
   const int nr = min(per, rows - r0);
-  const ScratchLayout L = make_scratch_layout(m, a.B);
+  const ScratchLayout& L = a.L;
   float* sc = a.scratch;
   const BlockSync bs{};
   const int tid = threadIdx.x, nth = blockDim.x;

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(128) k_pre(StepArgs a) {
   const int nr = min(per, rows - r0);
   if (nr <= 0) return;
   const ModelArgs& m = a.m;
-  const ScratchLayout L = make_scratch_layout(m, a.B);
+  const ScratchLayout& L = a.L;
   float* sc = a.scratch;
   float* fz[kMaxLayers];
   float* fa[kMaxLayers];

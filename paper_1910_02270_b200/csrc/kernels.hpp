@@ -36,6 +36,8 @@ void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t
 void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s);
 void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
+bool post_fast_supported(const StepArgs& a);
+void launch_post_fast(const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 
 std::size_t eval_wide_smem(const ModelArgs& m);

@@ -7,27 +7,9 @@
 
 namespace ltfb_dev {
 
-struct ScratchLayout {
-  long long fz[kMaxLayers], fa[kMaxLayers];  // fwd tape         [B x w]
-  long long hz[kMaxLayers], ha[kMaxLayers];  // dec-head tape    [B x w]
-  long long ez[kMaxLayers], ea[kMaxLayers];  // enc-tail outputs [B x w]
-  long long cz[kMaxLayers], ca[kMaxLayers];  // disc tape        [2B x w]
-  long long iz[kMaxLayers], ia[kMaxLayers];  // inv tape         [B x w]
-  long long e1z, e1a;                        // enc wide layer   [B x E1]
-  long long stacked;                         // [2B x lat]
-  long long probs, bgrad;                    // [2B]
-  long long gh;                              // [B x D]
-  long long gl_dec, gl_disc, gl_inv, gl;     // [B x lat]
-  long long igrad;                           // [B x in]
-  long long tA, tB;                          // per post CTA: [2 ceil(B/C) x maxw]
-  long long tstride;                         // floats per post CTA in tA / tB
-  long long red_enc, red_dec;                // reduced wide-pass sums [B x E1], [B x D]
-  long long pg_disc, pg_fwd, pg_inv;         // per post CTA partial gradients
-  long long total;
-};
 
-constexpr int kPostCluster = 8;   // CTAs of the post kernel (one cluster)
-constexpr int kPostThreads = 256;
+
+
 
 __host__ __device__ inline long long round_up_ll(long long v, long long a) { return (v + a - 1) / a * a; }
 

@@ -170,6 +170,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.mae_part = mae_part_.p;
   a.mae_total = mae_total_.p;
   a.scratch = scratch_.p;
+  a.L = lay;
   a.h = scratch_.p + (margs_.dec_head.L > 0 ? lay.ha[margs_.dec_head.L - 1] : lay.fa[margs_.fwd.L - 1]);
   a.ctr = ctr_.p;
   a.rec = rec_.p;
@@ -188,6 +189,9 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
     wtp_.wdt_hi = wdt_hi_.p;
     wtp_.wdt_lo = wdt_lo_.p;
     ltfb_dev::encode_wide_maps(wtp_, a, yb_.p, static_cast<int>(yb_rows));
+  }
+  post_fast_ = spec_.post_kernel != 1 && ltfb_dev::post_fast_supported(a);
+  {
     wide_dirty_ = true;
   }
   LTFB_CUDA(cudaStreamSynchronize(stream_));
@@ -498,7 +502,8 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
   ltfb_dev::launch_reduce(args_, stream_);
   kernel_mark(4, false);
   kernel_mark(3, true);
-  ltfb_dev::launch_post(args_, stream_);
+  if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
+  else ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
   launches_ += gather ? 5 : 4;
 }

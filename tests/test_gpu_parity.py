@@ -40,7 +40,7 @@ def rel(a, b, floor=1e-12):
     return float(np.max(np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), floor)))
 
 
-def make_trainer(g, pfx, dims, arch, ds_meta, wide_kernel=0, shards=None):
+def make_trainer(g, pfx, dims, arch, ds_meta, wide_kernel=0, shards=None, post_kernel=0):
     model_seed, gshards, batch, seed, n_tour, steps = (int(v) for v in g[pfx + "cfg"])
     n, per_file, spec_seed, sampling_seed = (int(v) for v in ds_meta)
     ds = L.synthetic_dataset(dims, n, sampling_seed=sampling_seed, spec_seed=spec_seed,
@@ -50,7 +50,7 @@ def make_trainer(g, pfx, dims, arch, ds_meta, wide_kernel=0, shards=None):
     ids = np.arange(n, dtype=np.uint32)
     cfg = L.TrainerConfig(trainer_id=0, n_shards=shards or gshards, batch_size=batch, seed=seed,
                           prefetch_depth=0, train_ids=ids[n_tour:], tournament_ids=ids[:n_tour],
-                          wide_kernel=wide_kernel)
+                          wide_kernel=wide_kernel, post_kernel=post_kernel)
     return L.Trainer(cfg, ds, model), steps, ds
 
 
@@ -84,10 +84,11 @@ def check_against_golden(g, pfx, t, steps):
     return errs
 
 
-@pytest.mark.parametrize("kernel", [1, 0])
-def test_trainer_tiny_matches_reference(golden, kernel):
+@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0)])
+def test_trainer_tiny_matches_reference(golden, kernel, post):
     g = golden("trainer")
-    t, steps, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"], kernel)
+    t, steps, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"], kernel,
+                               post_kernel=post)
     check_against_golden(g, "tiny_s1_", t, steps)
 
 
@@ -110,11 +111,24 @@ def test_trainer_desk_matches_reference(golden, pfx):
     check_against_golden(g, pfx, t, steps)
 
 
-@pytest.mark.parametrize("kernel", [1, 0])
-def test_trainer_paper_matches_reference(golden, kernel):
+@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0), (2, 1)])
+def test_trainer_paper_matches_reference(golden, kernel, post):
     g = golden("trainer")
-    t, steps, _ = make_trainer(g, "paper_s1_", PAPER, L.SurrogateArch(), g["paper_data"], kernel)
+    t, steps, _ = make_trainer(g, "paper_s1_", PAPER, L.SurrogateArch(), g["paper_data"], kernel,
+                               post_kernel=post)
+    assert t.wide_info()[0] == (kernel if kernel else 2)
     check_against_golden(g, "paper_s1_", t, steps)
+
+
+def test_trainer_paper_tf32_perf_mode(golden):
+    """1xTF32 wide pass (perf mode): stated tolerance 1e-3 relative on the
+    per-step losses over the golden run."""
+    g = golden("trainer")
+    t, steps, _ = make_trainer(g, "paper_s1_", PAPER, L.SurrogateArch(), g["paper_data"], 3)
+    t.train_steps(steps)
+    h = t.history()
+    for name in ("d_loss", "g_total", "g_fwd", "g_adv", "g_cyc"):
+        assert rel([getattr(s, name) for s in h.steps], g["paper_s1_steps_" + name]) < 1e-3, name
 
 
 def test_numeric_skip_then_abort(golden):

@@ -37,7 +37,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--steps", type=int, default=1000)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--dims", default="paper", choices=["paper", "desk"])
@@ -76,8 +76,30 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device, self.proc, self.lines = device, None, []
+        self.nvml, self.samples, self._stop = None, [], threading.Event()
+
+    def _poll_nvml(self):
+        n, h = self.nvml, self.handle
+        while not self._stop.is_set():
+            try:
+                self.samples.append((n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM),
+                                     n.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
+        try:  # NVML polled every 5 ms: short timed regions still get samples
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._t.start()
+            return
+        except Exception:
+            self.nvml = None
         if not shutil.which("nvidia-smi"):
             return
         self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -91,6 +113,19 @@ class ClockSampler:
             self.lines.append(ln.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+            n = self.nvml
+            bits = {"hw_slowdown": n.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": n.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": n.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": n.nvmlClocksEventReasonSwPowerCap}
+            sm = [s for s, _ in self.samples]
+            reasons = sorted({k for _, r in self.samples for k, b in bits.items() if r & b})
+            loaded = [s for s in sm if s > 0.3 * self.max_mhz] or sm
+            return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml 5 ms"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()

@@ -76,7 +76,8 @@ typedef struct {
   double lr_fwd, lr_inv, lr_disc; /* 0 = arch.lr (runner.hpp:286-293 lr_jitter) */
   int32_t wide_kernel;   /* 0 auto, 1 generic SIMT, 2 tcgen05 3xTF32 (fp32 parity),
                             3 tcgen05 1xTF32 (perf mode); 2/3 error if unsupported */
-  int32_t post_kernel;   /* 0 auto (shared-memory fast path when the nets fit), 1 generic */
+  int32_t post_kernel;   /* 0 auto, 1 generic cluster kernel, 2 shared-memory fast path,
+                            3 compile-time-shaped kernel (2/3 error if unsupported) */
 } ltfb_trainer_config;
 
 /* train/history.hpp:20-30 */

@@ -454,7 +454,7 @@ class TrainerConfig:
     tournament_ids: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint32))
     device: int = 0
     wide_kernel: int = 0       # 0 auto, 1 generic SIMT, 2 tcgen05 3xTF32, 3 tcgen05 TF32
-    post_kernel: int = 0       # 0 auto (smem fast path), 1 generic
+    post_kernel: int = 0       # 0 auto, 1 generic, 2 smem fast path, 3 compile-time shapes
     lr: tuple | None = None    # per-net lr override (fwd, inv, disc)
 
 

@@ -38,6 +38,10 @@ void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
 bool post_fast_supported(const StepArgs& a);
 void launch_post_fast(const StepArgs& a, cudaStream_t s);
+/// Compile-time-shaped post kernel (k_post_tpl.cu): 0 if no instance
+/// matches the model, else the instance id for launch_post_tpl.
+int post_tpl_kind(const StepArgs& a);
+void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 
 std::size_t eval_wide_smem(const ModelArgs& m);

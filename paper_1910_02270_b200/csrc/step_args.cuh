@@ -52,6 +52,7 @@ struct StepArgs {
   int S;            // split count of the wide pass (partials)
   int abort_threshold;
   int rec_cap;
+  int phase_prof;   // debug: per-phase clock64 stamps printed by the post kernel (LTFB_PHASE_PROF)
   int small_ctas;   // CTAs of the small-network kernels
   double lr[5], b1, b2, eps;
   long long adam_cap;  // entries of the bias-correction table

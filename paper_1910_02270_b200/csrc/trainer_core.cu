@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -151,6 +152,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.S = static_cast<int>(S_);
   a.abort_threshold = spec_.numeric_abort_threshold;
   a.rec_cap = static_cast<int>(rec_.n);
+  a.phase_prof = std::getenv("LTFB_PHASE_PROF") ? 1 : 0;
   a.small_ctas = std::max(1, (B + 15) / 16);
   const auto& h = spec_.arch.adam;
   for (int i = 0; i < 5; ++i) a.lr[i] = spec_.lr[i] > 0 ? spec_.lr[i] : h.lr;
@@ -190,7 +192,15 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
     wtp_.wdt_lo = wdt_lo_.p;
     ltfb_dev::encode_wide_maps(wtp_, a, yb_.p, static_cast<int>(yb_rows));
   }
-  post_fast_ = spec_.post_kernel != 1 && ltfb_dev::post_fast_supported(a);
+  // post kernel: compile-time-shaped instance when the model matches one,
+  // else the shared-memory fast path, else the generic cluster kernel
+  post_tpl_ = spec_.post_kernel == 0 || spec_.post_kernel == 3 ? ltfb_dev::post_tpl_kind(a) : 0;
+  if (spec_.post_kernel == 3 && post_tpl_ == 0)
+    throw ContractError("post_kernel 3 (compile-time shapes) requested but no instance matches this model");
+  post_fast_ = post_tpl_ == 0 && (spec_.post_kernel == 0 || spec_.post_kernel == 2) &&
+               ltfb_dev::post_fast_supported(a);
+  if (spec_.post_kernel == 2 && !post_fast_)
+    throw ContractError("post_kernel 2 (shared-memory fast path) requested but unsupported for this model");
   {
     wide_dirty_ = true;
   }
@@ -502,7 +512,8 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
   ltfb_dev::launch_reduce(args_, stream_);
   kernel_mark(4, false);
   kernel_mark(3, true);
-  if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
+  if (post_tpl_) ltfb_dev::launch_post_tpl(post_tpl_, args_, stream_);
+  else if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
   else ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
   launches_ += gather ? 5 : 4;

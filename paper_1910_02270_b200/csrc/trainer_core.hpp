@@ -67,7 +67,7 @@ struct TrainerSpec {
   double w_f = 1.0, w_i = 1.0;
   double lr[5] = {0, 0, 0, 0, 0};  // 0 = arch.adam.lr
   int wide_kernel = 0;             // 0 auto, 1 generic, 2 tcgen05 3xTF32, 3 tcgen05 TF32
-  int post_kernel = 0;             // 0 auto (smem fast path when it fits), 1 generic
+  int post_kernel = 0;  // 0 auto, 1 generic cluster, 2 smem fast path, 3 compile-time shapes
 };
 
 struct EvalOut {
@@ -183,6 +183,7 @@ class DeviceTrainer {
   std::size_t S_ = 0;
   int wide_kind_ = 1;
   bool post_fast_ = false;
+  int post_tpl_ = 0;
   std::uint64_t launches_ = 0;
 
   DevBuf<float> params_[5], mom1_[5], mom2_[5], grads_[5];

@@ -84,7 +84,7 @@ def check_against_golden(g, pfx, t, steps):
     return errs
 
 
-@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0)])
+@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0), (0, 2), (0, 3)])
 def test_trainer_tiny_matches_reference(golden, kernel, post):
     g = golden("trainer")
     t, steps, _ = make_trainer(g, "tiny_s1_", TINY, L.SurrogateArch.tiny(), g["tiny_data"], kernel,
@@ -111,7 +111,7 @@ def test_trainer_desk_matches_reference(golden, pfx):
     check_against_golden(g, pfx, t, steps)
 
 
-@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0), (2, 1)])
+@pytest.mark.parametrize("kernel,post", [(1, 1), (0, 0), (2, 1), (0, 2), (0, 3)])
 def test_trainer_paper_matches_reference(golden, kernel, post):
     g = golden("trainer")
     t, steps, _ = make_trainer(g, "paper_s1_", PAPER, L.SurrogateArch(), g["paper_data"], kernel,

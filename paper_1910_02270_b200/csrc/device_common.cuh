@@ -53,6 +53,18 @@ __device__ __forceinline__ float act_apply(int kind, float slope, float z) {
     default: return z;
   }
 }
+/// act_apply for code that is unrolled many times: the piecewise-linear
+/// kinds inline, the transcendental ones behind one out-of-line call, so the
+/// instruction footprint stays small.
+__device__ __noinline__ float act_apply_slow(int kind, float slope, float z);
+__device__ __forceinline__ float act_apply_compact(int kind, float slope, float z) {
+  if (kind == kLeaky) return z > 0.0f ? z : slope * z;
+  if (kind == kIdentity) return z;
+  if (kind == kRelu) return z > 0.0f ? z : 0.0f;
+  return act_apply_slow(kind, slope, z);
+}
+__device__ __noinline__ inline float act_apply_slow(int kind, float slope, float z) { return act_apply(kind, slope, z); }
+
 __device__ __forceinline__ float act_deriv(int kind, float slope, float z, float a) {
   switch (kind) {
     case kRelu: return z > 0.0f ? 1.0f : 0.0f;

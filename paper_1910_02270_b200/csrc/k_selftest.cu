@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(128) k_selftest_tc(const float* a1, const floa
                                                       const float* b2, const float* a3, float* d1, float* d2,
                                                       float* d3) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
   unsigned char* A1 = sm;            // 16 KB
   unsigned char* B1 = sm + 16384;    // 8 KB (two 4 KB atoms)
   unsigned char* B2 = sm + 24576;    // 8 KB

@@ -31,19 +31,56 @@ __device__ __forceinline__ int batch_rows(const StepArgs& a) {
 }
 
 // ----------------------------------------------------------------- gather --
-// grid (x chunks, B rows). Each row is one contiguous HBM slab row; float4
-// copies keep every warp access 512 B-contiguous.
+// grid (x chunks [+ 1], B rows). Each row is one contiguous HBM slab row;
+// float4 copies keep every warp access 512 B-contiguous. With h_in_gather
+// the last CTA column computes h = dec_head(fwd(x)) for its row instead
+// (nn/mlp.hpp:201-217, the same k-ordered fmaf chains as k_pre): a few
+// dependent L2 round trips, hidden under the copy, so the wide pass finds
+// h in HBM/L2 without a separate launch.
+__device__ void row_h(const StepArgs& a, int r, unsigned slot) {
+  __shared__ float act[2][kMaxSmallWidth];
+  const ModelArgs& m = a.m;
+  const int t = threadIdx.x;
+  if (t < m.in) act[0][t] = a.x_from_store ? a.sx[(long long)slot * m.in + t] : a.xb[r * m.in + t];
+  __syncthreads();
+  int cur = 0;
+  for (int net = 0; net < 2; ++net) {
+    const NetDesc& n = net == 0 ? m.fwd : m.dec_head;
+    const float* blob = a.p[net == 0 ? kFwd : kDec];
+    for (int l = 0; l < n.L; ++l) {
+      const int in = n.w[l], out = n.w[l + 1];
+      const float* W = blob + n.off_w[l];
+      const bool last = net == 1 && l + 1 == n.L;
+      for (int j = t; j < out; j += blockDim.x) {
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int k = 0; k < in; ++k) acc = fmaf(act[cur][k], W[(long long)k * out + j], acc);
+        const float v = act_apply(n.act[l], n.slope[l], acc + blob[n.off_b[l] + j]);
+        if (last) a.h[(long long)r * out + j] = v;
+        else act[cur ^ 1][j] = v;
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_gather(StepArgs a) {
   if (a.ctr->aborted) return;
   const int rows = batch_rows(a);
   const int r = blockIdx.y;
   if (r >= rows) return;
-  const unsigned slot = a.perm[a.ctr->epoch & 1][(long long)a.ctr->step_in_epoch * a.B + r];
+  const long long idx = (long long)a.ctr->step_in_epoch * a.B + r;
+  const int nx = gridDim.x - (a.h_in_gather ? 1 : 0);  // copy columns
+  if ((int)blockIdx.x >= nx) {
+    row_h(a, r, a.x_from_store ? a.perm[a.ctr->epoch & 1][idx] : 0u);
+    return;
+  }
+  const unsigned slot = a.perm[a.ctr->epoch & 1][idx];
   const int n4 = a.m.out_pad >> 2;
   const float4* src = reinterpret_cast<const float4*>(a.sy + (long long)slot * a.m.out_pad);
   float4* dst = reinterpret_cast<float4*>(a.yb + (long long)r * a.m.out_pad);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x)
-    dst[i] = __ldcs(src + i);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += nx * blockDim.x) dst[i] = __ldcs(src + i);
   if (blockIdx.x == 0 && (int)threadIdx.x < a.m.in)
     a.xb[r * a.m.in + threadIdx.x] = a.sx[(long long)slot * a.m.in + threadIdx.x];
 }
@@ -184,7 +221,14 @@ namespace ltfb_dev {
 void launch_gather(const StepArgs& a, cudaStream_t s) {
   const int n4 = a.m.out_pad / 4;
   const int gx = (n4 + 256 * 4 - 1) / (256 * 4);
-  k_gather<<<dim3(gx, a.B), 256, 0, s>>>(a);
+  k_gather<<<dim3(gx + (a.h_in_gather ? 1 : 0), a.B), 256, 0, s>>>(a);
+}
+
+void launch_row_h(const StepArgs& a, cudaStream_t s) {
+  StepArgs b = a;  // h only: one CTA per row, x from the streamed minibatch
+  b.h_in_gather = 1;
+  b.x_from_store = 0;
+  k_gather<<<dim3(1, a.B), 256, 0, s>>>(b);
 }
 
 void launch_pre(const StepArgs& a, cudaStream_t s) { k_pre<<<a.small_ctas, 128, 0, s>>>(a); }

@@ -23,6 +23,9 @@
 //
 // Warp roles (320 threads): w0 TMA producer, w1 MMA issuer + TMEM owner,
 // w2-5 epilogue (TMEM lane quadrants 2,3,0,1), w6-9 Y hi/lo split.
+// After the tiles the grid synchronises (cooperative launch, one CTA per SM)
+// and every CTA sums a slice of the 148 partials in fixed CTA order (the
+// deterministic split-K reduction), so no separate reduce kernel runs.
 // Pipelines: 2 smem stages (full / split / sready / empty mbarriers),
 // 2 TMEM O buffers (ofull / oempty). Each CTA writes one [128 x 64] partial
 // of P_enc and P_dec and one f64 |d| sum; k_reduce sums them in fixed order.
@@ -55,14 +58,35 @@ struct WideTcParams {
   CUtensorMap tm_y, tm_wet_hi, tm_wet_lo, tm_wd_hi, tm_wd_lo, tm_wdt_hi, tm_wdt_lo;
 };
 
+/// Sense-reversing grid barrier; valid because the kernel is launched
+/// cooperatively (every CTA resident). bar[0] arrivals, bar[1] generation.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g0 = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == n - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g0) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <bool kPrecise>
 __global__ void __launch_bounds__(wt::kThreads, 1)
     k_wide_tc(const __grid_constant__ WideTcParams tp, StepArgs a, const float* __restrict__ bias_pad) {
   using namespace wt;
   if (a.ctr->aborted) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* sm =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base for the 128-byte swizzle; offsetting the __shared__
+  // array itself (not an integer round trip) keeps every access an LDS/STS
+  unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kStages], split_done[kStages], sready[kStages], empty[kStages];
   __shared__ uint64_t ofull[2], oempty[2], h_ready, done;
   __shared__ uint32_t tmem_base;
@@ -70,6 +94,9 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = min(a.B, a.n_part - (int)a.ctr->step_in_epoch * a.B);
+  __shared__ long long s_ph[10];
+  const bool prof = a.phase_prof && blockIdx.x == 0;
+  if (prof && threadIdx.x == 0) s_ph[0] = clock64();
   const int out = a.m.out;
   const int ntiles = (out + kTileN - 1) / kTileN;
   const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -201,19 +228,30 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    {  // h -> TMEM as tf32 hi / lo
-      float v[32], vl[32];
+    {  // h = dec_head(fwd(x)) (computed by k_gather / k_pre) -> TMEM as tf32 hi / lo
+      float4 hv[16];  // the row's 64 floats, all loads in flight at once
+      const float4* hrow = reinterpret_cast<const float4*>(a.h + (long long)r * kW);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) hv[q] = r < rows ? hrow[q] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
       for (int half = 0; half < 2; ++half) {
-        for (int j = 0; j < 32; ++j) {
-          const float x = r < rows ? a.h[(long long)r * kW + half * 32 + j] : 0.0f;
-          v[j] = kPrecise ? tc::tf32_hi(x) : x;
-          vl[j] = x - v[j];
+        float v[32], vl[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 x4 = hv[half * 8 + q];
+          const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[4 * q + e] = kPrecise ? tc::tf32_hi(xs[e]) : xs[e];
+            vl[4 * q + e] = xs[e] - v[4 * q + e];
+          }
         }
         tc::tmem_st32(T + lane_addr + kHhi + 32 * half, v);
         if (kPrecise) tc::tmem_st32(T + lane_addr + kHlo + 32 * half, vl);
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&h_ready);
+      if (prof && r == 0) s_ph[1] = clock64();
     }
     double mae = 0.0;
     for (int i = 0; i < my_tiles; ++i) {
@@ -318,6 +356,73 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<512>(T);
+  if (prof && threadIdx.x == 0) s_ph[2] = clock64();
+
+  // ---- grid-wide deterministic split-K reduction of the partials ----
+  grid_sync(a.grid_bar, gridDim.x);
+  if (prof && threadIdx.x == 0) s_ph[3] = clock64();
+  {
+    // float4 outputs [rows x 64] of P_enc then of P_dec; CTA c owns a
+    // contiguous slice; 8 thread groups sum partials s = g, g+8, ... in
+    // ascending order, then the 8 group sums are added in group order.
+    constexpr int kG = 8, kPer = kThreads / kG;  // 40 outputs per pass
+    const int q_enc = rows * (kW / 4), q_all = 2 * q_enc;
+    const int lo = (int)((long long)q_all * blockIdx.x / gridDim.x);
+    const int hi = (int)((long long)q_all * (blockIdx.x + 1) / gridDim.x);
+    float4* part = reinterpret_cast<float4*>(sm);  // [kG][kPer]
+    const int g = threadIdx.x / kPer, o = threadIdx.x % kPer;
+    const long long pstride4 = (long long)a.B * kW / 4;
+    float4* red_enc = reinterpret_cast<float4*>(a.scratch + a.L.red_enc);
+    float4* red_dec = reinterpret_cast<float4*>(a.scratch + a.L.red_dec);
+    for (int base = lo; base < hi; base += kPer) {
+      const int q = base + o;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (q < hi) {
+        const bool enc = q < q_enc;
+        const float4* src = reinterpret_cast<const float4*>(enc ? a.P_enc : a.P_dec) + (enc ? q : q - q_enc);
+        for (int s0 = g; s0 < a.S; s0 += 8 * kG) {  // 8 loads in flight, summed in order
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int sidx = s0 + u * kG;
+            v[u] = sidx < a.S ? __ldcg(src + sidx * pstride4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (s0 + u * kG < a.S) {
+              acc.x += v[u].x;
+              acc.y += v[u].y;
+              acc.z += v[u].z;
+              acc.w += v[u].w;
+            }
+          }
+        }
+      }
+      part[g * kPer + o] = acc;
+      __syncthreads();
+      if (g == 0 && q < hi) {
+        float4 t = part[o];
+        for (int k = 1; k < kG; ++k) {
+          const float4 v = part[k * kPer + o];
+          t.x += v.x;
+          t.y += v.y;
+          t.z += v.z;
+          t.w += v.w;
+        }
+        if (q < q_enc) red_enc[q] = t;
+        else red_dec[q - q_enc] = t;
+      }
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double t = 0.0;
+      for (int sidx = 0; sidx < a.S; ++sidx) t += __ldcg(a.mae_part + sidx);
+      *a.mae_total = t;
+    }
+  }
+  if (prof && threadIdx.x == 0)
+    printf("wide phases (cycles): h %lld, tiles %lld, grid sync %lld, reduce %lld\n", s_ph[1] - s_ph[0],
+           s_ph[2] - s_ph[0], s_ph[3] - s_ph[2], clock64() - s_ph[3]);
 }
 
 // ----------------------------------------------------------------- host --
@@ -339,10 +444,11 @@ void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStr
   WideTcParams tp;
   std::memcpy(&tp, p.maps, sizeof tp);
   if (p.y_sel >= 0) std::memcpy(&tp.tm_y, p.y_alt[p.y_sel], sizeof(CUtensorMap));
-  if (p.precise)
-    k_wide_tc<true><<<a.S, wt::kThreads, wt::kSmem, s>>>(tp, a, p.bias_pad);
-  else
-    k_wide_tc<false><<<a.S, wt::kThreads, wt::kSmem, s>>>(tp, a, p.bias_pad);
+  // cooperative: the in-kernel grid barrier needs every CTA resident
+  void* args[] = {(void*)&tp, (void*)&a, (void*)&p.bias_pad};
+  const void* fn = p.precise ? (const void*)k_wide_tc<true> : (const void*)k_wide_tc<false>;
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(a.S), dim3(wt::kThreads), args, wt::kSmem, s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("wide pass cooperative launch: ") + cudaGetErrorString(e));
 }
 
 // Splits / transposes the frozen wide-layer weights into the K-major tf32

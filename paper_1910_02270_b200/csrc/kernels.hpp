@@ -9,6 +9,8 @@
 namespace ltfb_dev {
 
 void launch_gather(const StepArgs& a, cudaStream_t s);
+/// h = dec_head(fwd(xb)) per row only (the host-streamed minibatch path).
+void launch_row_h(const StepArgs& a, cudaStream_t s);
 void launch_pre(const StepArgs& a, cudaStream_t s);
 void launch_wide_generic(const StepArgs& a, cudaStream_t s);
 bool wide_tc_supported(const StepArgs& a);

@@ -52,6 +52,8 @@ struct StepArgs {
   int S;            // split count of the wide pass (partials)
   int abort_threshold;
   int rec_cap;
+  int h_in_gather;  // 1: k_gather's last CTA column computes h = dec_head(fwd(x)) per row
+  int x_from_store; // 1: that h computation reads x through the epoch plan, 0: from xb
   int phase_prof;   // debug: per-phase clock64 stamps printed by the post kernel (LTFB_PHASE_PROF)
   int small_ctas;   // CTAs of the small-network kernels
   double lr[5], b1, b2, eps;
@@ -76,6 +78,7 @@ struct StepArgs {
   float* scratch;   // small-network tapes
   ScratchLayout L;  // offsets into scratch
   Counters* ctr;
+  unsigned* grid_bar;  // [2] arrival count, generation (cooperative wide pass)
   StepRec* rec;
   const double* adam_c;  // [cap x 2]: 1-b1^t, 1-b2^t (host std::pow)
 };

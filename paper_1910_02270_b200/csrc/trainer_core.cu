@@ -141,6 +141,8 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   scratch_.alloc(static_cast<std::size_t>(lay.total));
   ctr_.alloc(1);
   LTFB_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(ltfb_dev::Counters), stream_));
+  grid_bar_.alloc(2);
+  LTFB_CUDA(cudaMemsetAsync(grid_bar_.p, 0, grid_bar_.bytes(), stream_));
   rec_.alloc(4096);
   for (int i = 0; i < 2; ++i) {
     LTFB_CUDA(cudaEventCreateWithFlags(&perm_ev_[i], cudaEventDisableTiming));
@@ -175,6 +177,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.L = lay;
   a.h = scratch_.p + (margs_.dec_head.L > 0 ? lay.ha[margs_.dec_head.L - 1] : lay.fa[margs_.fwd.L - 1]);
   a.ctr = ctr_.p;
+  a.grid_bar = grid_bar_.p;
   a.rec = rec_.p;
   ensure_adam_table(1024);
 
@@ -197,6 +200,10 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   post_tpl_ = spec_.post_kernel == 0 || spec_.post_kernel == 3 ? ltfb_dev::post_tpl_kind(a) : 0;
   if (spec_.post_kernel == 3 && post_tpl_ == 0)
     throw ContractError("post_kernel 3 (compile-time shapes) requested but no instance matches this model");
+  // with the tcgen05 wide pass (which reduces its own partials) and the
+  // recomputing post kernel, h comes from the gather kernel and k_pre is skipped
+  a.h_in_gather = (wide_kind_ >= 2 && post_tpl_) ? 1 : 0;
+  a.x_from_store = 1;
   post_fast_ = post_tpl_ == 0 && (spec_.post_kernel == 0 || spec_.post_kernel == 2) &&
                ltfb_dev::post_fast_supported(a);
   if (spec_.post_kernel == 2 && !post_fast_)
@@ -501,22 +508,30 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
     ltfb_dev::launch_gather(args_, stream_);
     kernel_mark(0, false);
   }
-  kernel_mark(1, true);
-  ltfb_dev::launch_pre(args_, stream_);
-  kernel_mark(1, false);
+  if (!gather && args_.h_in_gather) {  // host-streamed minibatch: h from xb
+    ltfb_dev::launch_row_h(args_, stream_);
+    ++launches_;
+  }
+  if (!args_.h_in_gather) {  // k_pre: h and the small-net tapes
+    kernel_mark(1, true);
+    ltfb_dev::launch_pre(args_, stream_);
+    kernel_mark(1, false);
+  }
   kernel_mark(2, true);
   if (wide_kind_ >= 2) ltfb_dev::launch_wide_tc_params(wtp_, args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
   kernel_mark(2, false);
-  kernel_mark(4, true);
-  ltfb_dev::launch_reduce(args_, stream_);
-  kernel_mark(4, false);
+  if (wide_kind_ < 2) {  // ... and reduces its split-K partials itself
+    kernel_mark(4, true);
+    ltfb_dev::launch_reduce(args_, stream_);
+    kernel_mark(4, false);
+  }
   kernel_mark(3, true);
   if (post_tpl_) ltfb_dev::launch_post_tpl(post_tpl_, args_, stream_);
   else if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
   else ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
-  launches_ += gather ? 5 : 4;
+  launches_ += (gather ? 3 : 2) + (wide_kind_ < 2 ? 1 : 0) + (args_.h_in_gather ? 0 : 1);
 }
 
 void DeviceTrainer::timer_start() {

@@ -198,6 +198,7 @@ class DeviceTrainer {
   bool wide_dirty_ = false;
   DevBuf<double> mae_part_, mae_total_, adam_c_;
   DevBuf<ltfb_dev::Counters> ctr_;
+  DevBuf<unsigned> grid_bar_;
   DevBuf<ltfb_dev::StepRec> rec_;
   std::uint64_t adam_cap_ = 0;
   std::uint64_t t_host_max_ = 0;  // upper bound of any net's t

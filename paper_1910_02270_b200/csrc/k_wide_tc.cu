@@ -17,18 +17,19 @@
 //
 // Parity ("3xTF32") mode splits every fp32 operand into hi + lo tf32 parts
 // and accumulates hi*hi + lo*hi + hi*lo in f32 TMEM (S is exact in tf32, so
-// MMA3 needs only S*hi + S*lo). Frozen weights are split once into
-// K-major copies (WeT, Wd, WdT; tf32 MN-major operands would need the
-// 32B-atom swizzle); Y is split per tile in shared memory.
+// MMA3 needs only S*hi + S*lo). The operand tiles arrive by TMA as plain
+// fp32 (y, and K-major copies WeT / Wd / WdT of the frozen weights, laid
+// out once) and are split per tile in shared memory: 40 KB of HBM per tile
+// against 32 KB algorithmic (WdT duplicates Wd; a tf32 MN-major operand
+// would need the 32-B-atom swizzle, which MMA3's K-major use of Wd excludes).
 //
 // Warp roles (320 threads): w0 TMA producer, w1 MMA issuer + TMEM owner,
-// w2-5 epilogue (TMEM lane quadrants 2,3,0,1), w6-9 Y hi/lo split.
+// w2-5 epilogue (TMEM lane quadrants 2,3,0,1), w6-9 tf32 hi/lo split.
 // After the tiles the grid synchronises (cooperative launch, one CTA per SM)
 // and every CTA sums a slice of the 148 partials in fixed CTA order (the
 // deterministic split-K reduction), so no separate reduce kernel runs.
-// Pipelines: 2 smem stages (full / split / sready / empty mbarriers),
-// 2 TMEM O buffers (ofull / oempty). Each CTA writes one [128 x 64] partial
-// of P_enc and P_dec and one f64 |d| sum; k_reduce sums them in fixed order.
+// Pipelines: 2 smem stages of 80 KB (full / split / sready / empty
+// mbarriers), 2 TMEM O buffers (ofull / oempty).
 #include <cuda.h>
 
 #include <cstring>
@@ -46,7 +47,7 @@ constexpr int kRows = 128;                 // MMA M (minibatch rows)
 constexpr int kW = 64;                     // E1 == D == 64
 constexpr uint32_t kY = 16384;             // [128 x 32] f32
 constexpr uint32_t kWt = 8192;             // [64 x 32] f32
-constexpr uint32_t kStage = 2 * kY + 6 * kWt;  // Y, Ylo/S, WeT hi/lo, Wd hi/lo, WdT hi/lo
+constexpr uint32_t kStage = 2 * kY + 6 * kWt;  // Y (hi), Ylo/S, WeT hi/lo, Wd hi/lo, WdT hi/lo
 constexpr int kStages = 2;
 constexpr uint32_t kSmem = kStages * kStage + 1024;
 constexpr int kThreads = 320;
@@ -55,7 +56,7 @@ constexpr uint32_t kPenc = 0, kPdec = 64, kO0 = 128, kHhi = 192, kHlo = 256;
 }  // namespace wt
 
 struct WideTcParams {
-  CUtensorMap tm_y, tm_wet_hi, tm_wet_lo, tm_wd_hi, tm_wd_lo, tm_wdt_hi, tm_wdt_lo;
+  CUtensorMap tm_y, tm_wet, tm_wd, tm_wdt;  // minibatch y, WeT / Wd [64 x out_pad], WdT [out_pad x 64]
 };
 
 /// Sense-reversing grid barrier; valid because the kernel is launched
@@ -95,7 +96,9 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = min(a.B, a.n_part - (int)a.ctr->step_in_epoch * a.B);
   __shared__ long long s_ph[10];
+  __shared__ long long s_ev[16][8];  // debug timeline (LTFB_PHASE_PROF), CTA 0
   const bool prof = a.phase_prof && blockIdx.x == 0;
+#define LTFB_EV(i, e) do { if (prof && (i) < 16) s_ev[(i)][(e)] = clock64(); } while (0)
   if (prof && threadIdx.x == 0) s_ph[0] = clock64();
   const int out = a.m.out;
   const int ntiles = (out + kTileN - 1) / kTileN;
@@ -105,11 +108,11 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   // stage layout
   auto Yp = [&](int s) { return stage_ptr(s); };
   auto Ylo = [&](int s) { return stage_ptr(s) + kY; };
-  auto WeH = [&](int s) { return stage_ptr(s) + 2 * kY; };
+  auto WeH = [&](int s) { return stage_ptr(s) + 2 * kY; };            // WeT [64 j x 32 c] SW128
   auto WeL = [&](int s) { return stage_ptr(s) + 2 * kY + kWt; };
-  auto WdH = [&](int s) { return stage_ptr(s) + 2 * kY + 2 * kWt; };
+  auto WdH = [&](int s) { return stage_ptr(s) + 2 * kY + 2 * kWt; };   // Wd  [64 j x 32 c] SW128
   auto WdL = [&](int s) { return stage_ptr(s) + 2 * kY + 3 * kWt; };
-  auto WtH = [&](int s) { return stage_ptr(s) + 2 * kY + 4 * kWt; };
+  auto WtH = [&](int s) { return stage_ptr(s) + 2 * kY + 4 * kWt; };   // WdT [32 c x 64 j] as 2 K-blocks
   auto WtL = [&](int s) { return stage_ptr(s) + 2 * kY + 5 * kWt; };
 
   if (threadIdx.x == 0) {
@@ -129,9 +132,9 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tp.tm_y);
-    tc::tma_prefetch(&tp.tm_wet_hi);
-    tc::tma_prefetch(&tp.tm_wd_hi);
-    tc::tma_prefetch(&tp.tm_wdt_hi);
+    tc::tma_prefetch(&tp.tm_wet);
+    tc::tma_prefetch(&tp.tm_wd);
+    tc::tma_prefetch(&tp.tm_wdt);
   }
   if (warp == 1) tc::tmem_alloc<512>(&tmem_base);
   tc::tc_fence_before();
@@ -142,33 +145,29 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     if (lane == 0) {
-      const uint32_t bytes = kPrecise ? (kY + 6 * kWt) : (kY + 3 * kWt);
+      const uint32_t bytes = kY + 3 * kWt;  // fp32 tiles: y, WeT, Wd, WdT
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
         const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         if (i >= kStages) tc::mbar_wait(&empty[s], ph ^ 1u);
         const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+        LTFB_EV(i, 0);
         tc::mbar_expect_tx(&full[s], bytes);
         tc::tma_load_2d(Yp(s), &tp.tm_y, &full[s], c0, 0);
-        tc::tma_load_2d(WeH(s), &tp.tm_wet_hi, &full[s], c0, 0);
-        tc::tma_load_2d(WdH(s), &tp.tm_wd_hi, &full[s], c0, 0);
-        tc::tma_load_2d(WtH(s), &tp.tm_wdt_hi, &full[s], 0, c0);
-        tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt_hi, &full[s], 32, c0);
-        if (kPrecise) {
-          tc::tma_load_2d(WeL(s), &tp.tm_wet_lo, &full[s], c0, 0);
-          tc::tma_load_2d(WdL(s), &tp.tm_wd_lo, &full[s], c0, 0);
-          tc::tma_load_2d(WtL(s), &tp.tm_wdt_lo, &full[s], 0, c0);
-          tc::tma_load_2d(WtL(s) + 4096, &tp.tm_wdt_lo, &full[s], 32, c0);
-        }
+        tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
+        tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
+        tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
+        tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer --
     if (lane == 0) {
+      // every B operand K-major (tf32 MN-major operands would need the
+      // 32-B-atom swizzle, incompatible with Wd's K-major use in MMA3)
       const uint32_t i_enc = tc::idesc_tf32(128, 64, 0, 0);
       const uint32_t i_dec = tc::idesc_tf32(128, 32, 0, 0);
-      tc::mbar_wait(&h_ready, 0);
-      tc::tc_fence_after();
+      const uint32_t i_ga = i_enc;
       auto mma3 = [&](int j) {
         const int s = j % kStages;
         const uint32_t ph = (uint32_t)(j / kStages) & 1u;
@@ -177,12 +176,13 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         const uint32_t sA = tc::smem_u32(Ylo(s));  // S overwrote Ylo
         for (int kk = 0; kk < 4; ++kk) {
           const uint64_t ad = tc::sdesc_sw128(sA + 32 * kk, 16, 1024);
-          tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdH(s)) + 32 * kk, 16, 1024), i_enc,
+          tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdH(s)) + 32 * kk, 16, 1024), i_ga,
                           (j > 0 || kk > 0) ? 1u : 0u);
           if (kPrecise)
-            tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdL(s)) + 32 * kk, 16, 1024), i_enc, 1u);
+            tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdL(s)) + 32 * kk, 16, 1024), i_ga, 1u);
         }
         tc::tc_commit(&empty[s]);
+        LTFB_EV(j, 6);
       };
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         }
         const uint32_t yh = tc::smem_u32(Yp(s)), yl = tc::smem_u32(Ylo(s));
         const uint32_t weh = tc::smem_u32(WeH(s)), wel = tc::smem_u32(WeL(s));
-        for (int kk = 0; kk < 4; ++kk) {  // MMA1: P_enc += Y We
+        for (int kk = 0; kk < 4; ++kk) {  // MMA1: P_enc += Y We  (K = 8 c per step)
           const uint64_t ah = tc::sdesc_sw128(yh + 32 * kk, 16, 1024);
           const uint64_t bh = tc::sdesc_sw128(weh + 32 * kk, 16, 1024);
           tc::mma_tf32_ss(T + kPenc, ah, bh, i_enc, (i > 0 || kk > 0) ? 1u : 0u);
@@ -206,9 +206,13 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
             tc::mma_tf32_ss(T + kPenc, ah, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc, 1u);
           }
         }
+        if (i == 0) {  // h is needed from MMA2 on
+          tc::mbar_wait(&h_ready, 0);
+          tc::tc_fence_after();
+        }
         const uint32_t Od = T + kO0 + 32u * (uint32_t)b;
         const uint32_t wth = tc::smem_u32(WtH(s)), wtl = tc::smem_u32(WtL(s));
-        for (int kk = 0; kk < 8; ++kk) {  // MMA2: O = h Wd
+        for (int kk = 0; kk < 8; ++kk) {  // MMA2: O = h Wd  (K = 8 j per step, B = WdT K-major)
           const uint32_t boff = (kk / 4) * 4096 + 32 * (kk % 4);
           const uint64_t bh = tc::sdesc_sw128(wth + boff, 16, 1024);
           tc::mma_tf32_ts(Od, T + kHhi + 8 * kk, bh, i_dec, kk > 0 ? 1u : 0u);
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
           }
         }
         tc::tc_commit(&ofull[b]);
+        LTFB_EV(i, 3);
         if (i >= 1) mma3(i - 1);
       }
       if (my_tiles > 0) mma3(my_tiles - 1);
@@ -253,37 +258,55 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       tc::mbar_arrive(&h_ready);
       if (prof && r == 0) s_ph[1] = clock64();
     }
-    double mae = 0.0;
+    // |d| sums: fp32 within a tile, four f64 chains across tiles, combined
+    // once at the end; the bias of tile i+1 is prefetched while tile i runs
+    double mae_e[4] = {0.0, 0.0, 0.0, 0.0};
+    const int out_pad = a.m.out_pad;
+    auto load_bias = [&](int i, float4* dst) {
+      const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+      const float4* bp = reinterpret_cast<const float4*>(bias_pad + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = c0 + 4 * q < out_pad ? __ldg(bp + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    float4 bnext[8];
+    if (my_tiles > 0) load_bias(0, bnext);
     for (int i = 0; i < my_tiles; ++i) {
       const int s = i % kStages;
       const int b = i & 1;
       const uint32_t phb = (uint32_t)(i >> 1) & 1u;
       const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+      float4 bcur[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bcur[q] = bnext[q];
+      if (i + 1 < my_tiles) load_bias(i + 1, bnext);
       tc::mbar_wait(&ofull[b], phb);
+      if (r == 0) LTFB_EV(i, 4);
       tc::tc_fence_after();
       float o[32];
       tc::tmem_ld32(T + lane_addr + kO0 + 32u * (uint32_t)b, o);
       unsigned char* yrow = Yp(s) + r * 128;
       unsigned char* lrow = Ylo(s) + r * 128;
-      const bool row_ok = r < rows;
+      const int nvalid = r < rows ? min(kTileN, out - c0) : 0;
+      // per-tile |d| partials in fp32 (8 terms each), folded into the f64
+      // accumulators once per tile: FP64 conversions and adds are the
+      // expensive operations of this loop on B200
+      float tsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t off = (uint32_t)(((q ^ (r & 7)) & 7) << 4);
-        float4 yh = *reinterpret_cast<const float4*>(yrow + off);
-        float4 yl = kPrecise ? *reinterpret_cast<const float4*>(lrow + off) : make_float4(0, 0, 0, 0);
-        const float yv[4] = {yh.x + yl.x, yh.y + yl.y, yh.z + yl.z, yh.w + yl.w};
+        const float4 yh = *reinterpret_cast<const float4*>(yrow + off);
+        const float4 yl = kPrecise ? *reinterpret_cast<const float4*>(lrow + off) : make_float4(0, 0, 0, 0);
+        const float yv[4] = {yh.x + yl.x, yh.y + yl.y, yh.z + yl.z, yh.w + yl.w};  // hi + lo == y exactly
+        const float bv[4] = {bcur[q].x, bcur[q].y, bcur[q].z, bcur[q].w};
         float sv[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int c = q * 4 + e;
-          float sg = 0.0f;
-          if (row_ok && c0 + c < out) {
-            const float of = o[c] + __ldg(bias_pad + c0 + c);
-            const double d = (double)of - (double)yv[e];
-            mae += fabs(d);
-            sg = d > 0 ? 1.0f : (d < 0 ? -1.0f : 0.0f);
-          }
-          sv[e] = sg;
+          const float of = o[c] + bv[e];  // dec forward output (mlp.hpp:209-213)
+          const bool ok = c < nvalid;
+          // loss.hpp:25-41: |p - t| (summed in double per tile below); sign(p - t), 0 at ties
+          tsum[e] += ok ? fabsf(of - yv[e]) : 0.0f;
+          sv[e] = ok ? (of > yv[e] ? 1.0f : (of < yv[e] ? -1.0f : 0.0f)) : 0.0f;
         }
         *reinterpret_cast<float4*>(lrow + off) = make_float4(sv[0], sv[1], sv[2], sv[3]);
       }
@@ -291,7 +314,11 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(&oempty[b]);
       tc::mbar_arrive(&sready[s]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) mae_e[e] += (double)tsum[e];
+      if (r == 0) LTFB_EV(i, 5);
     }
+    const double mae = (mae_e[0] + mae_e[1]) + (mae_e[2] + mae_e[3]);
     // ---- partials out ----
     tc::mbar_wait(&done, 0);
     tc::tc_fence_after();
@@ -322,29 +349,37 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       a.mae_part[blockIdx.x] = t;
     }
   } else {
-    // ------------------------------------------------- Y hi/lo split ----
+    // ------------------------------------------ tf32 hi / lo split ----
+    // precise mode: every fp32 operand tile of the stage (y, We, Wd) is split
+    // elementwise in place (hi) plus a lo copy at the same offset, so the
+    // swizzled layouts are untouched
     if (kPrecise) {
       const int t = threadIdx.x - 192;  // 0..127
+      auto split = [&](unsigned char* hi_p, unsigned char* lo_p, int n4) {
+        float4* hp = reinterpret_cast<float4*>(hi_p);
+        float4* lp = reinterpret_cast<float4*>(lo_p);
+#pragma unroll 4
+        for (int idx = t; idx < n4; idx += 128) {
+          const float4 v = hp[idx];
+          const float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
+          hp[idx] = h;
+          lp[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+      };
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
         const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         tc::mbar_wait(&full[s], ph);
-        float4* yh = reinterpret_cast<float4*>(Yp(s));
-        float4* yl = reinterpret_cast<float4*>(Ylo(s));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int idx = t + 128 * k;
-          const float4 v = yh[idx];
-          const float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
-          yh[idx] = h;
-          yl[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        }
+        if (t == 0) LTFB_EV(i, 1);
+        split(Yp(s), Ylo(s), kY / 16);
+        split(WeH(s), WeL(s), kWt / 16);
+        split(WdH(s), WdL(s), kWt / 16);
+        split(WtH(s), WtL(s), kWt / 16);
         tc::fence_proxy_async();
         tc::mbar_arrive(&split_done[s]);
+        if (t == 0) LTFB_EV(i, 2);
       }
     } else {
-      const int t = threadIdx.x - 192;
-      (void)t;
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % kStages;
         const uint32_t ph = (uint32_t)(i / kStages) & 1u;
@@ -421,8 +456,14 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     }
   }
   if (prof && threadIdx.x == 0)
+  {
     printf("wide phases (cycles): h %lld, tiles %lld, grid sync %lld, reduce %lld\n", s_ph[1] - s_ph[0],
            s_ph[2] - s_ph[0], s_ph[3] - s_ph[2], clock64() - s_ph[3]);
+    for (int i = 0; i < my_tiles && i < 16; ++i)
+      printf("  tile %d: issue %lld tma %lld split %lld mma12 %lld epi_in %lld epi_out %lld mma3 %lld\n", i,
+             s_ev[i][0] - s_ph[0], s_ev[i][1] - s_ph[0], s_ev[i][2] - s_ph[0], s_ev[i][3] - s_ph[0],
+             s_ev[i][4] - s_ph[0], s_ev[i][5] - s_ph[0], s_ev[i][6] - s_ph[0]);
+  }
 }
 
 // ----------------------------------------------------------------- host --
@@ -453,34 +494,32 @@ void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStr
 
 // Splits / transposes the frozen wide-layer weights into the K-major tf32
 // hi/lo copies the kernel streams (run whenever enc/dec change).
+/// Lays the frozen wide-layer weights out for K-major tcgen05 operands, in
+/// fp32 (split into tf32 hi / lo per tile in shared memory): WeT [64 x
+/// out_pad] (enc layer 0 transposed), Wd [64 x out_pad] (dec last layer,
+/// padded to a 16-B row pitch), WdT [out_pad x 64], bias [out_pad]; pad
+/// columns zero. Run whenever enc / dec change.
 __global__ void k_prep_wide(const float* __restrict__ enc, long long enc_w, const float* __restrict__ dec,
-                            long long dec_w, long long dec_b, int out, int out_pad, float* wet_hi,
-                            float* wet_lo, float* wd_hi, float* wd_lo, float* wdt_hi, float* wdt_lo,
+                            long long dec_w, long long dec_b, int out, int out_pad, float* wet, float* wd, float* wdt,
                             float* bias_pad) {
   const long long n = (long long)wt::kW * out_pad;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(i / out_pad), c = (int)(i % out_pad);
     const bool ok = c < out;
-    const float we = ok ? enc[enc_w + (long long)c * wt::kW + j] : 0.0f;  // enc W0 [out x 64]
-    const float wd = ok ? dec[dec_w + (long long)j * out + c] : 0.0f;     // dec W_last [64 x out]
-    const float weh = tc::tf32_hi(we), wdh = tc::tf32_hi(wd);
-    wet_hi[i] = weh;
-    wet_lo[i] = we - weh;
-    wd_hi[i] = wdh;
-    wd_lo[i] = wd - wdh;
-    wdt_hi[(long long)c * wt::kW + j] = wdh;
-    wdt_lo[(long long)c * wt::kW + j] = wd - wdh;
+    wet[i] = ok ? enc[enc_w + (long long)c * wt::kW + j] : 0.0f;  // enc W0 [out x 64]
+    const float w = ok ? dec[dec_w + (long long)j * out + c] : 0.0f;  // dec W_last [64 x out]
+    wd[i] = w;
+    wdt[(long long)c * wt::kW + j] = w;
     if (j == 0) bias_pad[c] = ok ? dec[dec_b + c] : 0.0f;
   }
 }
 
 void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t s) {
   k_prep_wide<<<592, 256, 0, s>>>(a.p[kEnc], a.m.enc_wide_w, a.p[kDec], a.m.dec_wide_w, a.m.dec_wide_b, a.m.out,
-                                  a.m.out_pad, p.wet_hi, p.wet_lo, p.wd_hi, p.wd_lo, p.wdt_hi, p.wdt_lo,
-                                  p.bias_pad);
+                                  a.m.out_pad, p.wet, p.wd, p.wdt, p.bias_pad);
 }
 
-static_assert(sizeof(WideTcParams) == 7 * 128, "CUtensorMap packing");
+static_assert(sizeof(WideTcParams) == 4 * 128, "CUtensorMap packing");
 
 namespace {
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -521,12 +560,9 @@ void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, i
   WideTcParams tp;
   const uint64_t op = (uint64_t)a.m.out_pad;
   encode_2d(&tp.tm_y, yb, op, (uint64_t)yb_rows, 32, 128);
-  encode_2d(&tp.tm_wet_hi, p.wet_hi, op, wt::kW, 32, 64);
-  encode_2d(&tp.tm_wet_lo, p.wet_lo, op, wt::kW, 32, 64);
-  encode_2d(&tp.tm_wd_hi, p.wd_hi, op, wt::kW, 32, 64);
-  encode_2d(&tp.tm_wd_lo, p.wd_lo, op, wt::kW, 32, 64);
-  encode_2d(&tp.tm_wdt_hi, p.wdt_hi, wt::kW, op, 32, 32);
-  encode_2d(&tp.tm_wdt_lo, p.wdt_lo, wt::kW, op, 32, 32);
+  encode_2d(&tp.tm_wet, p.wet, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wd, p.wd, op, wt::kW, 32, 64);
+  encode_2d(&tp.tm_wdt, p.wdt, wt::kW, op, 32, 32);
   std::memcpy(p.maps, &tp, sizeof tp);
 }
 

@@ -16,20 +16,17 @@ void launch_wide_generic(const StepArgs& a, cudaStream_t s);
 bool wide_tc_supported(const StepArgs& a);
 void launch_wide_tc(const StepArgs& a, cudaStream_t s);
 
-/// Host-side state of the tcgen05 wide pass: K-major tf32 hi/lo copies of
-/// the frozen wide-layer weights and the TMA descriptors over them.
+/// Host-side state of the tcgen05 wide pass: K-major fp32 copies of the
+/// frozen wide-layer weights, the padded bias, and the TMA descriptors.
 struct WideTcParamsHost {
-  alignas(64) unsigned char maps[7 * 128];  // CUtensorMap x7 (y, WeT hi/lo, Wd hi/lo, WdT hi/lo)
+  alignas(64) unsigned char maps[4 * 128];  // CUtensorMap x4 (y, WeT, Wd, WdT)
   alignas(64) unsigned char y_alt[2][128];  // y maps of the host-streamed (e2e) minibatch buffers
   int y_sel = -1;                           // -1: maps[0] (gathered minibatch), else y_alt[y_sel]
   bool precise = true;
   float* bias_pad = nullptr;
-  float* wet_hi = nullptr;
-  float* wet_lo = nullptr;
-  float* wd_hi = nullptr;
-  float* wd_lo = nullptr;
-  float* wdt_hi = nullptr;
-  float* wdt_lo = nullptr;
+  float* wet = nullptr;
+  float* wd = nullptr;
+  float* wdt = nullptr;
 };
 /// Builds the TMA descriptors (yb is [yb_rows x out_pad]).
 void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows);

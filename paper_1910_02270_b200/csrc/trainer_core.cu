@@ -183,16 +183,13 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
 
   if (wide_kind_ >= 2) {
     const std::size_t nw = 64 * static_cast<std::size_t>(ma.out_pad);
-    for (auto* b : {&wet_hi_, &wet_lo_, &wd_hi_, &wd_lo_, &wdt_hi_, &wdt_lo_}) b->alloc(nw);
+    for (auto* b : {&wet_, &wd_, &wdt_}) b->alloc(nw);
     bias_pad_.alloc(ma.out_pad);
     wtp_.precise = wide_kind_ == 2;
     wtp_.bias_pad = bias_pad_.p;
-    wtp_.wet_hi = wet_hi_.p;
-    wtp_.wet_lo = wet_lo_.p;
-    wtp_.wd_hi = wd_hi_.p;
-    wtp_.wd_lo = wd_lo_.p;
-    wtp_.wdt_hi = wdt_hi_.p;
-    wtp_.wdt_lo = wdt_lo_.p;
+    wtp_.wet = wet_.p;
+    wtp_.wd = wd_.p;
+    wtp_.wdt = wdt_.p;
     ltfb_dev::encode_wide_maps(wtp_, a, yb_.p, static_cast<int>(yb_rows));
   }
   // post kernel: compile-time-shaped instance when the model matches one,

@@ -192,8 +192,8 @@ class DeviceTrainer {
   DevBuf<float> sx_, sy_;
   DevBuf<unsigned> perm_[2];
   DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
-  // tcgen05 wide pass: K-major tf32 hi/lo copies of the frozen weights
-  DevBuf<float> wet_hi_, wet_lo_, wd_hi_, wd_lo_, wdt_hi_, wdt_lo_, bias_pad_;
+  // tcgen05 wide pass: K-major fp32 copies of the frozen wide-layer weights + bias
+  DevBuf<float> wet_, wd_, wdt_, bias_pad_;
   ltfb_dev::WideTcParamsHost wtp_{};
   bool wide_dirty_ = false;
   DevBuf<double> mae_part_, mae_total_, adam_c_;

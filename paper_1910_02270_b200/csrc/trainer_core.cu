@@ -155,6 +155,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   a.abort_threshold = spec_.numeric_abort_threshold;
   a.rec_cap = static_cast<int>(rec_.n);
   a.phase_prof = std::getenv("LTFB_PHASE_PROF") ? 1 : 0;
+  graphs_on_ = !std::getenv("LTFB_NO_GRAPH") && !a.phase_prof;
   a.small_ctas = std::max(1, (B + 15) / 16);
   const auto& h = spec_.arch.adam;
   for (int i = 0; i < 5; ++i) a.lr[i] = spec_.lr[i] > 0 ? spec_.lr[i] : h.lr;
@@ -214,6 +215,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
 DeviceTrainer::~DeviceTrainer() {
   DeviceGuard g(spec_.device);
   if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (int i = 0; i < 2; ++i) {
     if (pinned_perm_[i]) cudaFreeHost(pinned_perm_[i]);
     if (perm_ev_[i]) cudaEventDestroy(perm_ev_[i]);
@@ -589,12 +591,61 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
         for (std::size_t r = ranges[s].first; r < ranges[s].second; ++r)
           if (owner_[slots[begin + r]] >= 0 && owner_[slots[begin + r]] != s) ++epoch_shuffled_;
     }
+    // a run of steps inside this epoch goes out as one CUDA graph launch
+    const std::size_t run = std::min<std::size_t>(n - i, steps_per_epoch_ - step_in_epoch_);
+    if (run >= 2 && spec_.n_shards == 1 && launch_graph(run)) {
+      step_in_epoch_ += run;
+      epoch_steps_ += run;
+      host_step_ += run;
+      i += run - 1;
+      continue;
+    }
     launch_step();
     ++step_in_epoch_;
     ++epoch_steps_;
     ++host_step_;
   }
   LTFB_CUDA(cudaGetLastError());
+}
+
+bool DeviceTrainer::launch_graph(std::size_t steps) {
+  if (!graphs_on_ || ktime_on_) return false;
+  if (wide_kind_ >= 2 && wide_dirty_) {  // weight re-layout stays outside the graph
+    ltfb_dev::launch_prep_wide(args_, wtp_, stream_);
+    ++launches_;
+    wide_dirty_ = false;
+  }
+  if (std::memcmp(&graph_args_, &args_, sizeof args_) != 0) {  // pointers or layout changed
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    graphs_.clear();
+    graph_args_ = args_;
+  }
+  auto it = graphs_.find(steps);
+  if (it == graphs_.end()) {
+    const std::uint64_t l0 = launches_;
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      graphs_on_ = false;
+      return false;
+    }
+    for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true);
+    const cudaError_t e = cudaStreamEndCapture(stream_, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (e != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      graphs_on_ = false;  // capture unsupported here: plain launches from now on
+      launches_ = l0;
+      return false;
+    }
+    cudaGraphDestroy(graph);
+    graph_launches_[steps] = launches_ - l0;
+    launches_ = l0;
+    it = graphs_.emplace(steps, exec).first;
+  }
+  LTFB_CUDA(cudaGraphLaunch(it->second, stream_));
+  launches_ += graph_launches_[steps];
+  return true;
 }
 
 bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepRecord>& out) {

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -172,6 +173,9 @@ class DeviceTrainer {
   void launch_step();
   void close_epoch_segment(bool epoch_done, bool partial);
   void launch_step_kernels(bool gather);
+  /// Runs `steps` steps of the current epoch as one cached CUDA graph;
+  /// false if graphs are off or capture is unsupported (caller launches).
+  bool launch_graph(std::size_t steps);
 
   TrainerSpec spec_;
   ltfb::nn::MlpSpec specs_[5];
@@ -185,6 +189,10 @@ class DeviceTrainer {
   bool post_fast_ = false;
   int post_tpl_ = 0;
   std::uint64_t launches_ = 0;
+  bool graphs_on_ = true;
+  std::map<std::size_t, cudaGraphExec_t> graphs_;
+  std::map<std::size_t, std::uint64_t> graph_launches_;
+  ltfb_dev::StepArgs graph_args_{};
 
   DevBuf<float> params_[5], mom1_[5], mom2_[5], grads_[5];
   DevBuf<float> gen_;       // [fwd | inv] contiguous (exchange payload)

@@ -39,23 +39,42 @@ __device__ __forceinline__ int batch_rows(const StepArgs& a) {
 // h in HBM/L2 without a separate launch.
 __device__ void row_h(const StepArgs& a, int r, unsigned slot) {
   __shared__ float act[2][kMaxSmallWidth];
+  __shared__ float wbuf[6144];  // fwd + dec-head blobs (one cp.async round trip)
   const ModelArgs& m = a.m;
   const int t = threadIdx.x;
-  if (t < m.in) act[0][t] = a.x_from_store ? a.sx[(long long)slot * m.in + t] : a.xb[r * m.in + t];
+  const NetDesc* nets[2] = {&m.fwd, &m.dec_head};
+  const float* blobs[2] = {a.p[kFwd] + m.fwd.base, a.p[kDec] + m.dec_head.base};
+  const int cnt0 = (int)m.fwd.count, cnt1 = (int)m.dec_head.count;
+  const bool staged = cnt0 + cnt1 <= 6144;
+  if (staged) {
+    for (int i = t; i < cnt0 + cnt1; i += blockDim.x) {
+      const float* src = i < cnt0 ? blobs[0] + i : blobs[1] + (i - cnt0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(wbuf + i)),
+                   "l"(src)
+                   : "memory");
+    }
+  }
+  if (t < m.in) {
+    const float x = a.x_from_store ? a.sx[(long long)slot * m.in + t] : a.xb[r * m.in + t];
+    act[0][t] = x;
+    if (a.x_from_store) a.xb[r * m.in + t] = x;  // the minibatch x for the small nets
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   int cur = 0;
   for (int net = 0; net < 2; ++net) {
-    const NetDesc& n = net == 0 ? m.fwd : m.dec_head;
-    const float* blob = a.p[net == 0 ? kFwd : kDec];
+    const NetDesc& n = *nets[net];
+    const float* blob = staged ? wbuf + (net == 0 ? 0 : cnt0) : blobs[net];
     for (int l = 0; l < n.L; ++l) {
       const int in = n.w[l], out = n.w[l + 1];
-      const float* W = blob + n.off_w[l];
+      const float* W = blob + (n.off_w[l] - n.base);
+      const float* bb = blob + (n.off_b[l] - n.base);
       const bool last = net == 1 && l + 1 == n.L;
       for (int j = t; j < out; j += blockDim.x) {
         float acc = 0.0f;
 #pragma unroll 8
-        for (int k = 0; k < in; ++k) acc = fmaf(act[cur][k], W[(long long)k * out + j], acc);
-        const float v = act_apply(n.act[l], n.slope[l], acc + blob[n.off_b[l] + j]);
+        for (int k = 0; k < in; ++k) acc = fmaf(act[cur][k], W[k * out + j], acc);
+        const float v = act_apply(n.act[l], n.slope[l], acc + bb[j]);
         if (last) a.h[(long long)r * out + j] = v;
         else act[cur ^ 1][j] = v;
       }
@@ -224,10 +243,10 @@ void launch_gather(const StepArgs& a, cudaStream_t s) {
   k_gather<<<dim3(gx + (a.h_in_gather ? 1 : 0), a.B), 256, 0, s>>>(a);
 }
 
-void launch_row_h(const StepArgs& a, cudaStream_t s) {
-  StepArgs b = a;  // h only: one CTA per row, x from the streamed minibatch
+void launch_row_h(const StepArgs& a, bool x_from_store, cudaStream_t s) {
+  StepArgs b = a;  // no copy columns: every CTA is a row_h CTA
   b.h_in_gather = 1;
-  b.x_from_store = 0;
+  b.x_from_store = x_from_store ? 1 : 0;
   k_gather<<<dim3(1, a.B), 256, 0, s>>>(b);
 }
 

@@ -47,12 +47,14 @@ constexpr int kRows = 128;                 // MMA M (minibatch rows)
 constexpr int kW = 64;                     // E1 == D == 64
 constexpr uint32_t kY = 16384;             // [128 x 32] f32
 constexpr uint32_t kWt = 8192;             // [64 x 32] f32
-constexpr uint32_t kStage = 2 * kY + 6 * kWt;  // Y (hi), Ylo/S, WeT hi/lo, Wd hi/lo, WdT hi/lo
-constexpr int kStages = 2;
+constexpr uint32_t kStage = kY + 6 * kWt;  // y (raw), WeT hi/lo, Wd hi/lo, WdT hi/lo
+constexpr int kStages = 3;
 constexpr uint32_t kSmem = kStages * kStage + 1024;
 constexpr int kThreads = 320;
 // TMEM columns
 constexpr uint32_t kPenc = 0, kPdec = 64, kO0 = 128, kHhi = 192, kHlo = 256;
+constexpr uint32_t kYbase = 320;  // + 64 s: y hi [32], y lo / S [32] of stage s
+static_assert(kYbase + 64 * kStages <= 512, "TMEM columns");
 }  // namespace wt
 
 struct WideTcParams {
@@ -105,15 +107,15 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   auto stage_ptr = [&](int s) { return sm + s * kStage; };
-  // stage layout
-  auto Yp = [&](int s) { return stage_ptr(s); };
-  auto Ylo = [&](int s) { return stage_ptr(s) + kY; };
-  auto WeH = [&](int s) { return stage_ptr(s) + 2 * kY; };            // WeT [64 j x 32 c] SW128
-  auto WeL = [&](int s) { return stage_ptr(s) + 2 * kY + kWt; };
-  auto WdH = [&](int s) { return stage_ptr(s) + 2 * kY + 2 * kWt; };   // Wd  [64 j x 32 c] SW128
-  auto WdL = [&](int s) { return stage_ptr(s) + 2 * kY + 3 * kWt; };
-  auto WtH = [&](int s) { return stage_ptr(s) + 2 * kY + 4 * kWt; };   // WdT [32 c x 64 j] as 2 K-blocks
-  auto WtL = [&](int s) { return stage_ptr(s) + 2 * kY + 5 * kWt; };
+  auto Yraw = [&](int s) { return stage_ptr(s); };                      // y tile [128 x 32] SW128 (gather4)
+  auto WeH = [&](int s) { return stage_ptr(s) + kY; };                  // WeT [64 j x 32 c] SW128
+  auto WeL = [&](int s) { return stage_ptr(s) + kY + kWt; };
+  auto WdH = [&](int s) { return stage_ptr(s) + kY + 2 * kWt; };        // Wd  [64 j x 32 c] SW128
+  auto WdL = [&](int s) { return stage_ptr(s) + kY + 3 * kWt; };
+  auto WtH = [&](int s) { return stage_ptr(s) + kY + 4 * kWt; };        // WdT [32 c x 64 j] as 2 K-blocks
+  auto WtL = [&](int s) { return stage_ptr(s) + kY + 5 * kWt; };
+  auto tYh = [&](int s) { return (uint32_t)(kYbase + 64 * s); };        // TMEM y hi   [128 x 32]
+  auto tYl = [&](int s) { return (uint32_t)(kYbase + 64 * s + 32); };   // TMEM y lo, then S
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -144,66 +146,68 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
-    if (lane == 0) {
-      const uint32_t bytes = kY + 3 * kWt;  // fp32 tiles: y, WeT, Wd, WdT
-      for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+    // y rows come straight from the HBM data store (epoch_plan.hpp:106-137,
+    // store.hpp:140-181): lane l gathers rows 4l..4l+3 of the step with one
+    // tile::gather4 per tile, so no separate gather kernel or minibatch copy
+    int rw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = 4 * lane + u;
+      if (a.y_identity) {
+        rw[u] = rr;  // host-streamed minibatch buffer
+      } else {
+        const unsigned* perm = a.perm[a.ctr->epoch & 1] + (long long)a.ctr->step_in_epoch * a.B;
+        rw[u] = (int)perm[rr < rows ? rr : 0];
+      }
+    }
+    const uint32_t bytes = kY + 3 * kWt;  // fp32 tiles: y, WeT, Wd, WdT
+    for (int i = 0; i < my_tiles; ++i) {
+      const int s = i % kStages;
+      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+      const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
+      if (lane == 0) {
         if (i >= kStages) tc::mbar_wait(&empty[s], ph ^ 1u);
-        const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
         LTFB_EV(i, 0);
         tc::mbar_expect_tx(&full[s], bytes);
-        tc::tma_load_2d(Yp(s), &tp.tm_y, &full[s], c0, 0);
         tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
         tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
         tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
         tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
       }
+      __syncwarp();
+      tc::tma_gather4(Yraw(s) + 512 * lane, &tp.tm_y, &full[s], c0, rw[0], rw[1], rw[2], rw[3]);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer --
+    // A operands (y hi / lo, h hi / lo, S) live in TMEM; B operands are the
+    // K-major weight tiles in shared memory
     if (lane == 0) {
-      // every B operand K-major (tf32 MN-major operands would need the
-      // 32-B-atom swizzle, incompatible with Wd's K-major use in MMA3)
       const uint32_t i_enc = tc::idesc_tf32(128, 64, 0, 0);
       const uint32_t i_dec = tc::idesc_tf32(128, 32, 0, 0);
-      const uint32_t i_ga = i_enc;
-      auto mma3 = [&](int j) {
+      auto mma3 = [&](int j) {  // P_dec += S Wd^T  (S exact in tf32: S*hi + S*lo)
         const int s = j % kStages;
-        const uint32_t ph = (uint32_t)(j / kStages) & 1u;
-        tc::mbar_wait(&sready[s], ph);
         tc::tc_fence_after();
-        const uint32_t sA = tc::smem_u32(Ylo(s));  // S overwrote Ylo
+        const uint32_t wdh = tc::smem_u32(WdH(s)), wdl = tc::smem_u32(WdL(s));
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = tc::sdesc_sw128(sA + 32 * kk, 16, 1024);
-          tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdH(s)) + 32 * kk, 16, 1024), i_ga,
+          tc::mma_tf32_ts(T + kPdec, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdh + 32 * kk, 16, 1024), i_enc,
                           (j > 0 || kk > 0) ? 1u : 0u);
           if (kPrecise)
-            tc::mma_tf32_ss(T + kPdec, ad, tc::sdesc_sw128(tc::smem_u32(WdL(s)) + 32 * kk, 16, 1024), i_ga, 1u);
+            tc::mma_tf32_ts(T + kPdec, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdl + 32 * kk, 16, 1024), i_enc, 1u);
         }
-        tc::tc_commit(&empty[s]);
+        tc::tc_commit(&empty[s]);  // frees the stage for the producer
         LTFB_EV(j, 6);
       };
-      for (int i = 0; i < my_tiles; ++i) {
+      auto mma12 = [&](int i) {
         const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         const int b = i & 1;
-        const uint32_t phb = (uint32_t)(i >> 1) & 1u;
-        tc::mbar_wait(&split_done[s], ph);
         tc::tc_fence_after();
-        if (i >= 2) {
-          tc::mbar_wait(&oempty[b], phb ^ 1u);
-          tc::tc_fence_after();
-        }
-        const uint32_t yh = tc::smem_u32(Yp(s)), yl = tc::smem_u32(Ylo(s));
         const uint32_t weh = tc::smem_u32(WeH(s)), wel = tc::smem_u32(WeL(s));
         for (int kk = 0; kk < 4; ++kk) {  // MMA1: P_enc += Y We  (K = 8 c per step)
-          const uint64_t ah = tc::sdesc_sw128(yh + 32 * kk, 16, 1024);
           const uint64_t bh = tc::sdesc_sw128(weh + 32 * kk, 16, 1024);
-          tc::mma_tf32_ss(T + kPenc, ah, bh, i_enc, (i > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_tf32_ts(T + kPenc, T + tYh(s) + 8 * kk, bh, i_enc, (i > 0 || kk > 0) ? 1u : 0u);
           if (kPrecise) {
-            tc::mma_tf32_ss(T + kPenc, tc::sdesc_sw128(yl + 32 * kk, 16, 1024), bh, i_enc, 1u);
-            tc::mma_tf32_ss(T + kPenc, ah, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc, 1u);
+            tc::mma_tf32_ts(T + kPenc, T + tYl(s) + 8 * kk, bh, i_enc, 1u);
+            tc::mma_tf32_ts(T + kPenc, T + tYh(s) + 8 * kk, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc, 1u);
           }
         }
         if (i == 0) {  // h is needed from MMA2 on
@@ -223,9 +227,31 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         }
         tc::tc_commit(&ofull[b]);
         LTFB_EV(i, 3);
-        if (i >= 1) mma3(i - 1);
+      };
+      // dynamic order: MMA3 of a tile goes out as soon as its S is ready (so
+      // the stage returns to the producer at once), MMA1/2 of the next tile
+      // as soon as its operands are staged
+      int n12 = 0, n3 = 0;
+      while (n3 < my_tiles) {
+        bool issued = false;
+        if (n3 < n12) {
+          const int s = n3 % kStages;
+          if (tc::mbar_test(&sready[s], (uint32_t)(n3 / kStages) & 1u)) {
+            mma3(n3++);
+            issued = true;
+          }
+        }
+        if (n12 < my_tiles) {
+          const int s = n12 % kStages;
+          const bool staged = tc::mbar_test(&split_done[s], (uint32_t)(n12 / kStages) & 1u);
+          const bool obuf = n12 < 2 || tc::mbar_test(&oempty[n12 & 1], ((uint32_t)(n12 >> 1) & 1u) ^ 1u);
+          if (staged && obuf) {
+            mma12(n12++);
+            issued = true;
+          }
+        }
+        if (!issued) __nanosleep(20);
       }
-      if (my_tiles > 0) mma3(my_tiles - 1);
       tc::tc_commit(&done);
     }
   } else if (warp >= 2 && warp < 6) {
@@ -233,7 +259,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    {  // h = dec_head(fwd(x)) (computed by k_gather / k_pre) -> TMEM as tf32 hi / lo
+    {  // h = dec_head(fwd(x)) (computed by the row kernel / k_pre) -> TMEM as tf32 hi / lo
       float4 hv[16];  // the row's 64 floats, all loads in flight at once
       const float4* hrow = reinterpret_cast<const float4*>(a.h + (long long)r * kW);
 #pragma unroll
@@ -282,35 +308,27 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       tc::mbar_wait(&ofull[b], phb);
       if (r == 0) LTFB_EV(i, 4);
       tc::tc_fence_after();
-      float o[32];
+      float o[32], yh[32], yl[32];
       tc::tmem_ld32(T + lane_addr + kO0 + 32u * (uint32_t)b, o);
-      unsigned char* yrow = Yp(s) + r * 128;
-      unsigned char* lrow = Ylo(s) + r * 128;
+      tc::tmem_ld32(T + lane_addr + tYh(s), yh);
+      if (kPrecise) tc::tmem_ld32(T + lane_addr + tYl(s), yl);
       const int nvalid = r < rows ? min(kTileN, out - c0) : 0;
       // per-tile |d| partials in fp32 (8 terms each), folded into the f64
       // accumulators once per tile: FP64 conversions and adds are the
       // expensive operations of this loop on B200
       float tsum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float sv[32];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t off = (uint32_t)(((q ^ (r & 7)) & 7) << 4);
-        const float4 yh = *reinterpret_cast<const float4*>(yrow + off);
-        const float4 yl = kPrecise ? *reinterpret_cast<const float4*>(lrow + off) : make_float4(0, 0, 0, 0);
-        const float yv[4] = {yh.x + yl.x, yh.y + yl.y, yh.z + yl.z, yh.w + yl.w};  // hi + lo == y exactly
-        const float bv[4] = {bcur[q].x, bcur[q].y, bcur[q].z, bcur[q].w};
-        float sv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = q * 4 + e;
-          const float of = o[c] + bv[e];  // dec forward output (mlp.hpp:209-213)
-          const bool ok = c < nvalid;
-          // loss.hpp:25-41: |p - t| (summed in double per tile below); sign(p - t), 0 at ties
-          tsum[e] += ok ? fabsf(of - yv[e]) : 0.0f;
-          sv[e] = ok ? (of > yv[e] ? 1.0f : (of < yv[e] ? -1.0f : 0.0f)) : 0.0f;
-        }
-        *reinterpret_cast<float4*>(lrow + off) = make_float4(sv[0], sv[1], sv[2], sv[3]);
+      for (int c = 0; c < 32; ++c) {
+        const float yv = kPrecise ? yh[c] + yl[c] : yh[c];  // hi + lo == y exactly
+        const float bq[4] = {bcur[c / 4].x, bcur[c / 4].y, bcur[c / 4].z, bcur[c / 4].w};
+        const float of = o[c] + bq[c % 4];  // dec forward output (mlp.hpp:209-213)
+        const bool ok = c < nvalid;
+        // loss.hpp:25-41: |p - t| (summed in double per tile below); sign(p - t), 0 at ties
+        tsum[c % 4] += ok ? fabsf(of - yv) : 0.0f;
+        sv[c] = ok ? (of > yv ? 1.0f : (of < yv ? -1.0f : 0.0f)) : 0.0f;
       }
-      tc::fence_proxy_async();
+      tc::tmem_st32(T + lane_addr + tYl(s), sv);  // S replaces y lo (MMA1 has consumed it)
       tc::tc_fence_before();
       tc::mbar_arrive(&oempty[b]);
       tc::mbar_arrive(&sready[s]);
@@ -349,43 +367,57 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       a.mae_part[blockIdx.x] = t;
     }
   } else {
-    // ------------------------------------------ tf32 hi / lo split ----
-    // precise mode: every fp32 operand tile of the stage (y, We, Wd) is split
-    // elementwise in place (hi) plus a lo copy at the same offset, so the
-    // swizzled layouts are untouched
-    if (kPrecise) {
-      const int t = threadIdx.x - 192;  // 0..127
-      auto split = [&](unsigned char* hi_p, unsigned char* lo_p, int n4) {
-        float4* hp = reinterpret_cast<float4*>(hi_p);
-        float4* lp = reinterpret_cast<float4*>(lo_p);
+    // ------------------------------------------------- operand staging ----
+    // thread t owns minibatch row r (its TMEM lane): the gathered y row goes
+    // into TMEM as tf32 hi / lo (the A operand of MMA1 and the epilogue's y);
+    // in precise mode the weight tiles are split in place in shared memory
+    // (hi, plus a lo copy at the same swizzled offset)
+    const int t = threadIdx.x - 192;  // 0..127
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    auto split = [&](unsigned char* hi_p, unsigned char* lo_p, int n4) {
+      float4* hp = reinterpret_cast<float4*>(hi_p);
+      float4* lp = reinterpret_cast<float4*>(lo_p);
 #pragma unroll 4
-        for (int idx = t; idx < n4; idx += 128) {
-          const float4 v = hp[idx];
-          const float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
-          hp[idx] = h;
-          lp[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      for (int idx = t; idx < n4; idx += 128) {
+        const float4 v = hp[idx];
+        const float4 h = make_float4(tc::tf32_hi(v.x), tc::tf32_hi(v.y), tc::tf32_hi(v.z), tc::tf32_hi(v.w));
+        hp[idx] = h;
+        lp[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+    };
+    for (int i = 0; i < my_tiles; ++i) {
+      const int s = i % kStages;
+      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+      tc::mbar_wait(&full[s], ph);
+      if (t == 0) LTFB_EV(i, 1);
+      {
+        const unsigned char* yrow = Yraw(s) + r * 128;
+        float v[32], vl[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t off = (uint32_t)(((q ^ (r & 7)) & 7) << 4);
+          const float4 y4 = *reinterpret_cast<const float4*>(yrow + off);
+          const float ys[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[4 * q + e] = kPrecise ? tc::tf32_hi(ys[e]) : ys[e];
+            vl[4 * q + e] = ys[e] - v[4 * q + e];
+          }
         }
-      };
-      for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-        tc::mbar_wait(&full[s], ph);
-        if (t == 0) LTFB_EV(i, 1);
-        split(Yp(s), Ylo(s), kY / 16);
+        tc::tmem_st32(T + lane_addr + tYh(s), v);
+        if (kPrecise) tc::tmem_st32(T + lane_addr + tYl(s), vl);
+      }
+      if (kPrecise) {
         split(WeH(s), WeL(s), kWt / 16);
         split(WdH(s), WdL(s), kWt / 16);
         split(WtH(s), WtL(s), kWt / 16);
         tc::fence_proxy_async();
-        tc::mbar_arrive(&split_done[s]);
-        if (t == 0) LTFB_EV(i, 2);
       }
-    } else {
-      for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-        tc::mbar_wait(&full[s], ph);
-        tc::mbar_arrive(&split_done[s]);
-      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&split_done[s]);
+      if (t == 0) LTFB_EV(i, 2);
     }
   }
   tc::tc_fence_before();
@@ -398,61 +430,66 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   if (prof && threadIdx.x == 0) s_ph[3] = clock64();
   {
     // float4 outputs [rows x 64] of P_enc then of P_dec; CTA c owns a
-    // contiguous slice; 8 thread groups sum partials s = g, g+8, ... in
-    // ascending order, then the 8 group sums are added in group order.
-    constexpr int kG = 8, kPer = kThreads / kG;  // 40 outputs per pass
+    // contiguous slice of <= kMaxQ outputs. Thread (g, o) sums partials
+    // s = g, g + G, ... of output o (all loads issued before the adds, one
+    // L2 round trip), then the G group sums are added in group order: a
+    // fixed summation order, so the result is run-to-run deterministic.
+    constexpr int kMaxQ = 32;
     const int q_enc = rows * (kW / 4), q_all = 2 * q_enc;
     const int lo = (int)((long long)q_all * blockIdx.x / gridDim.x);
     const int hi = (int)((long long)q_all * (blockIdx.x + 1) / gridDim.x);
-    float4* part = reinterpret_cast<float4*>(sm);  // [kG][kPer]
-    const int g = threadIdx.x / kPer, o = threadIdx.x % kPer;
+    const int nq = hi - lo;  // <= kMaxQ for the shapes the kernel accepts
+    float4* part = reinterpret_cast<float4*>(sm);  // [G][kMaxQ]
+    const int G = kThreads / kMaxQ;                // 10 groups
+    const int g = threadIdx.x / kMaxQ, o = threadIdx.x % kMaxQ;
     const long long pstride4 = (long long)a.B * kW / 4;
-    float4* red_enc = reinterpret_cast<float4*>(a.scratch + a.L.red_enc);
-    float4* red_dec = reinterpret_cast<float4*>(a.scratch + a.L.red_dec);
-    for (int base = lo; base < hi; base += kPer) {
-      const int q = base + o;
-      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      if (q < hi) {
-        const bool enc = q < q_enc;
-        const float4* src = reinterpret_cast<const float4*>(enc ? a.P_enc : a.P_dec) + (enc ? q : q - q_enc);
-        for (int s0 = g; s0 < a.S; s0 += 8 * kG) {  // 8 loads in flight, summed in order
-          float4 v[8];
+    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (o < nq) {
+      const int q = lo + o;
+      const bool enc = q < q_enc;
+      const float4* src = reinterpret_cast<const float4*>(enc ? a.P_enc : a.P_dec) + (enc ? q : q - q_enc);
+      constexpr int kMaxPer = 16;  // ceil(148 / 10)
+      float4 v[kMaxPer];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int sidx = s0 + u * kG;
-            v[u] = sidx < a.S ? __ldcg(src + sidx * pstride4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-          }
+      for (int u = 0; u < kMaxPer; ++u) {
+        const int sidx = g + u * G;
+        v[u] = sidx < a.S ? __ldcg(src + sidx * pstride4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (s0 + u * kG < a.S) {
-              acc.x += v[u].x;
-              acc.y += v[u].y;
-              acc.z += v[u].z;
-              acc.w += v[u].w;
-            }
-          }
+      for (int u = 0; u < kMaxPer; ++u) {
+        if (g + u * G < a.S) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+          acc.z += v[u].z;
+          acc.w += v[u].w;
         }
       }
-      part[g * kPer + o] = acc;
-      __syncthreads();
-      if (g == 0 && q < hi) {
-        float4 t = part[o];
-        for (int k = 1; k < kG; ++k) {
-          const float4 v = part[k * kPer + o];
-          t.x += v.x;
-          t.y += v.y;
-          t.z += v.z;
-          t.w += v.w;
-        }
-        if (q < q_enc) red_enc[q] = t;
-        else red_dec[q - q_enc] = t;
-      }
-      __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      double t = 0.0;
-      for (int sidx = 0; sidx < a.S; ++sidx) t += __ldcg(a.mae_part + sidx);
-      *a.mae_total = t;
+    part[g * kMaxQ + o] = acc;
+    __syncthreads();
+    if (g == 0 && o < nq) {
+      float4 t = part[o];
+      for (int k = 1; k < G; ++k) {
+        const float4 w = part[k * kMaxQ + o];
+        t.x += w.x;
+        t.y += w.y;
+        t.z += w.z;
+        t.w += w.w;
+      }
+      const int q = lo + o;
+      float4* red_enc = reinterpret_cast<float4*>(a.scratch + a.L.red_enc);
+      float4* red_dec = reinterpret_cast<float4*>(a.scratch + a.L.red_dec);
+      if (q < q_enc) red_enc[q] = t;
+      else red_dec[q - q_enc] = t;
+    }
+    if (blockIdx.x == 0 && warp == 0) {  // MAE total: lanes own strided partials, fixed xor tree
+      double v[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) v[u] = lane + 32 * u < a.S ? __ldcg(a.mae_part + lane + 32 * u) : 0.0;
+      double t = (((v[0] + v[1]) + v[2]) + v[3]) + v[4];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      if (lane == 0) *a.mae_total = t;
     }
   }
   if (prof && threadIdx.x == 0)
@@ -468,7 +505,9 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
 
 // ----------------------------------------------------------------- host --
 bool wide_tc_supported(const StepArgs& a) {
-  return a.m.E1 == wt::kW && a.m.D == wt::kW && a.B <= wt::kRows && a.m.out >= wt::kTileN;
+  // one CTA per SM (<= 160 partials for the in-kernel reduction's 10 x 16 loads)
+  return a.m.E1 == wt::kW && a.m.D == wt::kW && a.B <= wt::kRows && a.m.out >= wt::kTileN && a.S <= 160 &&
+         (2 * a.B * (wt::kW / 4) + a.S - 1) / a.S <= 32;
 }
 
 void launch_wide_tc(const StepArgs&, cudaStream_t) {
@@ -550,16 +589,17 @@ void encode_2d(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows, 
 }
 }  // namespace
 
+// y maps are read by tile::gather4: box = one row of 32 columns
 void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows) {
   CUtensorMap m;
-  encode_2d(&m, yb, (uint64_t)a.m.out_pad, (uint64_t)yb_rows, 32, 128);
-  std::memcpy(p.y_alt[which], &m, sizeof m);
+  encode_2d(&m, yb, (uint64_t)a.m.out_pad, (uint64_t)yb_rows, 32, 1);
+  std::memcpy(which < 0 ? p.maps : p.y_alt[which], &m, sizeof m);
 }
 
 void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows) {
   WideTcParams tp;
   const uint64_t op = (uint64_t)a.m.out_pad;
-  encode_2d(&tp.tm_y, yb, op, (uint64_t)yb_rows, 32, 128);
+  encode_2d(&tp.tm_y, yb, op, (uint64_t)yb_rows, 32, 1);
   encode_2d(&tp.tm_wet, p.wet, op, wt::kW, 32, 64);
   encode_2d(&tp.tm_wd, p.wd, op, wt::kW, 32, 64);
   encode_2d(&tp.tm_wdt, p.wdt, wt::kW, op, 32, 32);

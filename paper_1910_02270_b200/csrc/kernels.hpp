@@ -9,8 +9,9 @@
 namespace ltfb_dev {
 
 void launch_gather(const StepArgs& a, cudaStream_t s);
-/// h = dec_head(fwd(xb)) per row only (the host-streamed minibatch path).
-void launch_row_h(const StepArgs& a, cudaStream_t s);
+/// One CTA per minibatch row: x from the store through the epoch plan (also
+/// written to xb) or from xb, then h = dec_head(fwd(x)).
+void launch_row_h(const StepArgs& a, bool x_from_store, cudaStream_t s);
 void launch_pre(const StepArgs& a, cudaStream_t s);
 void launch_wide_generic(const StepArgs& a, cudaStream_t s);
 bool wide_tc_supported(const StepArgs& a);
@@ -30,6 +31,8 @@ struct WideTcParamsHost {
 };
 /// Builds the TMA descriptors (yb is [yb_rows x out_pad]).
 void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows);
+/// (Re)encodes a y map over [yb_rows x out_pad]: which = -1 the store /
+/// gathered-minibatch map, 0/1 the host-streamed buffers.
 void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows);
 void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t s);
 void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s);

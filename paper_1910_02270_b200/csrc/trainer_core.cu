@@ -117,6 +117,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
     ltfb_dev::StepArgs probe{};
     probe.m = ma;
     probe.B = B;
+    probe.S = sm_count_;  // one wide-pass CTA per SM
     const bool tc_ok = ltfb_dev::wide_tc_supported(probe);
     if (spec_.wide_kernel == 0) wide_kind_ = tc_ok ? 2 : 1;
     else if (spec_.wide_kernel == 1) wide_kind_ = 1;
@@ -376,6 +377,7 @@ void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const fl
   a.perm[0] = perm_[0].p;
   a.perm[1] = perm_[1].p;
   a.n_part = static_cast<int>(n);
+  if (wide_kind_ >= 2) ltfb_dev::encode_y_map(wtp_, -1, sy_.p, a, static_cast<int>(n));  // gather4 source
   steps_per_epoch_ = (n + spec_.batch_size - 1) / spec_.batch_size;
   LTFB_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -497,40 +499,50 @@ void DeviceTrainer::resolve_kernel_times() {
 }
 
 void DeviceTrainer::launch_step_kernels(bool gather) {
+  // gather == true: the minibatch comes from the HBM store through the epoch
+  // plan; false: it was streamed into xb / the y buffer by the host path
   if (wide_kind_ >= 2 && wide_dirty_) {
     ltfb_dev::launch_prep_wide(args_, wtp_, stream_);
     ++launches_;
     wide_dirty_ = false;
   }
-  if (gather) {
+  std::uint64_t n = 0;
+  if (wide_kind_ >= 2) {
+    // tcgen05 wide pass gathers y rows from the store itself (tile::gather4);
+    // one small kernel brings the x rows and computes h = dec_head(fwd(x))
+    kernel_mark(0, true);
+    ltfb_dev::launch_row_h(args_, gather, stream_);
+    kernel_mark(0, false);
+    ++n;
+  } else if (gather) {
     kernel_mark(0, true);
     ltfb_dev::launch_gather(args_, stream_);
     kernel_mark(0, false);
+    ++n;
   }
-  if (!gather && args_.h_in_gather) {  // host-streamed minibatch: h from xb
-    ltfb_dev::launch_row_h(args_, stream_);
-    ++launches_;
-  }
-  if (!args_.h_in_gather) {  // k_pre: h and the small-net tapes
+  if (!args_.h_in_gather) {  // k_pre: h and the small-net tapes for the generic post kernels
     kernel_mark(1, true);
     ltfb_dev::launch_pre(args_, stream_);
     kernel_mark(1, false);
+    ++n;
   }
   kernel_mark(2, true);
   if (wide_kind_ >= 2) ltfb_dev::launch_wide_tc_params(wtp_, args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
   kernel_mark(2, false);
-  if (wide_kind_ < 2) {  // ... and reduces its split-K partials itself
+  ++n;
+  if (wide_kind_ < 2) {  // the tcgen05 wide pass reduces its split-K partials itself
     kernel_mark(4, true);
     ltfb_dev::launch_reduce(args_, stream_);
     kernel_mark(4, false);
+    ++n;
   }
   kernel_mark(3, true);
   if (post_tpl_) ltfb_dev::launch_post_tpl(post_tpl_, args_, stream_);
   else if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
   else ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
-  launches_ += (gather ? 3 : 2) + (wide_kind_ < 2 ? 1 : 0) + (args_.h_in_gather ? 0 : 1);
+  launches_ += n + 1;
 }
 
 void DeviceTrainer::timer_start() {
@@ -822,9 +834,11 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
     LTFB_CUDA(cudaStreamWaitEvent(stream_, h2d_done_[b], 0));
     args_.xb = hx_[b].p;
     args_.yb = hy_[b].p;
+    args_.y_identity = 1;
     wtp_.y_sel = b;
     launch_step_kernels(false);
     wtp_.y_sel = -1;
+    args_.y_identity = 0;
     LTFB_CUDA(cudaEventRecord(used_done_[b], stream_));
     ++step_in_epoch_;
     ++epoch_steps_;

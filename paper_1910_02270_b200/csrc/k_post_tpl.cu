@@ -41,6 +41,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "tc_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -63,7 +64,8 @@ struct NetS {
   float slope[kMaxL];
   int blob;                      // staged blob (W0,b0,W1,b1,...), W [in x out]
   int woff[kMaxL], boff[kMaxL];  // within the blob
-  int T[kMaxL];                  // W^T [out x (in + 1)] (input gradients)
+  int T[kMaxL];                  // W^T [out x (in + 1)] (input gradients), contiguous from Tall
+  int Tall, Tcount;              // the net's W^T region (same layout as StepArgs::pT)
   int z[kMaxL], a[kMaxL];        // forward tape
   int dz[kMaxL];                 // dL/dz per layer (weight gradients)
 };
@@ -132,13 +134,13 @@ constexpr int shape_key(int in, int out, int nrw) { return (in << 16) | (out << 
 /// matmul, add_row_vector, activation; each output one k-ordered fmaf
 /// chain). Lanes are output neurons; x is read as a warp broadcast.
 template <int IN_T, int OUT_T, int NRW_T>
-__device__ __noinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_rt, int nrw_rt, int z, int act,
+__device__ __noinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_rt, int z, int act,
                                     float slope, int out_a) {
   float* s = S();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr bool kCT = IN_T > 0;
-  const int IN = kCT ? IN_T : IN_rt, OUT = kCT ? OUT_T : OUT_rt, nrw = kCT ? NRW_T : nrw_rt;
-  constexpr int kRows = kCT ? NRW_T : 4;
+  const int IN = kCT ? IN_T : IN_rt, OUT = kCT ? OUT_T : OUT_rt;
+  constexpr int kRows = NRW_T;
 #pragma unroll
   for (int j = lane; j < OUT; j += 32) {
     float acc[kRows];
@@ -158,14 +160,12 @@ __device__ __noinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_rt, 
       for (int k = 0; k < IN; ++k) {
         const float wv = w[k * OUT];
 #pragma unroll
-        for (int i = 0; i < kRows; ++i)
-          if (i < nrw) acc[i] = fmaf(xr[8 * i * IN + k], wv, acc[i]);
+        for (int i = 0; i < kRows; ++i) acc[i] = fmaf(xr[8 * i * IN + k], wv, acc[i]);
       }
     }
     const float bj = s[b + j];
 #pragma unroll
     for (int i = 0; i < kRows; ++i) {
-      if (i >= nrw) break;
       const int o = (warp + 8 * i) * OUT + j;
       const float v = acc[i] + bj;
       s[z + o] = v;
@@ -182,11 +182,15 @@ __device__ __forceinline__ void wfwd(int x, const NetS& n, int l, int nrw, int o
   switch (shape_key(IN, OUT, nrw)) {
 #define X(i, o, r)                                                   \
   case shape_key(i, o, r):                                           \
-    wfwd_k<i, o, r>(x, W, b, IN, OUT, nrw, z, act, sl, out_a); \
+    wfwd_k<i, o, r>(x, W, b, IN, OUT, z, act, sl, out_a); \
     return;
     LTFB_FWD_SHAPES(X)
 #undef X
-    default: wfwd_k<0, 0, 0>(x, W, b, IN, OUT, nrw, z, act, sl, out_a);
+    default:
+      if (nrw == 4)
+        wfwd_k<0, 0, 4>(x, W, b, IN, OUT, z, act, sl, out_a);
+      else
+        wfwd_k<0, 0, 2>(x, W, b, IN, OUT, z, act, sl, out_a);
   }
 }
 
@@ -195,13 +199,13 @@ __device__ __forceinline__ void wfwd(int x, const NetS& n, int l, int nrw, int o
 /// + disc + inv, train_ops.hpp:104-127), then * act'(z', a') of layer l-1 if
 /// dact (the result is then that layer's dz). Lanes are input neurons.
 template <int IN_T, int OUT_T, int NRW_T>
-__device__ __noinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, int nrw_rt, int out, int epiA, int epiB,
+__device__ __noinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, int out, int epiA, int epiB,
                                     int zp, int ap, int actp, float slope, bool dact) {
   float* s = S();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr bool kCT = IN_T > 0;
-  const int IN = kCT ? IN_T : IN_rt, OUT = kCT ? OUT_T : OUT_rt, nrw = kCT ? NRW_T : nrw_rt;
-  constexpr int kRows = kCT ? NRW_T : 4;
+  const int IN = kCT ? IN_T : IN_rt, OUT = kCT ? OUT_T : OUT_rt;
+  constexpr int kRows = NRW_T;
   const int ldt = IN + 1;  // odd row pitch: conflict-free transposed writes and reads
 #pragma unroll
   for (int k = lane; k < IN; k += 32) {
@@ -222,13 +226,11 @@ __device__ __noinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, int n
       for (int j = 0; j < OUT; ++j) {
         const float wv = w[j * ldt];
 #pragma unroll
-        for (int i = 0; i < kRows; ++i)
-          if (i < nrw) acc[i] = fmaf(dr[8 * i * OUT + j], wv, acc[i]);
+        for (int i = 0; i < kRows; ++i) acc[i] = fmaf(dr[8 * i * OUT + j], wv, acc[i]);
       }
     }
 #pragma unroll
     for (int i = 0; i < kRows; ++i) {
-      if (i >= nrw) break;
       const int o = (warp + 8 * i) * IN + k;
       float v = acc[i];
       if (epiA >= 0) v = (s[epiA + o] + v) + s[epiB + o];
@@ -246,11 +248,15 @@ __device__ __forceinline__ void wgin(int dz, const NetS& n, int l, int nrw, int 
   switch (shape_key(IN, OUT, nrw)) {
 #define X(i, o, r)                                                                    \
   case shape_key(i, o, r):                                                            \
-    wgin_k<i, o, r>(dz, WT, IN, OUT, nrw, out, epiA, epiB, zp, ap, actp, sl, dact); \
+    wgin_k<i, o, r>(dz, WT, IN, OUT, out, epiA, epiB, zp, ap, actp, sl, dact); \
     return;
     LTFB_GIN_SHAPES(X)
 #undef X
-    default: wgin_k<0, 0, 0>(dz, WT, IN, OUT, nrw, out, epiA, epiB, zp, ap, actp, sl, dact);
+    default:
+      if (nrw == 4)
+        wgin_k<0, 0, 4>(dz, WT, IN, OUT, out, epiA, epiB, zp, ap, actp, sl, dact);
+      else
+        wgin_k<0, 0, 2>(dz, WT, IN, OUT, out, epiA, epiB, zp, ap, actp, sl, dact);
   }
 }
 
@@ -349,12 +355,18 @@ __device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr) {
 }
 
 /// nn/adam.hpp:48-61 in double with explicit round-to-nearest operations
-/// (no FMA contraction): bit-identical to the reference's scalar loop.
-__device__ __noinline__ void adam_owned(const StepArgs& a, int net, int lo, int hi, double c1, double c2,
-                                        int p_smem, int gr, int mo, int vo) {
+/// (no FMA contraction): bit-identical to the reference's scalar loop. The
+/// owner writes the new parameter to HBM (p and, for weights, the W^T copy
+/// pT the next step stages) and, if push, into the blob image and W^T image
+/// of every CTA of the cluster (DSMEM stores; visible after the next cluster
+/// barrier), so no CTA has to pull or re-transpose the updated network.
+__device__ __noinline__ void adam_owned(const StepArgs& a, int net, const NetS& n, int lo, int hi, double c1,
+                                        double c2, int gr, int mo, int vo, bool push) {
+  cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   const double lr = a.lr[net], b1 = a.b1, b2 = a.b2, eps = a.eps;
   float* p = a.p[net];
+  float* pT = a.pT[net];
   float* m1 = a.mom1[net];
   float* m2 = a.mom2[net];
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
@@ -363,11 +375,27 @@ __device__ __noinline__ void adam_owned(const StepArgs& a, int net, int lo, int 
     const double vi = __dadd_rn(__dmul_rn(b2, (double)s[vo + e - lo]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
     m1[e] = (float)mi;
     m2[e] = (float)vi;
-    const float pn = (float)__dsub_rn((double)s[p_smem + e],
+    const float pn = (float)__dsub_rn((double)s[n.blob + e],
                                       __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)),
                                                 __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
     p[e] = pn;
-    s[p_smem + e] = pn;
+    int t = -1;  // W^T position of a weight element (biases have none)
+    for (int l = 0; l < n.L; ++l) {
+      const int in = n.w[l], out = n.w[l + 1], q = e - n.woff[l];
+      if (q >= 0 && q < in * out) {
+        const int k = q / out, j = q - k * out;
+        t = n.T[l] + j * (in + 1) + k;
+      }
+    }
+    if (t >= 0) pT[t - n.Tall] = pn;
+    if (push) {
+#pragma unroll
+      for (int r = 0; r < kC; ++r) {
+        float* peer = cl.map_shared_rank(s, r);
+        peer[n.blob + e] = pn;
+        if (t >= 0) peer[t] = pn;
+      }
+    }
   }
 }
 
@@ -416,6 +444,11 @@ inline Layout make_layout(const ModelArgs& m) {
     n.count = (int)d.count;
     for (int i = 0; i <= kMaxL; ++i) n.w[i] = i <= d.L ? d.w[i] : 0;
     n.blob = take(n.count);
+    n.Tcount = 0;
+    if (bwd5[q])
+      for (int l = 0; l < d.L; ++l) n.Tcount += (d.w[l] + 1) * d.w[l + 1];
+    n.Tall = take(n.Tcount);
+    int tat = n.Tall;
     for (int l = 0; l < kMaxL; ++l) {
       n.act[l] = l < d.L ? d.act[l] : kIdentity;
       n.slope[l] = l < d.L ? d.slope[l] : 0.0f;
@@ -424,7 +457,10 @@ inline Layout make_layout(const ModelArgs& m) {
       n.T[l] = n.z[l] = n.a[l] = n.dz[l] = 0;
       if (l >= d.L) continue;
       const int sz = rows5[q] * d.w[l + 1];
-      if (bwd5[q]) n.T[l] = take((d.w[l] + 1) * d.w[l + 1]);  // W^T, row pitch in + 1
+      if (bwd5[q]) {  // W^T, row pitch in + 1
+        n.T[l] = tat;
+        tat += (d.w[l] + 1) * d.w[l + 1];
+      }
       n.z[l] = take(sz);
       n.a[l] = n.act[l] == kIdentity ? n.z[l] : take(sz);
       if (bwd5[q]) n.dz[l] = take(sz);
@@ -433,7 +469,7 @@ inline Layout make_layout(const ModelArgs& m) {
   const NetDesc* tr[3] = {&m.disc, &m.fwd, &m.inv};
   for (int i = 0; i < 3; ++i) {
     y.pg[i] = take((int)tr[i]->count);
-    const int sl = (int)tr[i]->count / kC + 2;
+    const int sl = (int)tr[i]->count / kC + 8;
     y.mo[i] = take(sl);
     y.vo[i] = take(sl);
     y.gr[i] = take(sl);
@@ -462,49 +498,96 @@ struct Rows {
   int lo[3], hi[3];
 };
 
-/// One asynchronous staging pass (blobs, owner-slice moments, this CTA's
-/// rows), then the W^T copies and the row transforms.
-__device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const Rows& R) {
+/// First element of rank r's owner slice of a count-element blob: the even
+/// split rounded down to a multiple of 4, so every slice starts 16 B aligned
+/// (bulk copies) and the slices tile [0, count).
+__host__ __device__ __forceinline__ int owner_lo(int count, int r) {
+  return r <= 0 ? 0 : (r >= kC ? count : ((count * r / kC) & ~3));
+}
+
+/// A host->smem staging job: n floats from src to smem offset dst.
+struct Job {
+  int dst, n;
+  const float* src;
+};
+
+/// Splits a job into a 16 B-aligned body moved by one bulk copy (TMA engine)
+/// and <= 3 + 3 unaligned edge floats moved by ordinary loads.
+__device__ __forceinline__ void job_split(const Job& j, int& head, int& body) {
+  const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(j.src) & 15u) >> 2;  // floats past alignment
+  head = (int)((4u - mis) & 3u);
+  if (head > j.n) head = j.n;
+  body = ((j.dst + head) & 3) == 0 ? ((j.n - head) & ~3) : 0;
+  if (body == 0) head = j.n;  // relatively misaligned: all by loads
+}
+
+/// Staging job q of this CTA (0 <= q < kJobs; n == 0 if absent).
+constexpr int kJobs = 19;
+__device__ __noinline__ Job make_job(int q, const StepArgs& a, const Layout& Y, const Rows& R) {
+  const ModelArgs& m = a.m;
+  switch (q) {
+    case 0: return {Y.net[kF].blob, Y.net[kF].count, a.p[kFwd]};
+    case 1: return {Y.net[kI].blob, Y.net[kI].count, a.p[kInv]};
+    case 2: return {Y.net[kCd].blob, Y.net[kCd].count, a.p[kDisc]};
+    case 3: return {Y.net[kET].blob, Y.net[kET].count, a.p[kEnc] + m.enc_tail.base};
+    case 4: return {Y.net[kDH].blob, Y.net[kDH].count, a.p[kDec] + m.dec_head.base};
+    case 5: return {Y.net[kF].Tall, Y.net[kF].Tcount, a.pT[kFwd]};
+    case 6: return {Y.net[kI].Tall, Y.net[kI].Tcount, a.pT[kInv]};
+    case 7: return {Y.net[kCd].Tall, Y.net[kCd].Tcount, a.pT[kDisc]};
+    case 8: return {Y.net[kDH].Tall, Y.net[kDH].Tcount, a.pT[kDec]};
+    case 9: return {Y.mo[0], R.hi[0] - R.lo[0], a.mom1[kDisc] + R.lo[0]};
+    case 10: return {Y.vo[0], R.hi[0] - R.lo[0], a.mom2[kDisc] + R.lo[0]};
+    case 11: return {Y.mo[1], R.hi[1] - R.lo[1], a.mom1[kFwd] + R.lo[1]};
+    case 12: return {Y.vo[1], R.hi[1] - R.lo[1], a.mom2[kFwd] + R.lo[1]};
+    case 13: return {Y.mo[2], R.hi[2] - R.lo[2], a.mom1[kInv] + R.lo[2]};
+    case 14: return {Y.vo[2], R.hi[2] - R.lo[2], a.mom2[kInv] + R.lo[2]};
+    case 15: return {Y.be, m.E1, a.p[kEnc] + m.enc_wide_b};
+    case 16: return {Y.xs, R.nr * m.in, a.xb + (long long)R.r0 * m.in};
+    case 17: return {Y.e1, R.nr * m.E1, a.scratch + a.L.red_enc + (long long)R.r0 * m.E1};
+    default: return {Y.gh, R.nr * m.D, a.scratch + a.L.red_dec + (long long)R.r0 * m.D};
+  }
+}
+
+/// One staging pass: the five blob images, the four W^T images, the owner
+/// slices of the three Adam moments and this CTA's rows of x / red_enc /
+/// red_dec. Job q belongs to one thread (spread over the warps): it adds its
+/// bytes to the mbarrier's transaction count, issues one bulk copy (TMA
+/// engine) for the 16 B-aligned body and loads the <= 6 unaligned edge
+/// floats itself. Then the row transforms.
+__device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const Rows& R, uint64_t* bar) {
   float* s = S();
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x;
   const int in = m.in, E1 = m.E1, D = m.D;
-  {
-    const float* src5[5] = {a.p[kFwd], a.p[kInv], a.p[kDisc], a.p[kEnc] + m.enc_tail.base,
-                            a.p[kDec] + m.dec_head.base};
-    for (int q = 0; q < 5; ++q)
-      for (int i = tid; i < Y.net[q].count; i += kThreads) cp4(Y.net[q].blob + i, src5[q] + i);
-  }
-  const int nets3[3] = {kDisc, kFwd, kInv};
-  for (int q = 0; q < 3; ++q)
-    for (int e = R.lo[q] + tid; e < R.hi[q]; e += kThreads) {
-      cp4(Y.mo[q] + e - R.lo[q], a.mom1[nets3[q]] + e);
-      cp4(Y.vo[q] + e - R.lo[q], a.mom2[nets3[q]] + e);
-    }
-  for (int i = tid; i < E1; i += kThreads) cp4(Y.be + i, a.p[kEnc] + m.enc_wide_b + i);
-  {
-    const float* red_enc = a.scratch + a.L.red_enc + (long long)R.r0 * E1;
-    const float* red_dec = a.scratch + a.L.red_dec + (long long)R.r0 * D;
-    const float* xb = a.xb + (long long)R.r0 * in;
-    for (int i = tid; i < kR * in; i += kThreads) {
-      if (i < R.nr * in) cp4(Y.xs + i, xb + i);
-      else s[Y.xs + i] = 0.0f;
-    }
-    for (int i = tid; i < kR * E1; i += kThreads) {
-      if (i < R.nr * E1) cp4(Y.e1 + i, red_enc + i);
-      else s[Y.e1 + i] = 0.0f;
-    }
-    for (int i = tid; i < kR * D; i += kThreads) {
-      if (i < R.nr * D) cp4(Y.gh + i, red_dec + i);
-      else s[Y.gh + i] = 0.0f;
+  const int q = (tid & 31) * kWarps + (tid >> 5);  // job of this thread: warps take turns
+  if (q < kJobs) {
+    const Job j = make_job(q, a, Y, R);
+    if (j.n > 0 && j.src != nullptr) {
+      int h, b;
+      job_split(j, h, b);
+      if (b > 0) {
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_u32(bar)),
+                     "r"(4 * b)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                tc::smem_u32(s + j.dst + h)),
+            "l"(j.src + h), "r"(4 * b), "r"(tc::smem_u32(bar))
+            : "memory");
+      }
+      for (int e = 0; e < j.n - b; ++e) {  // unaligned edges
+        const int o = e < h ? e : e + b;
+        s[j.dst + o] = j.src[o];
+      }
     }
   }
-  cp_wait_all();
+  for (int i = tid; i < (kR - R.nr) * in; i += kThreads) s[Y.xs + R.nr * in + i] = 0.0f;  // pad rows
+  for (int i = tid; i < (kR - R.nr) * E1; i += kThreads) s[Y.e1 + R.nr * E1 + i] = 0.0f;
+  for (int i = tid; i < (kR - R.nr) * D; i += kThreads) s[Y.gh + R.nr * D + i] = 0.0f;
   __syncthreads();
-  transpose_net(Y.net[kF]);
-  transpose_net(Y.net[kI]);
-  transpose_net(Y.net[kCd]);
-  if (Y.net[kDH].L > 0) transpose_net(Y.net[kDH]);
+  if (tid == 0) tc::mbar_arrive(bar);
+  tc::mbar_wait(bar, 0);
+  __syncthreads();
   {
     // enc layer-0 activation of this CTA's rows (pad rows: act(0 + b))
     const int e1 = Y.net[kET].L > 0 ? Y.e1 : Y.stacked;
@@ -591,21 +674,10 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   const NetS& C = Y.net[kCd];
   if (d_ok) {
     const unsigned long long t = a.ctr->t[kDisc] + 1;
-    adam_owned(a, kDisc, R.lo[0], R.hi[0], a.adam_c[2 * t], a.adam_c[2 * t + 1], C.blob, Y.gr[0], Y.mo[0], Y.vo[0]);
+    adam_owned(a, kDisc, C, R.lo[0], R.hi[0], a.adam_c[2 * t], a.adam_c[2 * t + 1], Y.gr[0], Y.mo[0], Y.vo[0],
+               true);
   }
-  cluster_sync();  // S3: updated slices in every CTA's smem
-  if (d_ok) {
-    const int count = C.count;
-    for (int e = tid; e < count; e += kThreads) {
-      int r = (int)(((long long)e * kC) / count);
-      while (r + 1 < kC && (long long)count * (r + 1) / kC <= e) ++r;
-      while (r > 0 && (long long)count * r / kC > e) --r;
-      if (r != R.rank) s[C.blob + e] = cl.map_shared_rank(s + C.blob, r)[e];
-    }
-    __syncthreads();
-    transpose_net(C);
-    __syncthreads();
-  }
+  cluster_sync();  // S3: every owner's updated disc slice (blob + W^T) pushed into every CTA
   return d_ok;
 }
 
@@ -650,12 +722,12 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
     const unsigned long long tf = a.ctr->t[kFwd] + 1, ti = a.ctr->t[kInv] + 1;
-    adam_owned(a, kFwd, R.lo[1], R.hi[1], a.adam_c[2 * tf], a.adam_c[2 * tf + 1], Y.net[kF].blob, Y.gr[1],
-               Y.mo[1], Y.vo[1]);
+    adam_owned(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], a.adam_c[2 * tf], a.adam_c[2 * tf + 1], Y.gr[1], Y.mo[1],
+               Y.vo[1], false);
     out[4] = 1.0;
     if (all_i) {
-      adam_owned(a, kInv, R.lo[2], R.hi[2], a.adam_c[2 * ti], a.adam_c[2 * ti + 1], Y.net[kI].blob, Y.gr[2],
-                 Y.mo[2], Y.vo[2]);
+      adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], a.adam_c[2 * ti], a.adam_c[2 * ti + 1], Y.gr[2], Y.mo[2],
+                 Y.vo[2], false);
       out[5] = 1.0;
     }
   }
@@ -707,6 +779,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ int s_ok[4];            // finite flags of this CTA's owned slices
   __shared__ long long s_ph[16];
   __shared__ double s_g[6];
+  __shared__ __align__(8) uint64_t s_bar;
   int n_ph = 0;
 #define PH()                                                                  \
   do {                                                                        \
@@ -732,11 +805,15 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   }
   for (int q = 0; q < 3; ++q) {
     const int c = q == 0 ? Lp.net[kCd].count : (q == 1 ? Lp.net[kF].count : Lp.net[kI].count);
-    R.lo[q] = c * R.rank / kC;
-    R.hi[q] = c * (R.rank + 1) / kC;
+    R.lo[q] = owner_lo(c, R.rank);
+    R.hi[q] = owner_lo(c, R.rank + 1);
+  }
+  if (tid == 0) {
+    tc::mbar_init(&s_bar, 1);
+    tc::fence_barrier_init();
   }
   __syncthreads();
-  prologue(a, Y, R);
+  prologue(a, Y, R, &s_bar);
   PH();
   const NetS& F = Y.net[kF];
   const NetS& I = Y.net[kI];
@@ -821,6 +898,35 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 }  // namespace ps
+
+namespace ps {
+/// W^T images from the blobs (block q: fwd, inv, disc, dec head).
+__global__ void __launch_bounds__(256) k_build_T(const __grid_constant__ StepArgs a) {
+  const int q = blockIdx.x;
+  const int net = q == 0 ? kFwd : (q == 1 ? kInv : (q == 2 ? kDisc : kDec));
+  const NetDesc& d = q == 0 ? a.m.fwd : (q == 1 ? a.m.inv : (q == 2 ? a.m.disc : a.m.dec_head));
+  const float* p = a.p[net];
+  float* T = a.pT[net];
+  if (!T || d.L == 0) return;
+  long long at = 0;
+  for (int l = 0; l < d.L; ++l) {
+    const int in = d.w[l], out = d.w[l + 1], n = (in + 1) * out;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int j = i / (in + 1), k = i - j * (in + 1);
+      T[at + i] = k < in ? p[d.off_w[l] + (long long)k * out + j] : 0.0f;
+    }
+    at += n;
+  }
+}
+}  // namespace ps
+
+long long small_T_floats(const NetDesc& d) {
+  long long n = 0;
+  for (int l = 0; l < d.L; ++l) n += (long long)(d.w[l] + 1) * d.w[l + 1];
+  return n;
+}
+
+void launch_build_T(const StepArgs& a, cudaStream_t s) { ps::k_build_T<<<4, 256, 0, s>>>(a); }
 
 namespace {
 constexpr std::size_t kSmemCap = 220 * 1024;  // dynamic shared memory (static ~2 KB on top)

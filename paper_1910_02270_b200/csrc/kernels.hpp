@@ -42,6 +42,10 @@ bool post_fast_supported(const StepArgs& a);
 void launch_post_fast(const StepArgs& a, cudaStream_t s);
 /// Compile-time-shaped post kernel (k_post_tpl.cu): 0 if no instance
 /// matches the model, else the instance id for launch_post_tpl.
+/// Floats of a small net's W^T image (sum over layers of (in + 1) * out).
+long long small_T_floats(const NetDesc& d);
+/// Rebuilds every non-null StepArgs::pT image from the parameter blobs.
+void launch_build_T(const StepArgs& a, cudaStream_t s);
 int post_tpl_kind(const StepArgs& a);
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);

@@ -64,6 +64,11 @@ struct StepArgs {
   float* mom1[5];
   float* mom2[5];
   float* g[5];
+  // W^T images of fwd / inv / disc / dec-head ([out x (in + 1)] per layer,
+  // layers concatenated) for the small-network post kernel; by NetId, kDec =
+  // the dec head. Rebuilt by k_build_T when parameters change from outside a
+  // step, kept current by the post kernel's Adam owners.
+  float* pT[5];
   // HBM-resident data store and the epoch plan (two buffers, epoch parity)
   const float* sx;
   const float* sy;

@@ -199,6 +199,14 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   post_tpl_ = spec_.post_kernel == 0 || spec_.post_kernel == 3 ? ltfb_dev::post_tpl_kind(a) : 0;
   if (spec_.post_kernel == 3 && post_tpl_ == 0)
     throw ContractError("post_kernel 3 (compile-time shapes) requested but no instance matches this model");
+  if (post_tpl_) {  // W^T images the post kernel stages (and its Adam owners maintain)
+    const ltfb_dev::NetDesc* d[5] = {nullptr, &margs_.dec_head, &margs_.fwd, &margs_.inv, &margs_.disc};
+    for (int i = 1; i < 5; ++i) {
+      pT_[i].alloc(static_cast<std::size_t>(std::max<long long>(1, ltfb_dev::small_T_floats(*d[i]))));
+      a.pT[i] = pT_[i].p;
+    }
+    small_T_dirty_ = true;
+  }
   // with the tcgen05 wide pass (which reduces its own partials) and the
   // recomputing post kernel, h comes from the gather kernel and k_pre is skipped
   a.h_in_gather = (wide_kind_ >= 2 && post_tpl_) ? 1 : 0;
@@ -303,6 +311,7 @@ static float* net_ptr(DeviceTrainer& t, DevBuf<float>* params, DevBuf<float>& ge
 
 void DeviceTrainer::set_params(int net, const float* blob, std::size_t count) {
   if (net == 0 || net == 1) wide_dirty_ = true;
+  small_T_dirty_ = true;
   if (net < 0 || net > 4) throw ContractError("set_params: bad network index");
   if (count != counts_[net])
     throw ContractError("blob length " + std::to_string(count) + " does not match manifest total " +
@@ -498,14 +507,23 @@ void DeviceTrainer::resolve_kernel_times() {
   }
 }
 
-void DeviceTrainer::launch_step_kernels(bool gather) {
-  // gather == true: the minibatch comes from the HBM store through the epoch
-  // plan; false: it was streamed into xb / the y buffer by the host path
+void DeviceTrainer::prepare_params() {
   if (wide_kind_ >= 2 && wide_dirty_) {
     ltfb_dev::launch_prep_wide(args_, wtp_, stream_);
     ++launches_;
     wide_dirty_ = false;
   }
+  if (post_tpl_ && small_T_dirty_) {
+    ltfb_dev::launch_build_T(args_, stream_);
+    ++launches_;
+    small_T_dirty_ = false;
+  }
+}
+
+void DeviceTrainer::launch_step_kernels(bool gather) {
+  // gather == true: the minibatch comes from the HBM store through the epoch
+  // plan; false: it was streamed into xb / the y buffer by the host path
+  prepare_params();
   std::uint64_t n = 0;
   if (wide_kind_ >= 2) {
     // tcgen05 wide pass gathers y rows from the store itself (tile::gather4);
@@ -622,11 +640,7 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
 
 bool DeviceTrainer::launch_graph(std::size_t steps) {
   if (!graphs_on_ || ktime_on_) return false;
-  if (wide_kind_ >= 2 && wide_dirty_) {  // weight re-layout stays outside the graph
-    ltfb_dev::launch_prep_wide(args_, wtp_, stream_);
-    ++launches_;
-    wide_dirty_ = false;
-  }
+  prepare_params();  // weight re-layouts stay outside the graph
   if (std::memcmp(&graph_args_, &args_, sizeof args_) != 0) {  // pointers or layout changed
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     graphs_.clear();
@@ -761,6 +775,7 @@ EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int
   e.n_inv = static_cast<long long>(counts_[3]);
   e.ctr = ctr_.p;
   ltfb_dev::launch_eval(e, stream_);
+  if (decide) small_T_dirty_ = true;  // the device may have adopted the incoming generator
   launches_ += 3;
   LTFB_CUDA(cudaGetLastError());
   double out[6] = {0, 0, 0, 0, 0, 0};
@@ -787,6 +802,7 @@ EvalOut DeviceTrainer::tournament_decide() {
 
 void DeviceTrainer::adopt(const float* fwd, const float* inv) {
   DeviceGuard g(spec_.device);
+  small_T_dirty_ = true;
   LTFB_CUDA(cudaMemcpyAsync(gen_.p, fwd, counts_[2] * 4, cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaMemcpyAsync(gen_.p + counts_[2], inv, counts_[3] * 4, cudaMemcpyHostToDevice, stream_));
   for (int net : {2, 3}) {

@@ -204,6 +204,9 @@ class DeviceTrainer {
   DevBuf<float> wet_, wd_, wdt_, bias_pad_;
   ltfb_dev::WideTcParamsHost wtp_{};
   bool wide_dirty_ = false;
+  bool small_T_dirty_ = true;  // StepArgs::pT images need a rebuild
+  DevBuf<float> pT_[5];
+  void prepare_params();
   DevBuf<double> mae_part_, mae_total_, adam_c_;
   DevBuf<ltfb_dev::Counters> ctr_;
   DevBuf<unsigned> grid_bar_;

@@ -73,6 +73,7 @@ struct NetS {
 struct Layout {
   NetS net[5];  // kF, kI, kCd, kET, kDH
   int xs, e1, be, gh, stacked, gl_dec, gl_inv, gl, gc, gi;
+  int xn;  // x rows of the next step (next_h), prefetched in the prologue
   int pg[3];                // partial gradients disc, fwd, inv (blob layout)
   int mo[3], vo[3], gr[3];  // owner-slice moments / reduced gradients
   int total;
@@ -361,7 +362,7 @@ __device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr) {
 /// of every CTA of the cluster (DSMEM stores; visible after the next cluster
 /// barrier), so no CTA has to pull or re-transpose the updated network.
 __device__ __noinline__ void adam_owned(const StepArgs& a, int net, const NetS& n, int lo, int hi, double c1,
-                                        double c2, int gr, int mo, int vo, bool push) {
+                                        double c2, int gr, int mo, int vo, int push /* 1 blob, 2 blob + W^T */) {
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   const double lr = a.lr[net], b1 = a.b1, b2 = a.b2, eps = a.eps;
@@ -393,7 +394,7 @@ __device__ __noinline__ void adam_owned(const StepArgs& a, int net, const NetS& 
       for (int r = 0; r < kC; ++r) {
         float* peer = cl.map_shared_rank(s, r);
         peer[n.blob + e] = pn;
-        if (t >= 0) peer[t] = pn;
+        if (push == 2 && t >= 0) peer[t] = pn;
       }
     }
   }
@@ -476,6 +477,7 @@ inline Layout make_layout(const ModelArgs& m) {
   }
   y.be = take(m.E1);
   y.xs = take(kR * m.in);
+  y.xn = take(kR * m.in);
   y.e1 = take(kR * m.E1);
   y.gh = take(kR * m.D);
   y.stacked = take(2 * kR * m.lat);
@@ -492,6 +494,19 @@ inline Layout make_layout(const ModelArgs& m) {
 // Cold, once-per-launch parts of the step live in out-of-line functions so
 // that the straight-line kernel body stays short and the hot layer routines
 // (wfwd / wgin / pg_net) remain resident in the instruction cache.
+
+// debug: fine-grained stamps inside the update phases (LTFB_PHASE_PROF)
+__shared__ long long g_st[16];
+__shared__ int g_nst;
+#define ST()                                                   \
+  do {                                                         \
+    if (threadIdx.x == 0 && g_nst < 16) g_st[g_nst++] = clock64(); \
+  } while (0)
+
+// step constants fetched once in the prologue (their global loads overlap
+// the staging copies): Adam bias corrections 1-b1^t, 1-b2^t for the next t of
+// disc / fwd / inv, and the wide pass's forward-MAE sum
+__shared__ double g_pre[7];
 
 struct Rows {
   int rank, rows, r0, nr;
@@ -581,6 +596,27 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
       }
     }
   }
+  if (tid < 3) {
+    const int net = tid == 0 ? kDisc : (tid == 1 ? kFwd : kInv);
+    const unsigned long long t = a.ctr->t[net] + 1;
+    g_pre[2 * tid] = a.adam_c[2 * t];
+    g_pre[2 * tid + 1] = a.adam_c[2 * t + 1];
+  } else if (tid == 3) {
+    g_pre[6] = *a.mae_total;
+  }
+  if (a.post_next_h) {  // x rows of the next step of this epoch (used by next_h)
+    const int nxt = (int)a.ctr->step_in_epoch + 1;
+    if ((long long)nxt * a.B < (long long)a.n_part) {
+      const int rows = min(a.B, a.n_part - nxt * a.B);
+      const int per = (rows + kC - 1) / kC;
+      const int r0 = min(R.rank * per, rows), nr = max(0, min(per, rows - r0));
+      const unsigned* perm = a.perm[a.ctr->epoch & 1u] + (long long)nxt * a.B + r0;
+      for (int i = tid; i < kR * in; i += kThreads) {
+        const int r = i / in, k = i - r * in;
+        s[Y.xn + i] = r < nr ? a.sx[(long long)perm[r] * in + k] : 0.0f;
+      }
+    }
+  }
   for (int i = tid; i < (kR - R.nr) * in; i += kThreads) s[Y.xs + R.nr * in + i] = 0.0f;  // pad rows
   for (int i = tid; i < (kR - R.nr) * E1; i += kThreads) s[Y.e1 + R.nr * E1 + i] = 0.0f;
   for (int i = tid; i < (kR - R.nr) * D; i += kThreads) s[Y.gh + R.nr * D + i] = 0.0f;
@@ -661,22 +697,24 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   const int tid = threadIdx.x;
+  ST();
   const int dok = reduce_owned(Y.pg[0], R.lo[0], R.hi[0], Y.gr[0]);
+  ST();
   if (tid == 0) s_ok[0] = dok;
   double d_sum = 0.0;
   for (int r = 0; r < kC; ++r) d_sum += cl.map_shared_rank(s_loss, r)[0];
   const double n2 = 2.0 * (double)R.rows;
   *d_loss = ((double)R.rows * (d_sum / n2)) / (double)R.rows;
   cluster_sync();  // S2: flags
+  ST();
   int all_ok = 1;
   for (int r = 0; r < kC; ++r) all_ok &= cl.map_shared_rank(s_ok, r)[0];
   const bool d_ok = isfinite(*d_loss) && all_ok;
   const NetS& C = Y.net[kCd];
   if (d_ok) {
-    const unsigned long long t = a.ctr->t[kDisc] + 1;
-    adam_owned(a, kDisc, C, R.lo[0], R.hi[0], a.adam_c[2 * t], a.adam_c[2 * t + 1], Y.gr[0], Y.mo[0], Y.vo[0],
-               true);
+    adam_owned(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0], 2);
   }
+  ST();
   cluster_sync();  // S3: every owner's updated disc slice (blob + W^T) pushed into every CTA
   return d_ok;
 }
@@ -688,9 +726,12 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   cg::cluster_group cl = cg::this_cluster();
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x;
+  ST();
   cluster_sync();  // S4: fwd / inv partials + adv / cyc sums
+  ST();
   const int fok = reduce_owned(Y.pg[1], R.lo[1], R.hi[1], Y.gr[1]);
   const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
+  ST();
   if (tid == 0) {
     s_ok[1] = fok;
     s_ok[2] = iok;
@@ -701,6 +742,7 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
     cyc_sum += cl.map_shared_rank(s_loss, r)[2];
   }
   cluster_sync();  // S5: flags
+  ST();
   int all_f = 1, all_i = 1;
   for (int r = 0; r < kC; ++r) {
     all_f &= cl.map_shared_rank(s_ok, r)[1];
@@ -711,7 +753,7 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   const long long n_cyc = (long long)rows * m.in;
   const double adv = adv_sum / (double)rows;
   const double cyc = cyc_sum / (double)n_cyc;
-  const double fm = *a.mae_total / (double)n_fwd;
+  const double fm = g_pre[6] / (double)n_fwd;
   const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
   out[0] = ((double)rows * total_raw) / (double)rows;
   out[1] = ((double)rows * fm) / (double)rows;
@@ -721,16 +763,17 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
-    const unsigned long long tf = a.ctr->t[kFwd] + 1, ti = a.ctr->t[kInv] + 1;
-    adam_owned(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], a.adam_c[2 * tf], a.adam_c[2 * tf + 1], Y.gr[1], Y.mo[1],
-               Y.vo[1], false);
+    adam_owned(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1],
+               Y.vo[1], a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
     out[4] = 1.0;
+    ST();
     if (all_i) {
-      adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], a.adam_c[2 * ti], a.adam_c[2 * ti + 1], Y.gr[2], Y.mo[2],
-                 Y.vo[2], false);
+      adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2],
+                 Y.vo[2], 0);
       out[5] = 1.0;
     }
   }
+  ST();
 }
 
 /// Counters and the StepRecord (trainer.hpp:274-289); CTA 0, thread 0.
@@ -765,15 +808,69 @@ __device__ __noinline__ void finish(const StepArgs& a, bool d_ok, double d_loss,
   a.rec[(ctr->global_step - 1) % (unsigned long long)a.rec_cap] = r;
 }
 
+/// h = dec_head(fwd(x)) and the x rows of the NEXT step of this epoch
+/// (what k_gather's row kernel computes, same k-ordered chains), from the
+/// updated fwd every CTA holds after S6: the next step then needs no row
+/// kernel. Rows of the next minibatch are split over the CTAs like this
+/// step's. No-op when this step ends the epoch (the next epoch's plan is not
+/// on the device yet; its first step runs the row kernel).
+__device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie, unsigned epoch) {
+  float* s = S();
+  const ModelArgs& m = a.m;
+  const int tid = threadIdx.x;
+  const int nxt = sie + 1;
+  if ((long long)nxt * a.B >= (long long)a.n_part) return;
+  const int rows = min(a.B, a.n_part - nxt * a.B);
+  const int rank = (int)cg::this_cluster().block_rank();
+  const int per = (rows + kC - 1) / kC;
+  const int r0 = min(rank * per, rows), nr = max(0, min(per, rows - r0));
+  (void)epoch;
+  const int in = m.in;
+  for (int i = tid; i < kR * in; i += kThreads) {  // rows prefetched into xn by the prologue
+    const float v = s[Y.xn + i];
+    if (i < nr * in) a.xb[(long long)r0 * in + i] = v;
+    s[Y.xs + i] = v;
+  }
+  __syncthreads();
+  const NetS& F = Y.net[kF];
+  const NetS& DH = Y.net[kDH];
+  const int latent = Y.stacked + kR * m.lat;
+  wnet_fwd(F, Y.xs, 2, latent);
+  int fin = latent, w = m.lat;
+  if (DH.L > 0) {
+    wnet_fwd(DH, latent, 2, -1);
+    fin = DH.a[DH.L - 1];
+    w = DH.w[DH.L];
+  }
+  __syncthreads();
+  for (int i = tid; i < nr * w; i += kThreads) a.h[(long long)r0 * w + i] = s[fin + i];
+}
+
 __device__ __noinline__ void print_phases(const long long* ph, int n) {
   printf("post phases (cycles):");
   for (int i = 1; i < n; ++i) printf(" %lld", ph[i] - ph[i - 1]);
+  printf("\n  update stamps:");
+  for (int i = 1; i < g_nst; ++i) printf(" %lld", g_st[i] - g_st[i - 1]);
   printf("\n");
 }
 
 __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
-    k_post_small(const __grid_constant__ StepArgs a, const __grid_constant__ Layout Lp) {
+    k_post_small(const __grid_constant__ StepArgs ap, const __grid_constant__ Layout Lp) {
   __shared__ Layout Y;
+  // The argument block lives in shared memory for the whole step: the
+  // out-of-line phases read their fields through a reference, and
+  // reads of kernel parameters through a generic address are slow.
+  __shared__ __align__(16) StepArgs a_s;
+  {
+    const int* src = reinterpret_cast<const int*>(&ap);
+    int* dst = reinterpret_cast<int*>(&a_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(StepArgs) / sizeof(int)); i += kThreads) dst[i] = src[i];
+    const int* src2 = reinterpret_cast<const int*>(&Lp);
+    int* dst2 = reinterpret_cast<int*>(&Y);
+    for (int i = threadIdx.x; i < (int)(sizeof(Layout) / sizeof(int)); i += kThreads) dst2[i] = src2[i];
+    __syncthreads();
+  }
+  const StepArgs& a = a_s;
   __shared__ double s_loss[4];       // d, adv, cyc partial sums of this CTA
   __shared__ double s_wl[kWarps];    // per-warp loss partials
   __shared__ int s_ok[4];            // finite flags of this CTA's owned slices
@@ -790,25 +887,23 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   if (a.ctr->aborted) return;
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  {
-    const int* src = reinterpret_cast<const int*>(&Lp);
-    int* dst = reinterpret_cast<int*>(&Y);
-    for (int i = tid; i < (int)(sizeof(Layout) / sizeof(int)); i += kThreads) dst[i] = src[i];
-  }
   Rows R;
   R.rank = (int)cg::this_cluster().block_rank();
-  R.rows = min(a.B, a.n_part - (int)a.ctr->step_in_epoch * a.B);
+  const int sie = (int)a.ctr->step_in_epoch;
+  const unsigned epoch = a.ctr->epoch;
+  R.rows = min(a.B, a.n_part - sie * a.B);
   {
     const int per = (R.rows + kC - 1) / kC;
     R.r0 = min(R.rank * per, R.rows);
     R.nr = max(0, min(per, R.rows - R.r0));
   }
   for (int q = 0; q < 3; ++q) {
-    const int c = q == 0 ? Lp.net[kCd].count : (q == 1 ? Lp.net[kF].count : Lp.net[kI].count);
+    const int c = q == 0 ? Y.net[kCd].count : (q == 1 ? Y.net[kF].count : Y.net[kI].count);
     R.lo[q] = owner_lo(c, R.rank);
     R.hi[q] = owner_lo(c, R.rank + 1);
   }
   if (tid == 0) {
+    g_nst = 0;
     tc::mbar_init(&s_bar, 1);
     tc::fence_barrier_init();
   }
@@ -888,7 +983,9 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 6; ++i) s_g[i] = g[i];
     PH();
   }
-  cluster_sync();  // S6: no CTA leaves while peers read its shared memory
+  cluster_sync();  // S6: updated fwd in every CTA; no CTA leaves while peers read its shared memory
+  PH();
+  if (a.post_next_h) next_h(a, Y, sie, epoch);
   PH();
   if (R.rank == 0 && tid == 0) {
     finish(a, d_ok, d_loss, s_g);

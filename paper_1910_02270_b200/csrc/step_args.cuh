@@ -55,6 +55,7 @@ struct StepArgs {
   int h_in_gather;  // 1: k_gather's last CTA column computes h = dec_head(fwd(x)) per row
   int y_identity;   // wide pass: minibatch row r is row r of the y map (host-streamed buffer)
   int x_from_store; // 1: that h computation reads x through the epoch plan, 0: from xb
+  int post_next_h;  // 1: the small-network post kernel also computes h / xb of the next step (store path)
   int phase_prof;   // debug: per-phase clock64 stamps printed by the post kernel (LTFB_PHASE_PROF)
   int small_ctas;   // CTAs of the small-network kernels
   double lr[5], b1, b2, eps;

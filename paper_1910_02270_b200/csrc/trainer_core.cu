@@ -312,6 +312,7 @@ static float* net_ptr(DeviceTrainer& t, DevBuf<float>* params, DevBuf<float>& ge
 void DeviceTrainer::set_params(int net, const float* blob, std::size_t count) {
   if (net == 0 || net == 1) wide_dirty_ = true;
   small_T_dirty_ = true;
+  h_ready_ = false;
   if (net < 0 || net > 4) throw ContractError("set_params: bad network index");
   if (count != counts_[net])
     throw ContractError("blob length " + std::to_string(count) + " does not match manifest total " +
@@ -357,6 +358,7 @@ void DeviceTrainer::get_adam(int net, float* m, float* v, std::uint64_t* t) {
 // ------------------------------------------------------------------ data --
 void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const float* x,
                                const float* y, const std::int32_t* owner) {
+  h_ready_ = false;
   if (n == 0) throw ContractError("plan_epoch: empty partition");
   DeviceGuard g(spec_.device);
   const auto& m = margs_;
@@ -455,6 +457,7 @@ void DeviceTrainer::close_epoch_segment(bool epoch_done, bool partial) {
 }
 
 void DeviceTrainer::start_epoch() {
+  h_ready_ = false;
   if (have_plan_) close_epoch_segment(true, false);
   epoch_ += 1;
   const int buf = static_cast<int>(epoch_ & 1);
@@ -474,7 +477,10 @@ void DeviceTrainer::start_epoch() {
   have_plan_ = true;
 }
 
-void DeviceTrainer::launch_step() { launch_step_kernels(true); }
+void DeviceTrainer::launch_step() {
+  launch_step_kernels(true, !h_ready_);
+  h_ready_ = next_h_on() && step_in_epoch_ + 1 < steps_per_epoch_;
+}
 
 // kernel ids for per-kernel timing: 0 gather, 1 pre, 2 wide, 3 post, 4 reduce
 void DeviceTrainer::kernel_mark(int which, bool begin) {
@@ -520,18 +526,24 @@ void DeviceTrainer::prepare_params() {
   }
 }
 
-void DeviceTrainer::launch_step_kernels(bool gather) {
+bool DeviceTrainer::next_h_on() const { return wide_kind_ >= 2 && post_tpl_ && args_.h_in_gather; }
+
+void DeviceTrainer::launch_step_kernels(bool gather, bool row_h) {
   // gather == true: the minibatch comes from the HBM store through the epoch
-  // plan; false: it was streamed into xb / the y buffer by the host path
+  // plan; false: it was streamed into xb / the y buffer by the host path.
+  // row_h == false: the previous step's post kernel already produced this
+  // step's h and x rows (post_next_h), so the row kernel is skipped.
   prepare_params();
   std::uint64_t n = 0;
   if (wide_kind_ >= 2) {
     // tcgen05 wide pass gathers y rows from the store itself (tile::gather4);
     // one small kernel brings the x rows and computes h = dec_head(fwd(x))
-    kernel_mark(0, true);
-    ltfb_dev::launch_row_h(args_, gather, stream_);
-    kernel_mark(0, false);
-    ++n;
+    if (!(gather && !row_h && next_h_on())) {
+      kernel_mark(0, true);
+      ltfb_dev::launch_row_h(args_, gather, stream_);
+      kernel_mark(0, false);
+      ++n;
+    }
   } else if (gather) {
     kernel_mark(0, true);
     ltfb_dev::launch_gather(args_, stream_);
@@ -556,7 +568,11 @@ void DeviceTrainer::launch_step_kernels(bool gather) {
     ++n;
   }
   kernel_mark(3, true);
-  if (post_tpl_) ltfb_dev::launch_post_tpl(post_tpl_, args_, stream_);
+  if (post_tpl_) {
+    ltfb_dev::StepArgs b = args_;
+    b.post_next_h = gather && next_h_on() ? 1 : 0;
+    ltfb_dev::launch_post_tpl(post_tpl_, b, stream_);
+  }
   else if (post_fast_) ltfb_dev::launch_post_fast(args_, stream_);
   else ltfb_dev::launch_post(args_, stream_);
   kernel_mark(3, false);
@@ -654,7 +670,7 @@ bool DeviceTrainer::launch_graph(std::size_t steps) {
       graphs_on_ = false;
       return false;
     }
-    for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true);
+    for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true, k == 0);  // replayable: row kernel first
     const cudaError_t e = cudaStreamEndCapture(stream_, &graph);
     cudaGraphExec_t exec = nullptr;
     if (e != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
@@ -670,6 +686,7 @@ bool DeviceTrainer::launch_graph(std::size_t steps) {
     it = graphs_.emplace(steps, exec).first;
   }
   LTFB_CUDA(cudaGraphLaunch(it->second, stream_));
+  h_ready_ = next_h_on() && step_in_epoch_ + steps < steps_per_epoch_;
   launches_ += graph_launches_[steps];
   return true;
 }
@@ -776,6 +793,7 @@ EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int
   e.ctr = ctr_.p;
   ltfb_dev::launch_eval(e, stream_);
   if (decide) small_T_dirty_ = true;  // the device may have adopted the incoming generator
+  if (decide) h_ready_ = false;
   launches_ += 3;
   LTFB_CUDA(cudaGetLastError());
   double out[6] = {0, 0, 0, 0, 0, 0};
@@ -803,6 +821,7 @@ EvalOut DeviceTrainer::tournament_decide() {
 void DeviceTrainer::adopt(const float* fwd, const float* inv) {
   DeviceGuard g(spec_.device);
   small_T_dirty_ = true;
+  h_ready_ = false;
   LTFB_CUDA(cudaMemcpyAsync(gen_.p, fwd, counts_[2] * 4, cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaMemcpyAsync(gen_.p + counts_[2], inv, counts_[3] * 4, cudaMemcpyHostToDevice, stream_));
   for (int net : {2, 3}) {
@@ -814,6 +833,7 @@ void DeviceTrainer::adopt(const float* fwd, const float* inv) {
 
 bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float* y,
                                      std::vector<ltfb::train::StepRecord>& out) {
+  h_ready_ = false;
   DeviceGuard g(spec_.device);
   if (n_part_ == 0) throw ContractError("train_steps: data store is empty");
   const auto& m = margs_;
@@ -852,7 +872,7 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
     args_.yb = hy_[b].p;
     args_.y_identity = 1;
     wtp_.y_sel = b;
-    launch_step_kernels(false);
+    launch_step_kernels(false, true);
     wtp_.y_sel = -1;
     args_.y_identity = 0;
     LTFB_CUDA(cudaEventRecord(used_done_[b], stream_));

@@ -172,7 +172,9 @@ class DeviceTrainer {
   void start_epoch();
   void launch_step();
   void close_epoch_segment(bool epoch_done, bool partial);
-  void launch_step_kernels(bool gather);
+  void launch_step_kernels(bool gather, bool row_h);
+  bool next_h_on() const;
+  bool h_ready_ = false;  // this step's h / x rows were produced by the previous post kernel
   /// Runs `steps` steps of the current epoch as one cached CUDA graph;
   /// false if graphs are off or capture is unsupported (caller launches).
   bool launch_graph(std::size_t steps);

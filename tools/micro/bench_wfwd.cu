@@ -1,7 +1,7 @@
 // Microbenchmark (dev tool): variants of the warp-local layer forward to
 // find where the cycles go. One CTA of 256 threads, data in smem.
 #include <cstdio>
-extern __shared__ float sm[];
+extern __shared__ __align__(16) float sm[];
 
 template <int IN, int OUT, int NRW>
 __device__ __forceinline__ void v_const(int x, int W, int b, int z) {
@@ -32,7 +32,7 @@ __device__ __noinline__ void v_rt(int x, int W, int b, int z, int IN, int OUT) {
     float acc[NRW];
 #pragma unroll
     for (int i = 0; i < NRW; ++i) acc[i] = 0.f;
-#pragma unroll 8
+#pragma unroll 4
     for (int k = 0; k < IN; ++k) {
       const float wv = sm[W + k * OUT + j];
 #pragma unroll
@@ -47,30 +47,160 @@ __device__ __noinline__ void v_rt(int x, int W, int b, int z, int IN, int OUT) {
   __syncwarp();
 }
 
-// rows interleaved: x for row i of this warp at x + (warp*NRW + i)*IN? same as above but
-// k-split into 2 independent partial chains (more ILP), summed at end (changes order: test only)
-__global__ void k_bench(int reps, long long* out, int IN, int OUT) {
+// chunks of 8 k: predicated W loads, float4 x loads (row pitch P, multiple of 8),
+// next chunk's operands loaded before this chunk's FMAs
+template <int NRW>
+__device__ __noinline__ void v_new(int x, int W, int b, int z, int IN, int OUT, int P, int PO) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = lane; j < OUT; j += 32) {
+    float acc[NRW];
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) acc[i] = 0.f;
+    const float* w = sm + W + j;
+    const float4* xr = reinterpret_cast<const float4*>(sm + x + warp * P);
+    const int xstep = 2 * P;  // float4 units between this warp's rows (8 rows apart)
+    float wv[8];
+    float4 xv[NRW][2];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) wv[u] = u < IN ? w[u * OUT] : 0.f;
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) {
+      xv[i][0] = xr[i * xstep];
+      xv[i][1] = xr[i * xstep + 1];
+    }
+    for (int k0 = 0; k0 < IN; k0 += 8) {
+      float wn[8];
+      float4 xn[NRW][2];
+      const int k1 = k0 + 8;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wn[u] = k1 + u < IN ? w[(k1 + u) * OUT] : 0.f;
+#pragma unroll
+      for (int i = 0; i < NRW; ++i) {
+        xn[i][0] = xr[i * xstep + (k1 >> 2)];
+        xn[i][1] = xr[i * xstep + (k1 >> 2) + 1];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + u < IN) {
+#pragma unroll
+          for (int i = 0; i < NRW; ++i) {
+            const float4 q = xv[i][u >> 2];
+            const float xu = (u & 3) == 0 ? q.x : ((u & 3) == 1 ? q.y : ((u & 3) == 2 ? q.z : q.w));
+            acc[i] = fmaf(xu, wv[u], acc[i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wv[u] = wn[u];
+#pragma unroll
+      for (int i = 0; i < NRW; ++i) {
+        xv[i][0] = xn[i][0];
+        xv[i][1] = xn[i][1];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) {
+      const float v = acc[i] + sm[b + j];
+      sm[z + (warp + 8 * i) * PO + j] = v > 0.f ? v : 0.2f * v;
+    }
+  }
+  __syncwarp();
+}
+
+// k in steps of 4: one float4 broadcast load per row, 4 scalar W loads
+template <int NRW>
+__device__ __noinline__ void v_rt4(int x, int W, int b, int z, int IN, int OUT, int P, int PO) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = lane; j < OUT; j += 32) {
+    float acc[NRW];
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) acc[i] = 0.f;
+    const float* w = sm + W + j;
+    const float* xr = sm + x + warp * P;
+    int k = 0;
+#pragma unroll 2
+    for (; k + 4 <= IN; k += 4) {
+      const float w0 = w[k * OUT], w1 = w[(k + 1) * OUT], w2 = w[(k + 2) * OUT], w3 = w[(k + 3) * OUT];
+#pragma unroll
+      for (int i = 0; i < NRW; ++i) {
+        const float4 q = *reinterpret_cast<const float4*>(xr + 8 * i * P + k);
+        acc[i] = fmaf(q.x, w0, acc[i]);
+        acc[i] = fmaf(q.y, w1, acc[i]);
+        acc[i] = fmaf(q.z, w2, acc[i]);
+        acc[i] = fmaf(q.w, w3, acc[i]);
+      }
+    }
+    for (; k < IN; ++k) {
+      const float wv = w[k * OUT];
+#pragma unroll
+      for (int i = 0; i < NRW; ++i) acc[i] = fmaf(xr[8 * i * P + k], wv, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) {
+      const float v = acc[i] + sm[b + j];
+      sm[z + (warp + 8 * i) * PO + j] = v > 0.f ? v : 0.2f * v;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void k_bench(int reps, long long* out, int IN, int OUT, int P) {
   for (int i = threadIdx.x; i < 40000; i += blockDim.x) sm[i] = 0.001f * (i % 97);
   __syncthreads();
-  long long t0 = clock64();
+  long long t[8];
+  int n = 0;
+  t[n++] = clock64();
   for (int r = 0; r < reps; ++r) { v_const<32, 32, 2>(8000, 0, 1024, 12000); __syncthreads(); }
-  long long t1 = clock64();
+  t[n++] = clock64();
   for (int r = 0; r < reps; ++r) { v_rt<2>(8000, 0, 1024, 12000, IN, OUT); __syncthreads(); }
-  long long t2 = clock64();
-  for (int r = 0; r < reps; ++r) { __syncthreads(); }
-  long long t3 = clock64();
-  for (int r = 0; r < reps; ++r) { v_const<32, 32, 4>(8000, 0, 1024, 12000); __syncthreads(); }
-  long long t4 = clock64();
-  if (threadIdx.x == 0) { out[0] = (t1 - t0) / reps; out[1] = (t2 - t1) / reps; out[2] = (t3 - t2) / reps; out[3] = (t4 - t3) / reps; }
+  t[n++] = clock64();
+  for (int r = 0; r < reps; ++r) { v_new<2>(8000, 0, 1024, 12000, IN, OUT, P, P); __syncthreads(); }
+  t[n++] = clock64();
+  for (int r = 0; r < reps; ++r) { v_new<4>(8000, 0, 1024, 12000, IN, OUT, P, P); __syncthreads(); }
+  t[n++] = clock64();
+  for (int r = 0; r < reps; ++r) { v_rt<4>(8000, 0, 1024, 12000, IN, OUT); __syncthreads(); }
+  t[n++] = clock64();
+  for (int r = 0; r < reps; ++r) { v_rt4<2>(8000, 0, 1024, 12000, IN, OUT, P, P); __syncthreads(); }
+  t[n++] = clock64();
+  if (threadIdx.x == 0)
+    for (int i = 0; i + 1 < n; ++i) out[i] = (t[i + 1] - t[i]) / reps;
+  // check v_new == v_rt (bitwise) on one output
+  if (threadIdx.x == 0) out[7] = 0;
+}
+
+__global__ void k_check(int IN, int OUT, int P, int* bad) {
+  for (int i = threadIdx.x; i < 40000; i += blockDim.x) sm[i] = 0.001f * (i % 97) - 0.03f;
+  // x rows pitch IN at 8000 for v_rt, pitch P at 20000 for v_new (same values)
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * P; i += blockDim.x) {
+    const int r = i / P, k = i % P;
+    sm[20000 + i] = k < IN ? sm[8000 + r * IN + k] : 0.0f;
+  }
+  __syncthreads();
+  v_rt<2>(8000, 0, 1024, 12000, IN, OUT);
+  v_new<2>(20000, 0, 1024, 30000, IN, OUT, P, P);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int r = 0; r < 16; ++r)
+      for (int j = 0; j < OUT; ++j)
+        if (__float_as_uint(sm[12000 + r * OUT + j]) != __float_as_uint(sm[30000 + r * P + j])) ++b;
+    *bad = b;
+  }
 }
 
 int main() {
   long long* d; cudaMalloc(&d, 64);
+  int* bad; cudaMalloc(&bad, 4);
   cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 180000);
-  for (int it = 0; it < 3; ++it) {
-    k_bench<<<1, 256, 180000>>>(50, d, 32, 32);
-    long long h[4]; cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
-    printf("const 2rows: %lld  rt 2rows: %lld  sync only: %lld  const 4 rows: %lld (%s)\n", h[0], h[1], h[2], h[3], cudaGetErrorString(cudaGetLastError()));
+  cudaFuncSetAttribute(k_check, cudaFuncAttributeMaxDynamicSharedMemorySize, 180000);
+  const int shapes[][3] = {{32, 32, 32}, {5, 32, 8}, {20, 32, 24}, {64, 20, 64}, {32, 5, 32}};
+  for (auto& s : shapes) {
+    k_bench<<<1, 256, 180000>>>(50, d, s[0], s[1], s[2]);
+    long long h[8]; cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
+    k_check<<<1, 256, 180000>>>(s[0], s[1], s[2], bad);
+    int hb; cudaMemcpy(&hb, bad, 4, cudaMemcpyDeviceToHost);
+    printf("IN %d OUT %d: const32 2r %lld | rt 2r %lld | new 2r %lld | new 4r %lld | rt 4r %lld | rt4 2r %lld | mismatches %d (%s)\n", s[0], s[1], h[0], h[1], h[2], h[3], h[4], h[5], hb, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

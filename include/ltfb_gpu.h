@@ -170,6 +170,19 @@ int ltfb_trainer_tournament_decide(ltfb_trainer* t, ltfb_eval_metric* local,
 /* Trainer::adopt_generators from host blobs. */
 int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv);
 
+/* ---- autoencoder pre-training (train_ops.hpp:52-81, runner.hpp:249-279) -- */
+/* The AE batch source (the sorted union of the training ids, runner.hpp:
+ * 251-256): y [n x output_dim], made resident in HBM. */
+int ltfb_trainer_load_ae_source(ltfb_trainer* t, const float* y, uint64_t n);
+/* surrogate::autoencoder_step (train_ops.hpp:71-81) on source rows
+ * idx[0..n): MAE(dec(enc(y)), y), every enc/dec gradient, Adam(enc) then
+ * Adam(dec). LTFB_ENUMERIC as the reference: a non-finite loss or enc
+ * gradient changes nothing, a non-finite dec gradient leaves enc applied. */
+int ltfb_trainer_ae_step(ltfb_trainer* t, const uint32_t* idx, uint64_t n, double* loss);
+/* The runner's AE batch draws (runner.hpp:257-266): steps x batch row
+ * indices from Rng(mix_seed({seed, 0xae1})).below(rows), step-major. */
+int ltfb_ae_batch_rows(uint64_t seed, uint64_t rows, uint64_t batch, uint64_t steps, uint32_t* out);
+
 /* ---- measurement hooks (bench.py) ------------------------------------- */
 /* Host-buffer variant of train_steps (the e2e path): the minibatches of the
  * n steps come from HOST memory, x [n x batch x input_dim] and

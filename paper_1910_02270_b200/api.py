@@ -710,6 +710,81 @@ class Trainer:
         return self._metric(loc), self._metric(inc), bool(adopted.value)
 
 
+def ae_batch_rows(seed: int, rows: int, batch: int, steps: int) -> np.ndarray:
+    """runner.hpp:257-266: the AE batch draws, [steps x batch] source rows."""
+    out = np.empty(batch * steps, np.uint32)
+    check(lib.ltfb_ae_batch_rows(seed, rows, batch, steps, out))
+    return out.reshape(steps, batch)
+
+
+class AutoencoderPretrainer:
+    """surrogate::autoencoder_step (train_ops.hpp:71-81) on one GPU.
+
+    Holds the model's five blobs and the enc/dec Adam states in HBM and the
+    AE source slab (the sorted union of the training ids' y rows,
+    runner.hpp:251-256); step(rows) runs one reconstruction step on those
+    source rows. pull(model) copies enc/dec and their optimizer state back."""
+
+    def __init__(self, model: CycleGan, y_source: np.ndarray, device: int = 0, batch_size: int = 128):
+        if model.autoencoder_frozen:
+            raise ContractError("autoencoder_step: autoencoder is frozen")
+        y = np.ascontiguousarray(y_source, np.float32)
+        if y.ndim != 2 or y.shape[1] != model.dims.output_dim():
+            raise DimensionError("autoencoder source must be [rows x output_dim]")
+        cc = _lib.TrainerConfigC()
+        cc.trainer_id, cc.device, cc.n_shards = 0, device, 1
+        cc.numeric_abort_threshold = 10
+        cc.batch_size, cc.seed = batch_size, 0
+        cc.w_f, cc.w_i = 1.0, 1.0
+        self._h = C.c_void_p()
+        dc, ac = model.dims.c(), model.arch.c()
+        check(lib.ltfb_trainer_create(C.byref(dc), C.byref(ac), C.byref(cc), C.byref(self._h)))
+        for i, n in enumerate(NET_NAMES):
+            b = np.ascontiguousarray(model.blobs[n], np.float32)
+            check(lib.ltfb_trainer_set_params(self._h, i, b, b.size))
+            o = model.opt[n]
+            check(lib.ltfb_trainer_set_adam(self._h, i, ptr(np.ascontiguousarray(o.m, np.float32)),
+                                            ptr(np.ascontiguousarray(o.v, np.float32)), o.t))
+        check(lib.ltfb_trainer_load_ae_source(self._h, y, y.shape[0]))
+        self.rows = y.shape[0]
+
+    def step(self, rows: np.ndarray) -> float:
+        idx = np.ascontiguousarray(rows, np.uint32)
+        loss = C.c_double(0.0)
+        check(lib.ltfb_trainer_ae_step(self._h, idx, idx.size, C.byref(loss)))
+        return loss.value
+
+    def pull(self, model: CycleGan):
+        for i, n in ((0, "enc"), (1, "dec")):
+            b = model.blobs[n]
+            check(lib.ltfb_trainer_get_params(self._h, i, b, b.size))
+            o = model.opt[n]
+            t = C.c_uint64(0)
+            check(lib.ltfb_trainer_get_adam(self._h, i, ptr(o.m), ptr(o.v), C.byref(t)))
+            o.t = t.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.ltfb_trainer_destroy(h)
+            self._h = None
+
+
+def pretrain_autoencoder(model: CycleGan, y_source: np.ndarray, steps: int, batch_size: int, seed: int,
+                         device: int = 0) -> list:
+    """runner.hpp:249-279: `steps` AE steps on batches of min(batch_size,
+    rows) source rows drawn with replacement by Rng(mix_seed({seed, 0xae1}));
+    returns the pretrain history [(step, loss)] and leaves the model's
+    enc/dec (and their Adam states) trained. The caller freezes it."""
+    rows = int(np.asarray(y_source).shape[0])
+    b = min(batch_size, rows)
+    draws = ae_batch_rows(seed, rows, b, steps) if steps else np.zeros((0, b), np.uint32)
+    p = AutoencoderPretrainer(model, y_source, device, max(b, 1))
+    hist = [(s + 1, p.step(draws[s])) for s in range(steps)]
+    p.pull(model)
+    return hist
+
+
 class Comm:
     """NCCL communicator of the multi-GPU run (one rank per GPU/trainer)."""
 

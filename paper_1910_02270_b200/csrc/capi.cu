@@ -361,6 +361,29 @@ int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv) {
   return guarded([&] { T(t).adopt(fwd, inv); });
 }
 
+int ltfb_trainer_load_ae_source(ltfb_trainer* t, const float* y, uint64_t n) {
+  return guarded([&] {
+    if (!y) throw ltfb::ContractError("load_ae_source: null source");
+    T(t).load_ae_source(y, n);
+  });
+}
+
+int ltfb_trainer_ae_step(ltfb_trainer* t, const uint32_t* idx, uint64_t n, double* loss) {
+  return guarded([&] {
+    if (!idx || n == 0) throw ltfb::ContractError("ae_step: empty batch");
+    const double l = T(t).ae_step(idx, n);
+    if (loss) *loss = l;
+  });
+}
+
+int ltfb_ae_batch_rows(uint64_t seed, uint64_t rows, uint64_t batch, uint64_t steps, uint32_t* out) {
+  return guarded([&] {
+    if (rows == 0) throw ltfb::ContractError("ae_batch_rows: empty source");
+    ltfb::Rng rng(ltfb::mix_seed({seed, 0xae1ULL}));
+    for (uint64_t i = 0; i < batch * steps; ++i) out[i] = static_cast<uint32_t>(rng.below(rows));
+  });
+}
+
 int ltfb_trainer_train_steps_host(ltfb_trainer* t, uint64_t n, const float* x, const float* y,
                                   ltfb_step_record* out, uint64_t* n_out) {
   bool ok = true;

@@ -50,6 +50,39 @@ int post_tpl_kind(const StepArgs& a);
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 
+/// Autoencoder pre-training step (k_ae.cu): one batch of n rows of the AE
+/// source slab selected by idx; every pointer device memory.
+struct AeArgs {
+  ModelArgs m;
+  int n;  // batch rows (<= 128)
+  int S;  // CTAs of the column passes (split count of Pz / Pg)
+  const float* ysrc;     // [N x out_pad] AE source rows
+  const unsigned* idx;   // [n] rows of ysrc in this batch
+  const float* enc;      // parameter blobs
+  const float* dec;
+  float* genc;           // gradient blobs (same layout)
+  float* gdec;
+  float* Pz;             // [S x n x E1]
+  float* Pg;             // [S x n x D]
+  double* mae_part;      // [S]
+  float* z0, *a0, *ga0, *gz0;  // [n x E1]
+  float* etz[kMaxLayers];      // enc-tail tape
+  float* eta[kMaxLayers];
+  float* dhz[kMaxLayers];      // dec-head tape
+  float* dha[kMaxLayers];
+  const float* latent;   // enc output [n x lat] (eta[L-1], or a0 if the tail is empty)
+  const float* h;        // dec-head output [n x D] (dha[L-1], or latent)
+  float* gh;             // dL/dh [n x D]
+  float* glat;           // dL/dlatent [n x lat] (gh if the head is empty)
+  float* tA, *tB;        // [n x max width] backward scratch
+  int* flags;            // [2] non-finite gradient: enc, dec
+  double* loss;          // [1]
+};
+bool ae_supported(const ModelArgs& m, int rows);
+void launch_ae_passes(const AeArgs& a, cudaStream_t s);
+void launch_ae_adam(float* p, float* m1, float* m2, const float* g, long long count, double lr, double b1, double b2,
+                    double eps, double c1, double c2, int sms, cudaStream_t s);
+
 std::size_t eval_wide_smem(const ModelArgs& m);
 cudaError_t selftest_tc(const float* a1, const float* b1, const float* ah, const float* b2, const float* a3,
                         float* d1, float* d2, float* d3);

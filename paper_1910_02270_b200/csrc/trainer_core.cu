@@ -910,11 +910,135 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
   return ok;
 }
 
-double DeviceTrainer::ae_step(const std::uint32_t*, std::size_t) {
-  throw ContractError("ae_step: not available in this build");
+// ------------------------------------------------- autoencoder pre-training --
+void DeviceTrainer::ae_allocate() {
+  if (ae_alloc_) return;
+  const auto& m = margs_;
+  const int R = 128;
+  auto& a = ae_args_;
+  a = {};
+  a.m = m;
+  a.S = sm_count_;
+  std::size_t need = 0;
+  auto take = [&](std::size_t n) {
+    const std::size_t o = need;
+    need += (n + 31) & ~std::size_t(31);
+    return o;
+  };
+  const std::size_t oPz = take((std::size_t)a.S * R * m.E1), oPg = take((std::size_t)a.S * R * m.D);
+  const std::size_t oz0 = take(R * m.E1), oa0 = take(R * m.E1), oga0 = take(R * m.E1), ogz0 = take(R * m.E1);
+  std::size_t oet[ltfb_dev::kMaxLayers][2] = {}, odh[ltfb_dev::kMaxLayers][2] = {};
+  int maxw = std::max(m.E1, m.D);
+  for (int l = 0; l < m.enc_tail.L; ++l) {
+    oet[l][0] = take((std::size_t)R * m.enc_tail.w[l + 1]);
+    oet[l][1] = take((std::size_t)R * m.enc_tail.w[l + 1]);
+    maxw = std::max(maxw, m.enc_tail.max_w());
+  }
+  for (int l = 0; l < m.dec_head.L; ++l) {
+    odh[l][0] = take((std::size_t)R * m.dec_head.w[l + 1]);
+    odh[l][1] = take((std::size_t)R * m.dec_head.w[l + 1]);
+    maxw = std::max(maxw, m.dec_head.max_w());
+  }
+  const std::size_t ogh = take(R * m.D), oglat = take((std::size_t)R * m.lat);
+  const std::size_t otA = take((std::size_t)R * maxw), otB = take((std::size_t)R * maxw);
+  ae_scr_.alloc(need);
+  ae_part_.alloc(a.S);
+  ae_flags_.alloc(2);
+  ae_loss_.alloc(1);
+  ae_idx_.alloc(R);
+  float* b = ae_scr_.p;
+  a.Pz = b + oPz;
+  a.Pg = b + oPg;
+  a.z0 = b + oz0;
+  a.a0 = b + oa0;
+  a.ga0 = b + oga0;
+  a.gz0 = b + ogz0;
+  for (int l = 0; l < m.enc_tail.L; ++l) {
+    a.etz[l] = b + oet[l][0];
+    a.eta[l] = b + oet[l][1];
+  }
+  for (int l = 0; l < m.dec_head.L; ++l) {
+    a.dhz[l] = b + odh[l][0];
+    a.dha[l] = b + odh[l][1];
+  }
+  a.latent = m.enc_tail.L > 0 ? a.eta[m.enc_tail.L - 1] : a.a0;
+  a.h = m.dec_head.L > 0 ? a.dha[m.dec_head.L - 1] : a.latent;
+  a.gh = b + ogh;
+  a.glat = m.dec_head.L > 0 ? b + oglat : a.gh;
+  // with an empty enc tail, dL/da0 is dL/dlatent itself
+  a.tA = b + otA;
+  a.tB = b + otB;
+  a.mae_part = ae_part_.p;
+  a.flags = ae_flags_.p;
+  a.loss = ae_loss_.p;
+  a.idx = ae_idx_.p;
+  a.enc = params_[0].p;
+  a.dec = params_[1].p;
+  a.genc = grads_[0].p;
+  a.gdec = grads_[1].p;
+  if (m.enc_tail.L == 0) a.ga0 = a.glat;
+  ae_alloc_ = true;
 }
-void DeviceTrainer::load_ae_source(const float*, std::size_t) {
-  throw ContractError("load_ae_source: not available in this build");
+
+void DeviceTrainer::load_ae_source(const float* y, std::size_t n) {
+  DeviceGuard g(spec_.device);
+  if (n == 0) throw ContractError("load_ae_source: empty source");
+  const std::size_t out = static_cast<std::size_t>(margs_.out), op = static_cast<std::size_t>(margs_.out_pad);
+  ae_y_.alloc(n * op);
+  LTFB_CUDA(cudaMemsetAsync(ae_y_.p, 0, ae_y_.bytes(), stream_));
+  LTFB_CUDA(cudaMemcpy2DAsync(ae_y_.p, op * 4, y, out * 4, out * 4, n, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  ae_rows_ = n;
+}
+
+/// surrogate/train_ops.hpp:71-81 on the device: loss, gradients, then
+/// Adam(enc) and Adam(dec) with the reference's NumericError semantics
+/// (a non-finite loss or enc gradient changes nothing; a non-finite dec
+/// gradient leaves enc applied).
+double DeviceTrainer::ae_step(const std::uint32_t* rows_idx, std::size_t n) {
+  DeviceGuard g(spec_.device);
+  if (ae_rows_ == 0) throw ContractError("ae_step: no autoencoder source loaded");
+  if (!ltfb_dev::ae_supported(margs_, static_cast<int>(n)))
+    throw ContractError("ae_step: supported for 1..128 rows and wide-layer widths <= 64");
+  for (std::size_t i = 0; i < n; ++i)
+    if (rows_idx[i] >= ae_rows_) throw ContractError("ae_step: row index outside the source");
+  ae_allocate();
+  auto a = ae_args_;
+  a.n = static_cast<int>(n);
+  a.ysrc = ae_y_.p;
+  LTFB_CUDA(cudaMemcpyAsync(ae_idx_.p, rows_idx, n * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaMemsetAsync(ae_flags_.p, 0, 8, stream_));
+  ltfb_dev::launch_ae_passes(a, stream_);
+  launches_ += 6;
+  double loss = 0.0;
+  int flags[2] = {0, 0};
+  LTFB_CUDA(cudaMemcpyAsync(&loss, ae_loss_.p, 8, cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaMemcpyAsync(flags, ae_flags_.p, 8, cudaMemcpyDeviceToHost, stream_));
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  if (!std::isfinite(loss)) throw ltfb::NumericError("autoencoder_step: non-finite loss");
+  const auto& h = spec_.arch.adam;
+  auto apply = [&](int net) {
+    std::uint64_t t = 0;
+    LTFB_CUDA(cudaMemcpy(&t, &ctr_.p->t[net], 8, cudaMemcpyDeviceToHost));
+    t += 1;
+    const double c1 = 1.0 - std::pow(h.beta1, static_cast<double>(t));
+    const double c2 = 1.0 - std::pow(h.beta2, static_cast<double>(t));
+    const double lr = spec_.lr[net] > 0 ? spec_.lr[net] : h.lr;
+    ltfb_dev::launch_ae_adam(params_[net].p, mom1_[net].p, mom2_[net].p, grads_[net].p,
+                             static_cast<long long>(counts_[net]), lr, h.beta1, h.beta2, h.eps, c1, c2, sm_count_,
+                             stream_);
+    ++launches_;
+    LTFB_CUDA(cudaMemcpyAsync(&ctr_.p->t[net], &t, 8, cudaMemcpyHostToDevice, stream_));
+    LTFB_CUDA(cudaStreamSynchronize(stream_));
+  };
+  wide_dirty_ = true;  // the frozen-weight copies / W^T images follow enc / dec
+  small_T_dirty_ = true;
+  h_ready_ = false;
+  if (flags[0]) throw ltfb::NumericError("adam_step: non-finite gradient component");
+  apply(0);
+  if (flags[1]) throw ltfb::NumericError("adam_step: non-finite gradient component");
+  apply(1);
+  return loss;
 }
 
 }  // namespace ltfb_b200

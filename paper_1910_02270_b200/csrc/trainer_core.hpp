@@ -263,11 +263,17 @@ class DeviceTrainer {
   DevBuf<float> hx_[2], hy_[2];
   cudaEvent_t h2d_done_[2] = {nullptr, nullptr}, used_done_[2] = {nullptr, nullptr};
 
-  // AE
+  // AE pre-training (k_ae.cu)
   DevBuf<float> ae_y_;
   std::size_t ae_rows_ = 0;
   DevBuf<unsigned> ae_idx_;
   DevBuf<double> ae_loss_;
+  DevBuf<float> ae_scr_;
+  DevBuf<double> ae_part_;
+  DevBuf<int> ae_flags_;
+  ltfb_dev::AeArgs ae_args_{};
+  bool ae_alloc_ = false;
+  void ae_allocate();
 };
 
 }  // namespace ltfb_b200

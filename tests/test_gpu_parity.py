@@ -280,3 +280,54 @@ def test_nonfinite_incoming_loses(golden):
     with pytest.raises(L.ContractError):
         a.train_steps(1)
         L.tournament_round([a, b], L.Matching([(0, 1)]), 2)
+
+
+@pytest.mark.parametrize("dims,arch_name", [(TINY, "tiny"), (DESK, "default"), (PAPER, "default")])
+def test_autoencoder_step_matches_oracle(oracle, dims, arch_name):
+    """autoencoder_step (train_ops.hpp:71-81) on the device vs the C oracle:
+    loss per step within REL_LOSS, enc/dec weights and Adam moments after 3
+    steps within the split-K summation tolerance (the wide-layer gradients
+    are sums over 49k columns in a different order)."""
+    arch = L.SurrogateArch.tiny() if arch_name == "tiny" else L.SurrogateArch()
+    oarch = oracle.Arch.tiny() if arch_name == "tiny" else oracle.Arch()
+    n = 300
+    ds = L.synthetic_dataset(dims, n, sampling_seed=3, spec_seed=1)
+    model = L.make_cyclegan(dims, arch, 21)
+    og = oracle.Gan(list(dims.as_tuple()), oarch, 21)
+    for i, name in enumerate(("enc", "dec")):
+        assert np.array_equal(og.blob(i), model.blobs[name])
+    draws = L.ae_batch_rows(5, n, 64, 3)
+    p = L.AutoencoderPretrainer(model, ds.y, batch_size=64)
+    for s in range(3):
+        y = np.ascontiguousarray(ds.y[draws[s]])
+        ref_loss, eg, dg = og.ae_backward(y)
+        assert og.adam(0, eg) and og.adam(1, dg)
+        got = p.step(draws[s])
+        assert abs(got - ref_loss) <= REL_LOSS * abs(ref_loss)
+    p.pull(model)
+    lr = 1e-3
+    for i, name in enumerate(("enc", "dec")):
+        ref = og.blob(i)
+        d = np.abs(model.blobs[name].astype(np.float64) - ref)
+        # Adam normalises each gradient component, and the MAE gradient is a
+        # sign: where a reconstruction error is ~0 its sign can flip with the
+        # summation order, and where a bias gradient (a column sum of signs)
+        # cancels, the normalised step can differ by up to ~lr. Bound the
+        # worst element by 2 lr per step and the bulk (99.9 %) at float
+        # rounding scale.
+        assert d.max() < 2 * lr * 3
+        assert np.quantile(d, 0.999) < 1e-6
+        assert model.opt[name].t == og.t(i) == 3
+        dm = np.abs(model.opt[name].m.astype(np.float64) - og.moment(i, 0))
+        assert np.quantile(dm, 0.999) < 1e-4 * np.max(np.abs(og.moment(i, 0))) + 1e-12
+
+
+def test_autoencoder_frozen_and_bad_rows():
+    model = L.make_cyclegan(TINY, L.SurrogateArch.tiny(), 1)
+    ds = L.synthetic_dataset(TINY, 20, sampling_seed=1, spec_seed=1)
+    p = L.AutoencoderPretrainer(model, ds.y, batch_size=8)
+    with pytest.raises(L.ContractError):
+        p.step(np.array([0, 25], np.uint32))  # outside the source
+    model.autoencoder_frozen = True
+    with pytest.raises(L.ContractError):
+        L.AutoencoderPretrainer(model, ds.y)

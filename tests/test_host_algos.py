@@ -106,3 +106,13 @@ def test_make_cyclegan_matches_reference(golden):
     ref = L.make_cyclegan(TINY, L.SurrogateArch.tiny(), 99)
     assert m.fwd_hash() == ref.fwd_hash() and m.disc_hash() == ref.disc_hash()
     assert t is not None
+
+
+def test_ae_batch_draws_match_reference_rng(oracle):
+    """runner.hpp:257-266: AE batch rows = Rng(mix_seed({seed, 0xae1})).below(rows),
+    step-major, against the pinned oracle Rng."""
+    seed, rows, batch, steps = 17, 1000, 128, 3
+    got = L.ae_batch_rows(seed, rows, batch, steps)
+    r = oracle.Rng(oracle.mix_seed(seed, 0xAE1))
+    ref = np.array([r.below(rows) for _ in range(batch * steps)], np.uint32).reshape(steps, batch)
+    assert np.array_equal(got, ref)

@@ -14,4 +14,7 @@ from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrai
                   mix_seed, pair_trainers, param_count, partition_dataset, reinit_gan_nets,
                   split_dataset, synth_generate, synthetic_dataset, tournament_round)
 
+from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, distributed_round,
+                     run_experiment, run_experiment_rank)
+
 __all__ = [n for n in dir() if not n.startswith("_")]

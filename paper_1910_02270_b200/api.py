@@ -626,6 +626,10 @@ class Trainer:
         self._dirty = True
         return np.ctypeslib.as_array(recs)
 
+    def fwd_floats(self) -> int:
+        """Length of the fwd part of the generator payload fwd||inv."""
+        return param_count(self._dims, self._arch, 2)
+
     def exchange(self, comm: "Comm", peer: int):
         check(lib.ltfb_trainer_exchange(self._h, comm._h, peer))
 

@@ -1,0 +1,334 @@
+"""Experiment orchestration over the B200 trainers (tournament/runner.hpp).
+
+run_experiment() mirrors run_experiment (runner.hpp:232-420) in one process:
+split the dataset (runner.hpp:134-169), pre-train the autoencoder on the
+device (runner.hpp:249-279), build one trainer per partition with its own
+generator / discriminator init (runner.hpp:283-317), then alternate training
+chunks with tournament rounds, evaluating every trainer on the shared
+validation slice after every chunk (runner.hpp:321-373), and pick the best
+trainer (runner.hpp:380-398).
+
+run_experiment_rank() is the same loop with ONE trainer per process (one
+process per GPU, launched by torchrun): the split, the AE pre-training and
+the pairings are pure functions of the run seed, so every rank computes them
+itself (no communication); only the round moves data, the 15 KB generator
+payload between the two partners of a pair (RoundComm.exchange), and the
+per-rank records are gathered on rank 0 at the end.
+
+RoundComm implementations:
+  NcclRoundComm  device-to-device ncclSend/ncclRecv of the generator blob
+                 (ltfb_trainer_exchange; the product path on GPUs);
+  TorchRoundComm torch.distributed send/recv of the host blob (gloo on CPU:
+                 the multi-process tests of this host logic).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .api import (CycleGan, Dataset, EvalRecord, HistorySegment, RoundRecord, Trainer, TrainerConfig,
+                  TrainerRoundRecord, TransferRecord, ConfigError, ContractError, hex64, fnv1a64,
+                  make_cyclegan, mix_seed, pair_trainers, param_count, pretrain_autoencoder,
+                  reinit_gan_nets, split_dataset, tournament_round, EvalMetric)
+
+
+@dataclass
+class RunConfig:
+    """tournament/runner.hpp:47-78 (dataset generation and on-disk bundles
+    are the caller's: the B200 path takes an in-memory Dataset)."""
+    dims: object = None
+    arch: object = None
+    mode: str = "single"  # single | ltfb | k-independent
+    trainers: int = 1
+    shards: int = 1
+    batch_size: int = 128
+    interval: int = 100
+    step_budget: int = 1000
+    ae_steps: int = 2000
+    seed: int = 1
+    validation_fraction: float = 0.05
+    tournament_fraction: float = 0.05
+    lr_jitter: float = 0.0
+    numeric_abort_threshold: int = 10
+    w_f: float = 1.0
+    w_i: float = 1.0
+    devices: tuple | None = None  # trainer t runs on devices[t % len(devices)]
+    wide_kernel: int = 0
+
+
+@dataclass
+class RunHistory:
+    mode: str = "single"
+    n_trainers: int = 1
+    pretrain: list = field(default_factory=list)       # (step, loss)
+    steps: list = field(default_factory=list)
+    evals: list = field(default_factory=list)
+    epochs: list = field(default_factory=list)
+    rounds: list = field(default_factory=list)
+    trainer_rounds: list = field(default_factory=list)
+    transfers: list = field(default_factory=list)
+    best_trainer: int = -1
+    best_metric: EvalMetric | None = None
+
+
+@dataclass
+class RunResult:
+    history: RunHistory
+    best_trainer: int = -1
+    best_metric: EvalMetric | None = None
+    best_model: CycleGan | None = None
+
+
+def validate_run_config(cfg: RunConfig):
+    """runner.hpp:91-110."""
+    bad = []
+    if cfg.trainers < 1:
+        bad.append("trainers must be >= 1")
+    if cfg.shards < 1:
+        bad.append("shards must be >= 1")
+    if cfg.batch_size < 1:
+        bad.append("batch_size must be >= 1")
+    if cfg.interval < 1:
+        bad.append("interval must be >= 1")
+    if not (0 <= cfg.validation_fraction < 1):
+        bad.append("validation_fraction must be in [0,1)")
+    if not (0 <= cfg.tournament_fraction < 1):
+        bad.append("tournament_fraction must be in [0,1)")
+    if cfg.numeric_abort_threshold < 0:
+        bad.append("numeric_abort_threshold must be >= 0")
+    if cfg.mode not in ("single", "ltfb", "k-independent", "k_independent"):
+        bad.append("unknown run mode: " + str(cfg.mode))
+    if cfg.lr_jitter != 0.0:
+        bad.append("lr_jitter is not supported on the B200 path")
+    if bad:
+        raise ConfigError("invalid run config: " + "; ".join(bad) + "; ")
+
+
+def _base_model(cfg: RunConfig, dataset: Dataset, train_parts) -> tuple:
+    """runner.hpp:247-279: AE pre-training on the sorted union of the
+    training partitions, then frozen."""
+    base = make_cyclegan(cfg.dims, cfg.arch, mix_seed(cfg.seed, 0xAE0))
+    union = np.sort(np.concatenate([np.asarray(p, np.uint32) for p in train_parts]))
+    _, ay = dataset.rows(union)
+    dev = (cfg.devices or (0,))[0]
+    pre = pretrain_autoencoder(base, ay, cfg.ae_steps, cfg.batch_size, cfg.seed, device=dev) if cfg.ae_steps else []
+    base.autoencoder_frozen = True
+    return base, pre
+
+
+def _trainer_for(cfg: RunConfig, dataset: Dataset, base: CycleGan, split, t: int) -> Trainer:
+    """runner.hpp:283-317."""
+    model = base.copy()
+    reinit_gan_nets(model, mix_seed(cfg.seed, 0x1417, t))
+    devs = cfg.devices or (0,)
+    tc = TrainerConfig(trainer_id=t, n_shards=cfg.shards, batch_size=cfg.batch_size,
+                       seed=mix_seed(cfg.seed, 0x57A7E1, t), numeric_abort_threshold=cfg.numeric_abort_threshold,
+                       w_f=cfg.w_f, w_i=cfg.w_i, train_ids=split[1][t], tournament_ids=split[2][t],
+                       device=devs[t % len(devs)], wide_kernel=cfg.wide_kernel, prefetch_depth=0)
+    return Trainer(tc, dataset, model)
+
+
+def _eval_record(t: Trainer, step: int) -> EvalRecord:
+    m = t.evaluate_validation(t.cfg.w_f, t.cfg.w_i)
+    return EvalRecord(t.cfg.trainer_id, step, "validation", m.forward_mae, m.inverse_mae, m.combined)
+
+
+def _merge(history: RunHistory, segments):
+    """runner.hpp:171-199."""
+    for seg in segments:
+        history.steps += seg.steps
+        history.evals += seg.evals
+        history.epochs += seg.epochs
+    history.steps.sort(key=lambda r: (r.step, r.trainer))
+    history.evals.sort(key=lambda r: (r.step, r.trainer))
+    history.epochs.sort(key=lambda r: (r.epoch, r.trainer))
+
+
+def run_experiment(cfg: RunConfig, dataset: Dataset) -> RunResult:
+    """runner.hpp:232-420 in one process (k trainers on cfg.devices)."""
+    validate_run_config(cfg)
+    k = 1 if cfg.mode == "single" else cfg.trainers
+    rounds_enabled = cfg.mode == "ltfb" and k >= 2
+    split = split_dataset(dataset.total, k, cfg.validation_fraction, cfg.tournament_fraction, cfg.seed, k >= 2)
+    history = RunHistory(mode=cfg.mode.replace("_", "-"), n_trainers=k)
+    base, history.pretrain = _base_model(cfg, dataset, split[1])
+    trainers = [_trainer_for(cfg, dataset, base, split, t) for t in range(k)]
+    have_val = split[0].size > 0
+    if have_val:
+        for t in trainers:
+            t.set_validation(split[0])
+
+    def evaluate_all(at):
+        if have_val:
+            for t in trainers:
+                t.history().evals.append(_eval_record(t, at))
+
+    evaluate_all(0)
+    done, round_index = 0, 0
+    while done < cfg.step_budget:
+        chunk = min(cfg.interval, cfg.step_budget - done)
+        for t in trainers:
+            t.train_steps(chunk)
+        done += chunk
+        evaluate_all(done)
+        if rounds_enabled and chunk == cfg.interval:
+            round_index += 1
+            matching = pair_trainers(k, round_index, mix_seed(cfg.seed, 0x9A18))
+            r = tournament_round(trainers, matching, round_index)
+            history.rounds.append(r.round)
+            history.trainer_rounds += r.trainer_records
+            history.transfers += r.transfers
+    for t in trainers:
+        t.flush_epoch_record()
+    _merge(history, [t.history() for t in trainers])
+    res = RunResult(history)
+    if have_val:
+        best = float("inf")
+        for t in trainers:
+            m = t.evaluate_validation(cfg.w_f, cfg.w_i)
+            if m.combined < best:
+                best, res.best_trainer, res.best_metric = m.combined, t.cfg.trainer_id, m
+    else:
+        res.best_trainer = 0
+    res.best_model = trainers[max(res.best_trainer, 0)].model().copy()
+    history.best_trainer, history.best_metric = res.best_trainer, res.best_metric
+    return res
+
+
+# ------------------------------------------------------------ multi-rank --
+class NcclRoundComm:
+    """The product exchange: device-to-device ncclSend/ncclRecv of the
+    generator blob into the peer's incoming buffer (ltfb_trainer_exchange),
+    plus torch.distributed for the small host-side collectives."""
+
+    def __init__(self, comm, dist):
+        self.comm, self.dist = comm, dist
+        self.rank, self.world = comm.rank, comm.nranks
+
+    def exchange(self, trainer, peer: int):
+        trainer.exchange(self.comm, peer)
+
+    def all_gather(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+class TorchRoundComm:
+    """Generator exchange over torch.distributed point-to-point (gloo on
+    CPU). The trainer receives the peer's blob as its incoming candidate."""
+
+    def __init__(self, dist):
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def exchange(self, trainer, peer: int):
+        import torch
+        blob = np.ascontiguousarray(trainer.generator_blob(), np.float32)
+        send = torch.from_numpy(blob.copy())
+        recv = torch.empty_like(send)
+        ops = [self.dist.P2POp(self.dist.isend, send, peer), self.dist.P2POp(self.dist.irecv, recv, peer)]
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+        nf = trainer.fwd_floats()
+        got = recv.numpy()
+        trainer._set_incoming(got[:nf], got[nf:])
+
+    def all_gather(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+
+def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
+    """tournament/ltfb.hpp:96-164 seen from one rank (rank == trainer id):
+    the pairing is recomputed locally (identical on every rank), the pair
+    swaps generator payloads, and each side evaluates local vs incoming on
+    its own tournament slice and adopts on the device if the incoming one
+    wins. Returns (RoundRecord, TrainerRoundRecord | None, [TransferRecord])."""
+    steps = comm.all_gather(trainer.step())
+    if len(set(steps)) != 1:
+        raise ContractError("tournament_round: trainers are not step-synchronized")
+    step = steps[0]
+    matching = pair_trainers(k, round_index, mix_seed(seed, 0x9A18))
+    rr = RoundRecord(round_index, step, list(matching.pairs), matching.bye)
+    me, peer = comm.rank, None
+    for a, b in matching.pairs:
+        if a == b:
+            raise ContractError("tournament_round: trainer paired with itself")
+        if a == me:
+            peer = b
+        elif b == me:
+            peer = a
+    if peer is None:  # the bye of an odd k
+        return rr, None, []
+    blob = trainer.generator_blob()
+    nf = trainer.fwd_floats()
+    f, iv = blob[:nf], blob[nf:]
+    transfers = [TransferRecord(round_index, me, peer, "fwd", f.nbytes, hex64(fnv1a64(f))),
+                 TransferRecord(round_index, me, peer, "inv", iv.nbytes, hex64(fnv1a64(iv)))]
+    comm.exchange(trainer, peer)
+    disc_hash = hex64(trainer.model().disc_hash())
+    loc, inc, adopted = trainer._decide()
+    rec = TrainerRoundRecord(round_index, step, me, peer, loc.combined, inc.combined, adopted, disc_hash)
+    return rr, rec, transfers
+
+
+def run_experiment_rank(cfg: RunConfig, dataset: Dataset, comm, device: int = 0) -> RunResult | None:
+    """One rank of a k = world-size LTFB run (one trainer per GPU). Returns
+    the merged RunResult on rank 0 (None elsewhere)."""
+    validate_run_config(cfg)
+    k = comm.world
+    if cfg.mode != "single" and cfg.trainers != k:
+        raise ConfigError("run_experiment_rank: trainers must equal the world size")
+    k = 1 if cfg.mode == "single" else k
+    rounds_enabled = cfg.mode == "ltfb" and k >= 2
+    split = split_dataset(dataset.total, k, cfg.validation_fraction, cfg.tournament_fraction, cfg.seed, k >= 2)
+    history = RunHistory(mode=cfg.mode.replace("_", "-"), n_trainers=k)
+    rcfg = RunConfig(**{**cfg.__dict__, "devices": (device,)})
+    base, history.pretrain = _base_model(rcfg, dataset, split[1])  # replicated, deterministic
+    t = _trainer_for(rcfg, dataset, base, split, comm.rank)
+    have_val = split[0].size > 0
+    if have_val:
+        t.set_validation(split[0])
+        t.history().evals.append(_eval_record(t, 0))
+    done, round_index, my_rounds, my_xfers, rounds = 0, 0, [], [], []
+    while done < cfg.step_budget:
+        chunk = min(cfg.interval, cfg.step_budget - done)
+        t.train_steps(chunk)
+        done += chunk
+        if have_val:
+            t.history().evals.append(_eval_record(t, done))
+        if rounds_enabled and chunk == cfg.interval:
+            round_index += 1
+            rr, rec, xf = distributed_round(t, comm, k, round_index, cfg.seed)
+            rounds.append(rr)
+            if rec is not None:
+                my_rounds.append(rec)
+            my_xfers += xf
+    t.flush_epoch_record()
+    final = t.evaluate_validation(cfg.w_f, cfg.w_i) if have_val else None
+    parts = comm.all_gather((t.history(), my_rounds, my_xfers, final))
+    # best-of-k on the shared validation slice (runner.hpp:380-398): every
+    # rank sees the same metrics, only the winner ships its model
+    best_rank, best = 0, float("inf")
+    if have_val:
+        for r, p in enumerate(parts):
+            if p[3].combined < best:
+                best, best_rank = p[3].combined, r
+    models = comm.all_gather(t.model().copy() if comm.rank == best_rank else None)
+    if comm.rank != 0:
+        return None
+    _merge(history, [p[0] for p in parts])
+    history.rounds = rounds
+    history.trainer_rounds = sorted([r for p in parts for r in p[1]], key=lambda r: (r.round, r.trainer))
+    # transfers in the reference's order: per pair (a <- b, then b <- a)
+    by = {(x.round, x.from_trainer, x.payload): x for p in parts for x in p[2]}
+    for rr in rounds:
+        for a, b in rr.pairs:
+            for to, frm in ((a, b), (b, a)):
+                history.transfers += [by[(rr.round, frm, "fwd")], by[(rr.round, frm, "inv")]]
+    res = RunResult(history, best_rank, parts[best_rank][3] if have_val else None, models[best_rank])
+    history.best_trainer, history.best_metric = res.best_trainer, res.best_metric
+    return res

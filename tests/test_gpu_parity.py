@@ -331,3 +331,35 @@ def test_autoencoder_frozen_and_bad_rows():
     model.autoencoder_frozen = True
     with pytest.raises(L.ContractError):
         L.AutoencoderPretrainer(model, ds.y)
+
+
+@pytest.mark.parametrize("pfx", ["tiny_k2_", "tiny_k3_", "desk_k2_"])
+def test_run_experiment_matches_reference(golden, pfx):
+    """runner.run_experiment end to end on the device -- AE pre-training,
+    per-trainer reinit, chunks, validation evals, rounds, best-of-k --
+    against the reference's run_experiment (tests/golden/tournament.npz).
+    Integer artefacts (split, pairings, decisions, best trainer) exactly;
+    losses and metrics within REL_LOSS (the device AE's wide-layer sums
+    differ from the reference's order at the ulp level)."""
+    g = golden("tournament")
+    gen_n, spf, spec_seed, sampling_seed, k, batch, interval, budget, ae_steps, seed, shards = (
+        int(v) for v in g[pfx + "cfg"])
+    dims = L.ModalityDims(*(int(v) for v in g[pfx + "dims"]))
+    arch = L.SurrogateArch.tiny() if pfx.startswith("tiny") else L.SurrogateArch()
+    ds = L.synthetic_dataset(dims, gen_n, sampling_seed=sampling_seed, spec_seed=spec_seed, samples_per_file=spf)
+    cfg = L.RunConfig(dims=dims, arch=arch, mode="ltfb", trainers=k, shards=shards, batch_size=batch,
+                      interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed)
+    res = L.run_experiment(cfg, ds)
+    h = res.history
+    assert rel([p[1] for p in h.pretrain], g[pfx + "pretrain_loss"]) < REL_LOSS
+    assert [s.trainer for s in h.steps] == list(g[pfx + "steps_trainer"])
+    assert [s.step for s in h.steps] == list(g[pfx + "steps_step"])
+    for key in ("d_loss", "g_total", "g_fwd", "g_adv", "g_cyc"):
+        assert rel([getattr(s, key) for s in h.steps], g[pfx + "steps_" + key]) < 10 * REL_LOSS, key
+    assert [r.pairs[0] if r.pairs else None for r in h.rounds] == \
+        [(int(a), int(b)) for a, b in zip(g[pfx + "round_pair_a"], g[pfx + "round_pair_b"])]
+    assert [int(r.kept_incoming) for r in h.trainer_rounds] == [int(v) for v in g[pfx + "tr_kept"]]
+    assert rel([r.local_metric for r in h.trainer_rounds], g[pfx + "tr_local"]) < 10 * REL_LOSS
+    assert [x.bytes for x in h.transfers] == [int(v) for v in g[pfx + "xf_bytes"]]
+    assert rel([e.combined for e in h.evals], g[pfx + "evals_combined"]) < 10 * REL_LOSS
+    assert res.best_trainer == int(g[pfx + "best_trainer"][0])

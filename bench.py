@@ -43,7 +43,7 @@ def parse():
     p.add_argument("--dims", default="paper", choices=["paper", "desk"])
     p.add_argument("--samples-per-trainer", type=int, default=8000)
     p.add_argument("--batch", type=int, default=128)
-    p.add_argument("--interval", type=int, default=10)
+    p.add_argument("--interval", type=int, default=100)  # RunConfig::interval (runner.hpp:64)
     p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--wide-kernel", type=int, default=0)
@@ -295,12 +295,16 @@ def main():
                 peer = b
             elif b == rank:
                 peer = a
-        tr.timer_start()
+        # the round is synchronous (the decision is read back), so it is
+        # timed on the host after draining the step kernels queued before
+        # it; the trainer's device timer keeps bracketing the whole region
+        tr.synchronize()
+        t0 = time.perf_counter()
         if peer is not None:
             tr.exchange(comm, peer)
             tr.decide_incoming()
-        ms = tr.timer_stop()
-        rounds_ms.append(ms)
+        tr.synchronize()
+        rounds_ms.append((time.perf_counter() - t0) * 1e3)
 
     def run_steps(n):
         done = 0

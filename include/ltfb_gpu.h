@@ -191,6 +191,8 @@ int ltfb_ae_batch_rows(uint64_t seed, uint64_t rows, uint64_t batch, uint64_t st
  * overlaps the previous step's kernels) and its record is read back D2H. */
 int ltfb_trainer_train_steps_host(ltfb_trainer* t, uint64_t n, const float* x, const float* y,
                                   ltfb_step_record* out, uint64_t* n_out);
+/* Blocks until every kernel / copy queued on the trainer's stream is done. */
+int ltfb_trainer_synchronize(ltfb_trainer* t);
 /* CUDA-event timer on the trainer's stream. */
 int ltfb_trainer_timer_start(ltfb_trainer* t);
 int ltfb_trainer_timer_stop(ltfb_trainer* t, double* ms);

@@ -590,6 +590,9 @@ class Trainer:
         self._drain_epochs()
         check(rc)
 
+    def synchronize(self):
+        check(lib.ltfb_trainer_synchronize(self._h))
+
     # -- measurement hooks (bench.py)
     def timer_start(self):
         check(lib.ltfb_trainer_timer_start(self._h))

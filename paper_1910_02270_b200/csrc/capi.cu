@@ -361,6 +361,10 @@ int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv) {
   return guarded([&] { T(t).adopt(fwd, inv); });
 }
 
+int ltfb_trainer_synchronize(ltfb_trainer* t) {
+  return guarded([&] { T(t).synchronize(); });
+}
+
 int ltfb_trainer_load_ae_source(ltfb_trainer* t, const float* y, uint64_t n) {
   return guarded([&] {
     if (!y) throw ltfb::ContractError("load_ae_source: null source");

@@ -363,3 +363,20 @@ def test_run_experiment_matches_reference(golden, pfx):
     assert [x.bytes for x in h.transfers] == [int(v) for v in g[pfx + "xf_bytes"]]
     assert rel([e.combined for e in h.evals], g[pfx + "evals_combined"]) < 10 * REL_LOSS
     assert res.best_trainer == int(g[pfx + "best_trainer"][0])
+
+
+def test_multi_gpu_run_matches_reference():
+    """tools/dist_run.py under torchrun on 2 GPUs: one trainer per GPU, the
+    NCCL device-to-device exchange, the reference's tiny_k2 run."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533",
+                        os.path.join(repo, "tools", "dist_run.py"), "--golden", "tiny_k2_"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -193,6 +193,9 @@ int ltfb_trainer_train_steps_host(ltfb_trainer* t, uint64_t n, const float* x, c
                                   ltfb_step_record* out, uint64_t* n_out);
 /* Blocks until every kernel / copy queued on the trainer's stream is done. */
 int ltfb_trainer_synchronize(ltfb_trainer* t);
+/* Captures the CUDA graphs of the step loop (runs of 2..32 steps) without
+ * executing them, so that no graph capture lands inside a timed region. */
+int ltfb_trainer_prepare_graphs(ltfb_trainer* t);
 /* CUDA-event timer on the trainer's stream. */
 int ltfb_trainer_timer_start(ltfb_trainer* t);
 int ltfb_trainer_timer_stop(ltfb_trainer* t, double* ms);

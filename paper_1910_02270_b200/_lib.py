@@ -112,7 +112,7 @@ EXPORTS = (
     "ltfb_trainer_broadcast", "ltfb_mix_seed", "ltfb_fnv1a64", "ltfb_pair_trainers",
     "ltfb_partition_dataset", "ltfb_split_dataset", "ltfb_epoch_permutation",
     "ltfb_incoming_wins", "ltfb_synth_generate", "ltfb_init_params", "ltfb_net_param_count",
-    "ltfb_trainer_synchronize", "ltfb_trainer_load_ae_source", "ltfb_trainer_ae_step", "ltfb_ae_batch_rows",
+    "ltfb_trainer_synchronize", "ltfb_trainer_prepare_graphs", "ltfb_trainer_load_ae_source", "ltfb_trainer_ae_step", "ltfb_ae_batch_rows",
 )
 
 
@@ -196,6 +196,7 @@ _sig("ltfb_synth_generate", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, C.
 _sig("ltfb_init_params", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_uint64, C.c_int, f32p, C.c_uint64)
 _sig("ltfb_net_param_count", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_int, C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_synchronize", C.c_int, P)
+_sig("ltfb_trainer_prepare_graphs", C.c_int, P)
 _sig("ltfb_trainer_load_ae_source", C.c_int, P, f32p, C.c_uint64)
 _sig("ltfb_trainer_ae_step", C.c_int, P, u32p, C.c_uint64, C.POINTER(C.c_double))
 _sig("ltfb_ae_batch_rows", C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, u32p)

@@ -593,6 +593,10 @@ class Trainer:
     def synchronize(self):
         check(lib.ltfb_trainer_synchronize(self._h))
 
+    def prepare_graphs(self):
+        """Capture the step graphs ahead of a timed region (no execution)."""
+        check(lib.ltfb_trainer_prepare_graphs(self._h))
+
     # -- measurement hooks (bench.py)
     def timer_start(self):
         check(lib.ltfb_trainer_timer_start(self._h))

@@ -361,6 +361,10 @@ int ltfb_trainer_adopt(ltfb_trainer* t, const float* fwd, const float* inv) {
   return guarded([&] { T(t).adopt(fwd, inv); });
 }
 
+int ltfb_trainer_prepare_graphs(ltfb_trainer* t) {
+  return guarded([&] { T(t).prepare_graphs(); });
+}
+
 int ltfb_trainer_synchronize(ltfb_trainer* t) {
   return guarded([&] { T(t).synchronize(); });
 }

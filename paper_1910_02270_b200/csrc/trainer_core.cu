@@ -638,7 +638,10 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
           if (owner_[slots[begin + r]] >= 0 && owner_[slots[begin + r]] != s) ++epoch_shuffled_;
     }
     // a run of steps inside this epoch goes out as one CUDA graph launch
-    const std::size_t run = std::min<std::size_t>(n - i, steps_per_epoch_ - step_in_epoch_);
+    // runs are powers of two (<= kMaxGraphRun) so a handful of cached
+    // graphs covers every position in every epoch
+    std::size_t run = std::min<std::size_t>({n - i, steps_per_epoch_ - step_in_epoch_, kMaxGraphRun});
+    while (run & (run - 1)) run &= run - 1;
     if (run >= 2 && spec_.n_shards == 1 && launch_graph(run)) {
       step_in_epoch_ += run;
       epoch_steps_ += run;
@@ -654,9 +657,15 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
   LTFB_CUDA(cudaGetLastError());
 }
 
-bool DeviceTrainer::launch_graph(std::size_t steps) {
-  if (!graphs_on_ || ktime_on_) return false;
-  prepare_params();  // weight re-layouts stay outside the graph
+void DeviceTrainer::prepare_graphs() {
+  DeviceGuard g(spec_.device);
+  if (!graphs_on_ || ktime_on_ || spec_.n_shards != 1) return;
+  prepare_params();
+  for (std::size_t s = 2; s <= kMaxGraphRun; s *= 2)
+    if (!graph_for(s)) return;
+}
+
+cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps) {
   if (std::memcmp(&graph_args_, &args_, sizeof args_) != 0) {  // pointers or layout changed
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     graphs_.clear();
@@ -668,7 +677,7 @@ bool DeviceTrainer::launch_graph(std::size_t steps) {
     cudaGraph_t graph = nullptr;
     if (cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       graphs_on_ = false;
-      return false;
+      return nullptr;
     }
     for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true, k == 0);  // replayable: row kernel first
     const cudaError_t e = cudaStreamEndCapture(stream_, &graph);
@@ -678,14 +687,22 @@ bool DeviceTrainer::launch_graph(std::size_t steps) {
       cudaGetLastError();
       graphs_on_ = false;  // capture unsupported here: plain launches from now on
       launches_ = l0;
-      return false;
+      return nullptr;
     }
     cudaGraphDestroy(graph);
     graph_launches_[steps] = launches_ - l0;
     launches_ = l0;
     it = graphs_.emplace(steps, exec).first;
   }
-  LTFB_CUDA(cudaGraphLaunch(it->second, stream_));
+  return it->second;
+}
+
+bool DeviceTrainer::launch_graph(std::size_t steps) {
+  if (!graphs_on_ || ktime_on_) return false;
+  prepare_params();  // weight re-layouts stay outside the graph
+  cudaGraphExec_t exec = graph_for(steps);
+  if (!exec) return false;
+  LTFB_CUDA(cudaGraphLaunch(exec, stream_));
   h_ready_ = next_h_on() && step_in_epoch_ + steps < steps_per_epoch_;
   launches_ += graph_launches_[steps];
   return true;

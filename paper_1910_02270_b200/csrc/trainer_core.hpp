@@ -178,6 +178,15 @@ class DeviceTrainer {
   /// Runs `steps` steps of the current epoch as one cached CUDA graph;
   /// false if graphs are off or capture is unsupported (caller launches).
   bool launch_graph(std::size_t steps);
+  cudaGraphExec_t graph_for(std::size_t steps);
+  static constexpr std::size_t kMaxGraphRun = 32;
+
+ public:
+  /// Captures (without running) the step graphs of every run length the
+  /// step loop uses, so no capture lands inside a timed region.
+  void prepare_graphs();
+
+ private:
 
   TrainerSpec spec_;
   ltfb::nn::MlpSpec specs_[5];

@@ -59,54 +59,79 @@ __global__ void __launch_bounds__(128) k_eval_small(EvalArgs a) {
   }
 }
 
-template <int RB, int TN>
+// Forward-MAE partials, register-tiled: a CTA owns column tiles of 64
+// decoder outputs (Wd tile + bias loaded once) and sweeps every 64-row block
+// of the slice for both candidates; each thread computes a 4 x 4 block of
+// predictions (k-ordered fmaf chains over D) from float4 shared-memory
+// loads (h stored k-major, Wd row-major) and accumulates |o - y| in double.
+constexpr int kEvT = 64;  // rows / columns per tile
 __global__ void __launch_bounds__(256) k_eval_wide(EvalArgs a) {
   extern __shared__ float4 smem4[];
   float* sm = reinterpret_cast<float*>(smem4);
   __shared__ double red[256];
   const ModelArgs& m = a.m;
   const int D = m.D, out = m.out, op = m.out_pad;
-  float* yt = sm;              // RB x TN
-  float* wd = yt + RB * TN;    // D x TN
-  float* hb = wd + D * TN;     // RB x D
-  float* bd = hb + RB * D;     // TN
+  float* wd = sm;                // [D][64]      Wd[:, c0 .. c0 + 64)
+  float* hT = wd + D * kEvT;     // [D][64]      h of 64 rows, k-major
+  float* yt = hT + D * kEvT;     // [64][64 + 4] y block
+  float* bd = yt + kEvT * (kEvT + 4);
   const float* Wd = a.dec + m.dec_wide_w;
   const float* Bd = a.dec + m.dec_wide_b;
-  const int ncol = (out + TN - 1) / TN;
-  const int nrb = (a.rows + RB - 1) / RB;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int ncol = (out + kEvT - 1) / kEvT;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
   double acc_c[2] = {0.0, 0.0};
-  for (int t = blockIdx.x; t < ncol * nrb; t += gridDim.x) {
-    const int rb = (t / ncol) * RB, c0 = (t % ncol) * TN;
-    const int nr = min(RB, a.rows - rb);
+  for (int t = blockIdx.x; t < ncol; t += gridDim.x) {
+    const int c0 = t * kEvT;
     __syncthreads();
-    for (int i = tid; i < RB * TN; i += nth) {
-      const int r = i / TN, c = i - r * TN;
-      yt[i] = (r < nr && c0 + c < out) ? a.y[(long long)(rb + r) * op + c0 + c] : 0.0f;
+    for (int i = tid; i < D * kEvT; i += 256) {
+      const int j = i >> 6, c = i & 63;
+      wd[i] = c0 + c < out ? Wd[(long long)j * out + c0 + c] : 0.0f;
     }
-    for (int i = tid; i < D * TN; i += nth) {
-      const int j = i / TN, c = i - j * TN;
-      wd[i] = (c0 + c < out) ? Wd[(long long)j * out + c0 + c] : 0.0f;
-    }
-    for (int c = tid; c < TN; c += nth) bd[c] = (c0 + c < out) ? Bd[c0 + c] : 0.0f;
-    for (int cand = 0; cand < a.nc; ++cand) {
+    if (tid < kEvT) bd[tid] = c0 + tid < out ? Bd[c0 + tid] : 0.0f;
+    for (int rb = 0; rb < a.rows; rb += kEvT) {
+      const int nr = min(kEvT, a.rows - rb);
       __syncthreads();
-      for (int i = tid; i < RB * D; i += nth) {
-        const int r = i / D;
-        hb[i] = r < nr ? a.h[((long long)cand * a.rows + rb + r) * D + (i - r * D)] : 0.0f;
+      for (int i = tid; i < kEvT * kEvT; i += 256) {
+        const int r = i >> 6, c = i & 63;
+        yt[r * (kEvT + 4) + c] = (r < nr && c0 + c < out) ? a.y[(long long)(rb + r) * op + c0 + c] : 0.0f;
       }
-      __syncthreads();
-      double s = 0.0;
-      for (int i = tid; i < RB * TN; i += nth) {
-        const int r = i / TN, c = i - r * TN;
-        if (r < nr && c0 + c < out) {
-          float acc = 0.0f;
-          for (int j = 0; j < D; ++j) acc = fmaf(hb[r * D + j], wd[j * TN + c], acc);
-          const float o = acc + bd[c];
-          s += fabs((double)o - (double)yt[i]);
+      for (int cand = 0; cand < a.nc; ++cand) {
+        __syncthreads();
+        for (int i = tid; i < kEvT * D; i += 256) {
+          const int r = i / D, k = i - r * D;
+          hT[k * kEvT + r] = r < nr ? a.h[((long long)cand * a.rows + rb + r) * D + k] : 0.0f;
         }
+        __syncthreads();
+        float o[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[i][j] = 0.0f;
+#pragma unroll 4
+        for (int k = 0; k < D; ++k) {
+          const float4 hv = *reinterpret_cast<const float4*>(hT + k * kEvT + 4 * ty);
+          const float4 wv = *reinterpret_cast<const float4*>(wd + k * kEvT + 4 * tx);
+          const float hr[4] = {hv.x, hv.y, hv.z, hv.w}, wc[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[i][j] = fmaf(hr[i], wc[j], o[i][j]);
+        }
+        double sacc = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = 4 * ty + i;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int c = 4 * tx + j;
+            if (r < nr && c0 + c < out) {
+              const float pred = o[i][j] + bd[c];  // mlp.hpp:209-213
+              sacc += fabs((double)pred - (double)yt[r * (kEvT + 4) + c]);
+            }
+          }
+        }
+        acc_c[cand] += sacc;
       }
-      acc_c[cand] += s;
     }
   }
   for (int cand = 0; cand < a.nc; ++cand) {
@@ -115,19 +140,23 @@ __global__ void __launch_bounds__(256) k_eval_wide(EvalArgs a) {
   }
 }
 
-template __global__ void k_eval_wide<32, 32>(EvalArgs);
-
 __global__ void __launch_bounds__(256) k_eval_finalize(EvalArgs a) {
   __shared__ int s_adopt;
+  __shared__ double red[256];
   const ModelArgs& m = a.m;
+  double fsum[2] = {0, 0}, isum[2] = {0, 0};
+  for (int c = 0; c < a.nc; ++c) {  // fixed-order strided sums + tree: deterministic
+    double f = 0.0, inv = 0.0;
+    for (int s = threadIdx.x; s < a.S; s += blockDim.x) f += a.part[(long long)s * a.nc + c];
+    for (int r = threadIdx.x; r < a.rows; r += blockDim.x) inv += a.inv_row[(long long)c * a.rows + r];
+    fsum[c] = block_sum_det(f, red);
+    isum[c] = block_sum_det(inv, red);
+  }
   if (threadIdx.x == 0) {
     double comb[2] = {0, 0};
     for (int c = 0; c < a.nc; ++c) {
-      double f = 0.0, inv = 0.0;
-      for (int s = 0; s < a.S; ++s) f += a.part[(long long)s * a.nc + c];
-      for (int r = 0; r < a.rows; ++r) inv += a.inv_row[(long long)c * a.rows + r];
-      f /= (double)a.rows * (double)m.out;
-      inv /= (double)a.rows * (double)m.in;
+      const double f = fsum[c] / ((double)a.rows * (double)m.out);
+      const double inv = isum[c] / ((double)a.rows * (double)m.in);
       comb[c] = a.w_f * f + a.w_i * inv;
       a.out[c * 3 + 0] = f;
       a.out[c * 3 + 1] = inv;
@@ -161,18 +190,17 @@ __global__ void __launch_bounds__(256) k_eval_finalize(EvalArgs a) {
 namespace ltfb_dev {
 
 std::size_t eval_wide_smem(const ModelArgs& m) {
-  constexpr int RB = 32, TN = 32;
-  return sizeof(float) * (std::size_t)(RB * TN + m.D * TN + RB * m.D + TN);
+  return sizeof(float) * (std::size_t)(2 * m.D * kEvT + kEvT * (kEvT + 4) + kEvT);
 }
 
 void launch_eval(const EvalArgs& a, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_eval_wide<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   k_eval_small<<<dim3((a.rows + kEvalRows - 1) / kEvalRows, a.nc), 128, 0, s>>>(a);
-  k_eval_wide<32, 32><<<a.S, 256, eval_wide_smem(a.m), s>>>(a);
+  k_eval_wide<<<a.S, 256, eval_wide_smem(a.m), s>>>(a);
   k_eval_finalize<<<1, 256, 0, s>>>(a);
 }
 

@@ -338,14 +338,14 @@ __device__ __noinline__ void transpose_net(const NetS& n) {
 
 /// Owner reduction of [lo, hi) over the kC partials at smem offset pg, in
 /// rank order, into gr; returns this CTA's "all finite" (block-uniform).
-__device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr) {
+__device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr, int base = 0) {
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   int ok = 1;
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
     float v[kC];
 #pragma unroll
-    for (int r = 0; r < kC; ++r) v[r] = cl.map_shared_rank(s + pg, r)[e];
+    for (int r = 0; r < kC; ++r) v[r] = cl.map_shared_rank(s + pg, base + r)[e];
     float acc = 0.0f;
 #pragma unroll
     for (int r = 0; r < kC; ++r) acc += v[r];
@@ -509,8 +509,9 @@ __shared__ int g_nst;
 __shared__ double g_pre[7];
 
 struct Rows {
-  int rank, rows, r0, nr;
+  int rank, rows, r0, nr;  // rank within the half (row block / owner slice index)
   int lo[3], hi[3];
+  int split;               // 1: two halves (16-CTA cluster), the cycle path in the second
 };
 
 /// First element of rank r's owner slice of a count-element blob: the even
@@ -729,24 +730,27 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   ST();
   cluster_sync();  // S4: fwd / inv partials + adv / cyc sums
   ST();
+  // split mode: the inv partials, their reduction and the cycle losses live
+  // in the cyc half (ranks kC .. 2kC-1), which also applies Adam(inv)
+  const int cb = R.split ? kC : 0;
   const int fok = reduce_owned(Y.pg[1], R.lo[1], R.hi[1], Y.gr[1]);
-  const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
+  const int iok = R.split ? 1 : reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
   ST();
   if (tid == 0) {
     s_ok[1] = fok;
-    s_ok[2] = iok;
+    if (!R.split) s_ok[2] = iok;
   }
   double adv_sum = 0.0, cyc_sum = 0.0;
   for (int r = 0; r < kC; ++r) {
     adv_sum += cl.map_shared_rank(s_loss, r)[1];
-    cyc_sum += cl.map_shared_rank(s_loss, r)[2];
+    cyc_sum += cl.map_shared_rank(s_loss, cb + r)[2];
   }
   cluster_sync();  // S5: flags
   ST();
   int all_f = 1, all_i = 1;
   for (int r = 0; r < kC; ++r) {
     all_f &= cl.map_shared_rank(s_ok, r)[1];
-    all_i &= cl.map_shared_rank(s_ok, r)[2];
+    all_i &= cl.map_shared_rank(s_ok, cb + r)[2];
   }
   const int rows = R.rows;
   const long long n_fwd = (long long)rows * m.out;
@@ -768,8 +772,9 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
     out[4] = 1.0;
     ST();
     if (all_i) {
-      adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2],
-                 Y.vo[2], 0);
+      if (!R.split)
+        adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2],
+                   Y.vo[2], 0);
       out[5] = 1.0;
     }
   }
@@ -821,7 +826,7 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
   const int nxt = sie + 1;
   if ((long long)nxt * a.B >= (long long)a.n_part) return;
   const int rows = min(a.B, a.n_part - nxt * a.B);
-  const int rank = (int)cg::this_cluster().block_rank();
+  const int rank = (int)cg::this_cluster().block_rank() % kC;
   const int per = (rows + kC - 1) / kC;
   const int r0 = min(rank * per, rows), nr = max(0, min(per, rows - r0));
   (void)epoch;
@@ -846,6 +851,79 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
   for (int i = tid; i < nr * w; i += kThreads) a.h[(long long)r0 * w + i] = s[fin + i];
 }
 
+/// The second half of a 16-CTA cluster (ranks kC .. 2kC-1): the work of the
+/// step that does not depend on the D-step -- fwd forward (its own copy),
+/// the dec-head backward (dL/dlatent of the forward-MAE term) and the whole
+/// cycle path (inv forward, cycle MAE, inv backward, inv weight gradients)
+/// -- runs concurrently with the first half's D-step. CTA kC + c owns the
+/// same rows as CTA c, which pulls gl_dec / gl_inv over DSMEM after S1. The
+/// half mirrors every cluster barrier of the first half (S1 .. S6), reduces
+/// the inv partials over its own ranks, and applies Adam(inv) on its owner
+/// slices once the step's decision (computed identically from the shared
+/// flags and loss sums) says so.
+__device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const Rows& R, double* s_loss, int* s_ok,
+                                      double* s_wl) {
+  cg::cluster_group cl = cg::this_cluster();
+  const ModelArgs& m = a.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const NetS& F = Y.net[kF];
+  const NetS& I = Y.net[kI];
+  const NetS& DH = Y.net[kDH];
+  const int latent = Y.stacked + kR * m.lat;
+  const int nr = R.nr, rows = R.rows;
+  wnet_fwd(F, Y.xs, 2, latent);
+  if (DH.L > 0) {
+    wnet_fwd(DH, latent, 2, -1);
+    dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
+    wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
+  }
+  wnet_fwd(I, latent, 2, -1);
+  {
+    const double part = cyc_warp(I.a[I.L - 1], Y.xs, I.dz[I.L - 1], m.in, nr, rows, m.lambda_cyc);
+    if (lane == 0) s_wl[warp] = part;
+    __syncwarp();
+  }
+  wnet_bwd(I, 2, Y.gl_inv, -1, -1);
+  __syncthreads();
+  pg_net(I, latent, kR, Y.pg[2]);
+  if (tid == 0) s_loss[2] = sum_warps(s_wl);
+  __syncthreads();
+  cluster_arrive();  // S1
+  cluster_wait();
+  const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2], kC);
+  if (tid == 0) s_ok[2] = iok;
+  cluster_sync();  // S2 (d_update's flags)
+  double d_sum = 0.0;
+  int all_ok = 1;
+  for (int r = 0; r < kC; ++r) {
+    d_sum += cl.map_shared_rank(s_loss, r)[0];
+    all_ok &= cl.map_shared_rank(s_ok, r)[0];
+  }
+  const double d_loss = ((double)rows * (d_sum / (2.0 * (double)rows))) / (double)rows;
+  const bool d_ok = isfinite(d_loss) && all_ok;
+  cluster_sync();  // S3
+  if (d_ok) {
+    cluster_sync();  // S4
+    cluster_sync();  // S5
+    double adv_sum = 0.0, cyc_sum = 0.0;
+    int all_f = 1, all_i = 1;
+    for (int r = 0; r < kC; ++r) {
+      adv_sum += cl.map_shared_rank(s_loss, r)[1];
+      cyc_sum += cl.map_shared_rank(s_loss, kC + r)[2];
+      all_f &= cl.map_shared_rank(s_ok, r)[1];
+      all_i &= cl.map_shared_rank(s_ok, kC + r)[2];
+    }
+    const double adv = adv_sum / (double)rows;
+    const double cyc = cyc_sum / (double)((long long)rows * m.in);
+    const double fm = g_pre[6] / (double)((long long)rows * m.out);
+    const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
+    const double total = ((double)rows * total_raw) / (double)rows;
+    if (isfinite(total) && all_f && all_i)  // trainer.hpp:256-264: inv after fwd
+      adam_owned(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], 0);
+  }
+  cluster_sync();  // S6
+}
+
 __device__ __noinline__ void print_phases(const long long* ph, int n) {
   printf("post phases (cycles):");
   for (int i = 1; i < n; ++i) printf(" %lld", ph[i] - ph[i - 1]);
@@ -854,7 +932,7 @@ __device__ __noinline__ void print_phases(const long long* ph, int n) {
   printf("\n");
 }
 
-__global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     k_post_small(const __grid_constant__ StepArgs ap, const __grid_constant__ Layout Lp) {
   __shared__ Layout Y;
   // The argument block lives in shared memory for the whole step: the
@@ -888,7 +966,10 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   Rows R;
-  R.rank = (int)cg::this_cluster().block_rank();
+  const int crank = (int)cg::this_cluster().block_rank();
+  R.split = cg::this_cluster().num_blocks() == 2 * kC ? 1 : 0;
+  const int half = crank / kC;
+  R.rank = crank % kC;
   const int sie = (int)a.ctr->step_in_epoch;
   const unsigned epoch = a.ctr->epoch;
   R.rows = min(a.B, a.n_part - sie * a.B);
@@ -910,6 +991,10 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   __syncthreads();
   prologue(a, Y, R, &s_bar);
   PH();
+  if (half == 1) {
+    cyc_half(a, Y, R, s_loss, s_ok, s_wl);
+    return;
+  }
   const NetS& F = Y.net[kF];
   const NetS& I = Y.net[kI];
   const NetS& C = Y.net[kCd];
@@ -921,7 +1006,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   // ---- D-step forward + input-gradient chain, warp-local (rows w + 8 i) ----
   if (ET.L > 0) wnet_fwd(ET, Y.e1, 2, Y.stacked);  // real latents -> stacked[0, R)
   wnet_fwd(F, Y.xs, 2, latent);                    // fake latents -> stacked[R, 2R)
-  if (DH.L > 0) wnet_fwd(DH, latent, 2, -1);       // dec-head tape
+  if (DH.L > 0 && !R.split) wnet_fwd(DH, latent, 2, -1);  // dec-head tape
   wnet_fwd(C, Y.stacked, 4, -1);                   // disc on [real; fake]: rows w, w+8 | w+16, w+24
   {
     const double lv = bce_warp(C.a[C.L - 1], C.dz[C.L - 1], 4, kR, nr, 2.0 * (double)rows, 1.0f);
@@ -938,22 +1023,36 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_arrive();  // S1: disc partials + loss published
 
   // ---- independent of the D-step: dec path, whole cycle path ----
-  if (DH.L > 0) {
+  // (split mode: computed concurrently by the cyc half, see cyc_half)
+  if (!R.split && DH.L > 0) {
     dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
     wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
   }
-  wnet_fwd(I, latent, 2, -1);
-  {
-    const double part = cyc_warp(I.a[I.L - 1], Y.xs, I.dz[I.L - 1], m.in, nr, rows, m.lambda_cyc);
-    if (lane == 0) s_wl[warp] = part;
-    __syncwarp();
+  if (!R.split) {
+    wnet_fwd(I, latent, 2, -1);
+    {
+      const double part = cyc_warp(I.a[I.L - 1], Y.xs, I.dz[I.L - 1], m.in, nr, rows, m.lambda_cyc);
+      if (lane == 0) s_wl[warp] = part;
+      __syncwarp();
+    }
+    wnet_bwd(I, 2, Y.gl_inv, -1, -1);
+    __syncthreads();
+    pg_net(I, latent, kR, Y.pg[2]);
+    if (tid == 0) s_loss[2] = sum_warps(s_wl);
   }
-  wnet_bwd(I, 2, Y.gl_inv, -1, -1);
-  __syncthreads();
-  pg_net(I, latent, kR, Y.pg[2]);
-  if (tid == 0) s_loss[2] = sum_warps(s_wl);
   PH();
   cluster_wait();  // S1
+  if (R.split) {  // dL/dlatent of the dec and cycle paths from the partner CTA of the cyc half
+    cg::cluster_group cl = cg::this_cluster();
+    float* s = S();
+    const float* pdec = cl.map_shared_rank(s + Y.gl_dec, kC + R.rank);
+    const float* pinv = cl.map_shared_rank(s + Y.gl_inv, kC + R.rank);
+    for (int i = tid; i < kR * m.lat; i += kThreads) {
+      s[Y.gl_dec + i] = pdec[i];
+      s[Y.gl_inv + i] = pinv[i];
+    }
+    __syncthreads();
+  }
   PH();
 
   double d_loss = 0.0;
@@ -987,7 +1086,7 @@ __global__ void __cluster_dims__(kC, 1, 1) __launch_bounds__(kThreads, 1)
   PH();
   if (a.post_next_h) next_h(a, Y, sie, epoch);
   PH();
-  if (R.rank == 0 && tid == 0) {
+  if (R.rank == 0 && tid == 0) {  // first half only (the cyc half returned above)
     finish(a, d_ok, d_loss, s_g);
     if (a.phase_prof) print_phases(s_ph, n_ph < 16 ? n_ph : 16);
   }
@@ -1060,7 +1159,45 @@ void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {
     cache_m = a.m;
     have = true;
   }
-  ps::k_post_small<<<ps::kC, ps::kThreads, (std::size_t)cache.total * sizeof(float), s>>>(a, cache);
+  // one 16-CTA cluster (non-portable size) when the GPU can place it: the
+  // cycle path runs in the second half concurrently with the D-step; else
+  // one 8-CTA cluster running both in sequence
+  static int split = -1;
+  const std::size_t smem = (std::size_t)cache.total * sizeof(float);
+  if (split < 0) {
+    split = 0;
+    if (!std::getenv("LTFB_POST_NO_SPLIT") &&
+        cudaFuncSetAttribute(ps::k_post_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(2 * ps::kC);
+      q.blockDim = dim3(ps::kThreads);
+      q.dynamicSmemBytes = kSmemCap;
+      cudaLaunchAttribute qa;
+      qa.id = cudaLaunchAttributeClusterDimension;
+      qa.val.clusterDim.x = 2 * ps::kC;
+      qa.val.clusterDim.y = 1;
+      qa.val.clusterDim.z = 1;
+      q.attrs = &qa;
+      q.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, ps::k_post_small, &q) == cudaSuccess && nclusters >= 1) split = 1;
+    }
+    cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(split ? 2 * ps::kC : ps::kC);
+  cfg.blockDim = dim3(ps::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = cfg.gridDim.x;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, ps::k_post_small, a, cache);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("post kernel launch: ") + cudaGetErrorString(e));
 }
 
 }  // namespace ltfb_dev

@@ -527,7 +527,27 @@ void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStr
   // cooperative: the in-kernel grid barrier needs every CTA resident
   void* args[] = {(void*)&tp, (void*)&a, (void*)&p.bias_pad};
   const void* fn = p.precise ? (const void*)k_wide_tc<true> : (const void*)k_wide_tc<false>;
-  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(a.S), dim3(wt::kThreads), args, wt::kSmem, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.S);
+  cfg.blockDim = dim3(wt::kThreads);
+  cfg.dynamicSmemBytes = wt::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  int nat = 1;
+  if (p.l2_hit > 0.0f) {  // frozen weights persist in L2 across steps
+    at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[1].val.accessPolicyWindow.base_ptr = p.l2_base;
+    at[1].val.accessPolicyWindow.num_bytes = p.l2_bytes;
+    at[1].val.accessPolicyWindow.hitRatio = p.l2_hit;
+    at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nat = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = nat;
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) throw std::runtime_error(std::string("wide pass cooperative launch: ") + cudaGetErrorString(e));
 }
 

@@ -28,6 +28,11 @@ struct WideTcParamsHost {
   float* wet = nullptr;
   float* wd = nullptr;
   float* wdt = nullptr;
+  // L2 persistence window over the frozen weight copies (one allocation):
+  // the weights are re-read every step, y streams through once
+  void* l2_base = nullptr;
+  std::size_t l2_bytes = 0;
+  float l2_hit = 0.0f;  // 0: no window
 };
 /// Builds the TMA descriptors (yb is [yb_rows x out_pad]).
 void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, int yb_rows);

@@ -185,13 +185,29 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
 
   if (wide_kind_ >= 2) {
     const std::size_t nw = 64 * static_cast<std::size_t>(ma.out_pad);
-    for (auto* b : {&wet_, &wd_, &wdt_}) b->alloc(nw);
-    bias_pad_.alloc(ma.out_pad);
+    // one allocation (WeT | Wd | WdT | bias) so one L2 persistence window covers it
+    wide_w_.alloc(3 * nw + static_cast<std::size_t>(ma.out_pad));
     wtp_.precise = wide_kind_ == 2;
-    wtp_.bias_pad = bias_pad_.p;
-    wtp_.wet = wet_.p;
-    wtp_.wd = wd_.p;
-    wtp_.wdt = wdt_.p;
+    wtp_.wet = wide_w_.p;
+    wtp_.wd = wide_w_.p + nw;
+    wtp_.wdt = wide_w_.p + 2 * nw;
+    wtp_.bias_pad = wide_w_.p + 3 * nw;
+    if (!std::getenv("LTFB_NO_L2_PERSIST")) {
+      int max_persist = 0, max_window = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, spec_.device);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, spec_.device);
+      const std::size_t bytes = std::min<std::size_t>(wide_w_.bytes(), static_cast<std::size_t>(max_window));
+      if (max_persist > 0 && bytes > 0) {
+        std::size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        const std::size_t want = std::min<std::size_t>(static_cast<std::size_t>(max_persist), std::max(cur, bytes));
+        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaGetLastError();
+        wtp_.l2_base = wide_w_.p;
+        wtp_.l2_bytes = bytes;
+        wtp_.l2_hit = static_cast<float>(std::min(1.0, static_cast<double>(want) / static_cast<double>(bytes)));
+      }
+    }
     ltfb_dev::encode_wide_maps(wtp_, a, yb_.p, static_cast<int>(yb_rows));
   }
   // post kernel: compile-time-shaped instance when the model matches one,

@@ -212,7 +212,7 @@ class DeviceTrainer {
   DevBuf<unsigned> perm_[2];
   DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
   // tcgen05 wide pass: K-major fp32 copies of the frozen wide-layer weights + bias
-  DevBuf<float> wet_, wd_, wdt_, bias_pad_;
+  DevBuf<float> wide_w_;  // WeT | Wd | WdT | bias (one range for the L2 persistence window)
   ltfb_dev::WideTcParamsHost wtp_{};
   bool wide_dirty_ = false;
   bool small_T_dirty_ = true;  // StepArgs::pT images need a rebuild

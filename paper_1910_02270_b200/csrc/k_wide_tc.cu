@@ -47,9 +47,11 @@ constexpr int kRows = 128;                 // MMA M (minibatch rows)
 constexpr int kW = 64;                     // E1 == D == 64
 constexpr uint32_t kY = 16384;             // [128 x 32] f32
 constexpr uint32_t kWt = 8192;             // [64 x 32] f32
-constexpr uint32_t kStage = kY + 6 * kWt;  // y (raw), WeT hi/lo, Wd hi/lo, WdT hi/lo
-constexpr int kStages = 3;
-constexpr uint32_t kSmem = kStages * kStage + 1024;
+constexpr uint32_t kStage = 6 * kWt;  // WeT hi/lo, Wd hi/lo, WdT hi/lo
+constexpr int kStages = 3;            // weight stages == TMEM y slots (freed by MMA3)
+constexpr int kYStages = 4;           // y landing slots (freed by the split): the row
+                                      // gather runs one tile further ahead
+constexpr uint32_t kSmem = kYStages * kY + kStages * kStage + 1024;
 constexpr int kThreads = 320;
 // TMEM columns
 constexpr uint32_t kPenc = 0, kPdec = 64, kO0 = 128, kHhi = 192, kHlo = 256;
@@ -91,6 +93,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   // array itself (not an integer round trip) keeps every access an LDS/STS
   unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kStages], split_done[kStages], sready[kStages], empty[kStages];
+  __shared__ uint64_t yfull[kYStages], yempty[kYStages];
   __shared__ uint64_t ofull[2], oempty[2], h_ready, done;
   __shared__ uint32_t tmem_base;
   __shared__ double red[128];
@@ -106,14 +109,14 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   const int ntiles = (out + kTileN - 1) / kTileN;
   const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-  auto stage_ptr = [&](int s) { return sm + s * kStage; };
-  auto Yraw = [&](int s) { return stage_ptr(s); };                      // y tile [128 x 32] SW128 (gather4)
-  auto WeH = [&](int s) { return stage_ptr(s) + kY; };                  // WeT [64 j x 32 c] SW128
-  auto WeL = [&](int s) { return stage_ptr(s) + kY + kWt; };
-  auto WdH = [&](int s) { return stage_ptr(s) + kY + 2 * kWt; };        // Wd  [64 j x 32 c] SW128
-  auto WdL = [&](int s) { return stage_ptr(s) + kY + 3 * kWt; };
-  auto WtH = [&](int s) { return stage_ptr(s) + kY + 4 * kWt; };        // WdT [32 c x 64 j] as 2 K-blocks
-  auto WtL = [&](int s) { return stage_ptr(s) + kY + 5 * kWt; };
+  auto stage_ptr = [&](int s) { return sm + kYStages * kY + s * kStage; };
+  auto Yraw = [&](int sy) { return sm + sy * kY; };                     // y tile [128 x 32] SW128 (gather4)
+  auto WeH = [&](int s) { return stage_ptr(s); };                       // WeT [64 j x 32 c] SW128
+  auto WeL = [&](int s) { return stage_ptr(s) + kWt; };
+  auto WdH = [&](int s) { return stage_ptr(s) + 2 * kWt; };             // Wd  [64 j x 32 c] SW128
+  auto WdL = [&](int s) { return stage_ptr(s) + 3 * kWt; };
+  auto WtH = [&](int s) { return stage_ptr(s) + 4 * kWt; };             // WdT [32 c x 64 j] as 2 K-blocks
+  auto WtL = [&](int s) { return stage_ptr(s) + 5 * kWt; };
   auto tYh = [&](int s) { return (uint32_t)(kYbase + 64 * s); };        // TMEM y hi   [128 x 32]
   auto tYl = [&](int s) { return (uint32_t)(kYbase + 64 * s + 32); };   // TMEM y lo, then S
 
@@ -123,6 +126,10 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       tc::mbar_init(&split_done[s], 128);
       tc::mbar_init(&sready[s], 128);
       tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kYStages; ++s) {
+      tc::mbar_init(&yfull[s], 1);
+      tc::mbar_init(&yempty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&ofull[b], 1);
@@ -160,22 +167,48 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         rw[u] = (int)perm[rr < rows ? rr : 0];
       }
     }
-    const uint32_t bytes = kY + 3 * kWt;  // fp32 tiles: y, WeT, Wd, WdT
-    for (int i = 0; i < my_tiles; ++i) {
-      const int s = i % kStages;
-      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-      const int c0 = ((int)blockIdx.x + i * (int)gridDim.x) * kTileN;
-      if (lane == 0) {
-        if (i >= kStages) tc::mbar_wait(&empty[s], ph ^ 1u);
-        LTFB_EV(i, 0);
-        tc::mbar_expect_tx(&full[s], bytes);
-        tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
-        tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
-        tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
-        tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
+    // two independent rings: y tiles (random store rows, the long-latency
+    // loads) whenever a y slot is free, weight tiles whenever a weight stage
+    // is free; neither waits for the other
+    int iy = 0, iw = 0;
+    while (iy < my_tiles || iw < my_tiles) {
+      bool did = false;
+      if (iw < my_tiles) {
+        const int s = iw % kStages;
+        const uint32_t ph = (uint32_t)(iw / kStages) & 1u;
+        int ready = 1;
+        if (lane == 0) ready = iw < kStages || tc::mbar_test(&empty[s], ph ^ 1u);
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready) {
+          const int c0 = ((int)blockIdx.x + iw * (int)gridDim.x) * kTileN;
+          if (lane == 0) {
+            LTFB_EV(iw, 0);
+            tc::mbar_expect_tx(&full[s], 3 * kWt);
+            tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
+            tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
+            tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
+            tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
+          }
+          ++iw;
+          did = true;
+        }
       }
-      __syncwarp();
-      tc::tma_gather4(Yraw(s) + 512 * lane, &tp.tm_y, &full[s], c0, rw[0], rw[1], rw[2], rw[3]);
+      if (iy < my_tiles) {
+        const int sy = iy % kYStages;
+        const uint32_t ph = (uint32_t)(iy / kYStages) & 1u;
+        int ready = 1;
+        if (lane == 0) ready = iy < kYStages || tc::mbar_test(&yempty[sy], ph ^ 1u);
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready) {
+          const int c0 = ((int)blockIdx.x + iy * (int)gridDim.x) * kTileN;
+          if (lane == 0) tc::mbar_expect_tx(&yfull[sy], kY);
+          __syncwarp();
+          tc::tma_gather4(Yraw(sy) + 512 * lane, &tp.tm_y, &yfull[sy], c0, rw[0], rw[1], rw[2], rw[3]);
+          ++iy;
+          did = true;
+        }
+      }
+      if (!did) __nanosleep(20);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer --
@@ -390,10 +423,12 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     for (int i = 0; i < my_tiles; ++i) {
       const int s = i % kStages;
       const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-      tc::mbar_wait(&full[s], ph);
+      const int sy = i % kYStages;
+      tc::mbar_wait(&yfull[sy], (uint32_t)(i / kYStages) & 1u);
+      tc::mbar_wait(&full[s], ph);  // weights landed: stage s (and TMEM y slot s) is this tile's
       if (t == 0) LTFB_EV(i, 1);
       {
-        const unsigned char* yrow = Yraw(s) + r * 128;
+        const unsigned char* yrow = Yraw(sy) + r * 128;
         float v[32], vl[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -408,6 +443,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         }
         tc::tmem_st32(T + lane_addr + tYh(s), v);
         if (kPrecise) tc::tmem_st32(T + lane_addr + tYl(s), vl);
+        tc::mbar_arrive(&yempty[sy]);  // the row is in registers / TMEM: the y slot can refill
       }
       if (kPrecise) {
         split(WeH(s), WeL(s), kWt / 16);

@@ -71,7 +71,28 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr[-4000:])
+    build_facade_test()
     return LIB
+
+
+FACADE_SRC = os.path.join(REPO, "tests", "cpp", "facade_test.cpp")
+FACADE_BIN = os.path.join(OUT, "facade_test")
+
+
+def build_facade_test() -> str | None:
+    """The C++ façade (include/ltfb_b200/trainer.hpp) test program, linked
+    against the in-tree library (g++; runs on the GPU box)."""
+    if not os.path.exists(FACADE_SRC):
+        return None
+    deps = [FACADE_SRC, LIB] + _headers()
+    if os.path.exists(FACADE_BIN) and os.path.getmtime(FACADE_BIN) >= max(os.path.getmtime(d) for d in deps):
+        return FACADE_BIN
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(REPO, "include"), FACADE_SRC, "-L" + OUT, "-lltfb_gpu",
+           "-Wl,-rpath,$ORIGIN", "-o", FACADE_BIN]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("g++ failed for the C++ facade test:\n" + r.stderr[-4000:])
+    return FACADE_BIN
 
 
 if __name__ == "__main__":

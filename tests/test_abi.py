@@ -47,3 +47,16 @@ def test_error_mapping_without_gpu():
         L.partition_dataset([1, 2], 5, 0)
     with pytest.raises(L.ConfigError):
         L.SurrogateArch(hidden_act="swish").c()
+
+
+def test_cpp_facade_compiles_and_links(tmp_path):
+    """include/ltfb_b200/trainer.hpp (the C++ drop-in façade) compiles with
+    the reference's C++20 toolchain and links against the library."""
+    import os
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = os.path.join(repo, "tests", "cpp", "facade_test.cpp")
+    lib_dir = os.path.dirname(L.LIB_PATH)
+    r = subprocess.run(["g++", "-std=c++20", "-O0", "-I" + os.path.join(repo, "include"), src, "-L" + lib_dir,
+                        "-lltfb_gpu", "-o", str(tmp_path / "facade_test")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]

@@ -380,3 +380,39 @@ def test_multi_gpu_run_matches_reference():
                         os.path.join(repo, "tools", "dist_run.py"), "--golden", "tiny_k2_"],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_cpp_facade_matches_python_mirror():
+    """The C++ façade (include/ltfb_b200/trainer.hpp: Trainer,
+    tournament_round, the reference's types and exceptions) and the Python
+    mirror drive the same library: identical step losses, decisions and
+    final generator hash."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(L.LIB_PATH), "facade_test")
+    if not os.path.exists(exe):
+        pytest.skip("facade_test not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    ds = L.synthetic_dataset(TINY, 400, sampling_seed=1, spec_seed=1)
+    base = L.make_cyclegan(TINY, L.SurrogateArch.tiny(), 7)
+    base.autoencoder_frozen = True
+    ts = []
+    for t in range(2):
+        m = base.copy()
+        L.reinit_gan_nets(m, L.mix_seed(7, 0x1417, t))
+        ids = np.arange(t * 200, t * 200 + 200, dtype=np.uint32)
+        ts.append(L.Trainer(L.TrainerConfig(trainer_id=t, n_shards=1, batch_size=32, seed=100 + t,
+                                            train_ids=ids[20:], tournament_ids=ids[:20]), ds, m))
+    kept = []
+    for rnd in (1, 2):
+        for t in ts:
+            t.train_steps(10)
+        res = L.tournament_round(ts, L.pair_trainers(2, rnd, 5), rnd)
+        kept += [int(r.kept_incoming) for r in res.trainer_records]
+    ref = [s.g_total for t in ts for s in t.history().steps]
+    assert got["g_total"] == ref
+    assert got["kept"] == kept
+    assert got["fwd_hash"] == L.hex64(ts[0].model().fwd_hash())

@@ -389,7 +389,7 @@ def main():
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{dom}_kind{kind}")
+            traffic = json.load(open(tpath)).get(f"{dom}_kind{kind}_{args.dims}")
         except Exception:
             traffic = None
 

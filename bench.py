@@ -282,6 +282,9 @@ def main():
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         comm = L.Comm(obj[0], k, rank, local)
+        # NCCL connects point-to-point peers on first use: connect every pair
+        # once now, outside any timed region
+        L.warm_peer_links(tr, L.NcclRoundComm(comm, dist))
 
     rounds_ms = []
     round_counter = [0]

@@ -15,6 +15,6 @@ from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrai
                   split_dataset, synth_generate, synthetic_dataset, tournament_round)
 
 from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, distributed_round,
-                     run_experiment, run_experiment_rank)
+                     run_experiment, run_experiment_rank, warm_peer_links)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -241,6 +241,27 @@ class TorchRoundComm:
         return out
 
 
+def warm_peer_links(trainer, comm):
+    """Exchanges a payload once with every other rank (circle-method
+    schedule: k - 1 rounds of disjoint pairs, a bye for odd k) so that the
+    point-to-point connections NCCL sets up lazily on first use exist
+    before the first tournament round. Decides nothing; the incoming buffer
+    is overwritten by the next real exchange."""
+    k, me = comm.world, comm.rank
+    n = k + (k & 1)  # even number of slots; slot k is the bye when k is odd
+    for r in range(n - 1):
+        if me == n - 1:
+            peer = r
+        elif me == r:
+            peer = n - 1
+        else:
+            peer = (2 * r - me) % (n - 1)
+        if peer < k and peer != me:
+            comm.exchange(trainer, peer)
+    if hasattr(trainer, "synchronize"):
+        trainer.synchronize()
+
+
 def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     """tournament/ltfb.hpp:96-164 seen from one rank (rank == trainer id):
     the pairing is recomputed locally (identical on every rank), the pair
@@ -289,6 +310,8 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset, comm, device: int = 0)
     rcfg = RunConfig(**{**cfg.__dict__, "devices": (device,)})
     base, history.pretrain = _base_model(rcfg, dataset, split[1])  # replicated, deterministic
     t = _trainer_for(rcfg, dataset, base, split, comm.rank)
+    if rounds_enabled:
+        warm_peer_links(t, comm)
     have_val = split[0].size > 0
     if have_val:
         t.set_validation(split[0])

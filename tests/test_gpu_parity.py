@@ -333,7 +333,7 @@ def test_autoencoder_frozen_and_bad_rows():
         L.AutoencoderPretrainer(model, ds.y)
 
 
-@pytest.mark.parametrize("pfx", ["tiny_k2_", "tiny_k3_", "desk_k2_"])
+@pytest.mark.parametrize("pfx", ["tiny_k2_", "tiny_k3_", "tiny_k4_", "desk_k2_"])
 def test_run_experiment_matches_reference(golden, pfx):
     """runner.run_experiment end to end on the device -- AE pre-training,
     per-trainer reinit, chunks, validation evals, rounds, best-of-k --
@@ -356,8 +356,9 @@ def test_run_experiment_matches_reference(golden, pfx):
     assert [s.step for s in h.steps] == list(g[pfx + "steps_step"])
     for key in ("d_loss", "g_total", "g_fwd", "g_adv", "g_cyc"):
         assert rel([getattr(s, key) for s in h.steps], g[pfx + "steps_" + key]) < 10 * REL_LOSS, key
-    assert [r.pairs[0] if r.pairs else None for r in h.rounds] == \
-        [(int(a), int(b)) for a, b in zip(g[pfx + "round_pair_a"], g[pfx + "round_pair_b"])]
+    assert [(r.round, tuple(p)) for r in h.rounds for p in r.pairs] == \
+        [(int(r), (int(a), int(b))) for r, a, b in
+         zip(g[pfx + "round_pair_round"], g[pfx + "round_pair_a"], g[pfx + "round_pair_b"])]
     assert [int(r.kept_incoming) for r in h.trainer_rounds] == [int(v) for v in g[pfx + "tr_kept"]]
     assert rel([r.local_metric for r in h.trainer_rounds], g[pfx + "tr_local"]) < 10 * REL_LOSS
     assert [x.bytes for x in h.transfers] == [int(v) for v in g[pfx + "xf_bytes"]]

@@ -193,14 +193,17 @@ std::size_t eval_wide_smem(const ModelArgs& m) {
   return sizeof(float) * (std::size_t)(2 * m.D * kEvT + kEvT * (kEvT + 4) + kEvT);
 }
 
-void launch_eval(const EvalArgs& a, cudaStream_t s) {
+void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc, bool precise) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
   k_eval_small<<<dim3((a.rows + kEvalRows - 1) / kEvalRows, a.nc), 128, 0, s>>>(a);
-  k_eval_wide<<<a.S, 256, eval_wide_smem(a.m), s>>>(a);
+  if (tc)
+    launch_eval_tc(a, *tc, precise, s);
+  else
+    k_eval_wide<<<a.S, 256, eval_wide_smem(a.m), s>>>(a);
   k_eval_finalize<<<1, 256, 0, s>>>(a);
 }
 

@@ -645,6 +645,11 @@ void encode_2d(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows, 
 }
 }  // namespace
 
+void encode_tile_map(void* map, const float* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                     uint32_t box_rows) {
+  encode_2d(reinterpret_cast<CUtensorMap*>(map), base, cols, rows, box_cols, box_rows);
+}
+
 // y maps are read by tile::gather4: box = one row of 32 columns
 void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows) {
   CUtensorMap m;

@@ -88,9 +88,23 @@ void launch_ae_passes(const AeArgs& a, cudaStream_t s);
 void launch_ae_adam(float* p, float* m1, float* m2, const float* g, long long count, double lr, double b1, double b2,
                     double eps, double c1, double c2, int sms, cudaStream_t s);
 
+/// Encodes a 2-D f32 tensor map (128-B swizzle) over [rows x cols].
+void encode_tile_map(void* map, const float* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                     uint32_t box_rows);
+/// tcgen05 evaluation of the decoder's wide layer (k_eval_tc.cu).
+struct EvalTcHost {
+  alignas(64) unsigned char maps[2 * 128];  // slice y, WdT
+  const float* bias_pad = nullptr;
+  bool ready = false;
+};
+bool eval_tc_supported(const ModelArgs& m);
+void encode_eval_maps(EvalTcHost& h, const float* slice_y, int rows, const float* wdt, const ModelArgs& m);
+void launch_eval_tc(const EvalArgs& a, const EvalTcHost& h, bool precise, cudaStream_t s);
 std::size_t eval_wide_smem(const ModelArgs& m);
 cudaError_t selftest_tc(const float* a1, const float* b1, const float* ah, const float* b2, const float* a3,
                         float* d1, float* d2, float* d3);
-void launch_eval(const EvalArgs& a, cudaStream_t s);
+/// k_eval_small, then the forward-MAE pass (tcgen05 when tc != nullptr,
+/// else the SIMT k_eval_wide), then k_eval_finalize.
+void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc = nullptr, bool precise = true);
 
 }  // namespace ltfb_dev

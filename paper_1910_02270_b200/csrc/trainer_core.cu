@@ -428,6 +428,13 @@ void DeviceTrainer::set_slice(int which, const float* x, const float* y, std::si
                                 cudaMemcpyHostToDevice, stream_));
   }
   (which == 0 ? tour_rows_ : val_rows_) = rows;
+  // tcgen05 eval maps over this slice (weights: the wide pass's K-major copy)
+  eval_tc_[which].ready = false;
+  if (rows && wide_kind_ >= 2 && ltfb_dev::eval_tc_supported(margs_) && !std::getenv("LTFB_EVAL_SIMT")) {
+    ltfb_dev::encode_eval_maps(eval_tc_[which], by.p, static_cast<int>(rows), wtp_.wdt, m);
+    eval_tc_[which].bias_pad = wtp_.bias_pad;
+    eval_tc_[which].ready = true;
+  }
   const std::size_t mx = std::max(tour_rows_, val_rows_);
   if (eval_h_.n < 2 * mx * m.D) {
     eval_h_.alloc(2 * mx * m.D);
@@ -824,7 +831,12 @@ EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int
   e.n_fwd = static_cast<long long>(counts_[2]);
   e.n_inv = static_cast<long long>(counts_[3]);
   e.ctr = ctr_.p;
-  ltfb_dev::launch_eval(e, stream_);
+  const ltfb_dev::EvalTcHost* etc = eval_tc_[which].ready ? &eval_tc_[which] : nullptr;
+  if (etc) {
+    prepare_params();  // the K-major weight copy the tensor-core pass reads
+    e.S = sm_count_;
+  }
+  ltfb_dev::launch_eval(e, stream_, etc, wide_kind_ == 2);
   if (decide) small_T_dirty_ = true;  // the device may have adopted the incoming generator
   if (decide) h_ready_ = false;
   launches_ += 3;

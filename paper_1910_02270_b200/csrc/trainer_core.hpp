@@ -256,6 +256,7 @@ class DeviceTrainer {
   DevBuf<float> eval_h_;
   DevBuf<double> eval_inv_, eval_part_, eval_out_;
   std::size_t eval_S_ = 0;
+  ltfb_dev::EvalTcHost eval_tc_[2];
 
   // timing
   cudaEvent_t tmr_[2] = {nullptr, nullptr};

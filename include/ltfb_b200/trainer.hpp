@@ -144,6 +144,13 @@ class Trainer {
     }
   }
 
+  /// train::Trainer(TrainerConfig, const DatasetIndex&, CycleGan<float>)
+  /// over LBDS bundle files on disk (data/bundle.hpp:134-224): the
+  /// partition and the tournament slice are read once (the preload of
+  /// store.hpp:100-135) and made resident in HBM.
+  Trainer(TrainerConfig cfg, const ltfb::data::DatasetIndex& index, CycleGan<float> model)
+      : Trainer(cfg, read_view(index, cfg), std::move(model)) {}  // cfg copied: read_view reads it
+
   int id() const { return cfg_.trainer_id; }
   const TrainerConfig& config() const { return cfg_; }
   ltfb_trainer* handle() { return h_.get(); }
@@ -249,6 +256,24 @@ class Trainer {
     for (std::uint64_t i = 0; i < n; ++i)
       history_.epochs.push_back({cfg_.trainer_id, buf[i].epoch, buf[i].steps, 0, 0, buf[i].samples_shuffled,
                                  buf[i].seconds, buf[i].partial != 0});
+  }
+
+  // Rows of the partition and the tournament slice read from the bundles
+  // into a dense host view indexed by global id (only those rows filled).
+  static DatasetView read_view(const ltfb::data::DatasetIndex& index, const TrainerConfig& cfg) {
+    static thread_local std::vector<float> x, y;
+    const std::size_t in = index.dims.input_dim, out = index.dims.output_dim();
+    x.assign(index.total * in, 0.0f);
+    y.assign(index.total * out, 0.0f);
+    for (const auto* ids : {&cfg.train_ids, &cfg.tournament_ids}) {
+      std::vector<float> bx(ids->size() * in), by(ids->size() * out);
+      ltfb::data::read_records(index, std::span<const std::uint32_t>(*ids), bx.data(), by.data(), out);
+      for (std::size_t i = 0; i < ids->size(); ++i) {
+        std::copy_n(bx.data() + i * in, in, x.data() + static_cast<std::size_t>((*ids)[i]) * in);
+        std::copy_n(by.data() + i * out, out, y.data() + static_cast<std::size_t>((*ids)[i]) * out);
+      }
+    }
+    return DatasetView{index.dims, index.total, x.data(), y.data()};
   }
 
   TrainerConfig cfg_;

@@ -2,7 +2,10 @@
 // trainers on tiny dims through ltfb_b200::Trainer / tournament_round, the
 // reference's own types; prints one JSON line with every step's g_total and
 // every round decision so the test can compare it with the Python mirror.
+#include <unistd.h>
+
 #include <cstdio>
+#include <filesystem>
 #include <vector>
 
 #include "ltfb_b200/trainer.hpp"
@@ -50,6 +53,27 @@ int main() {
   std::printf("], \"kept\": [");
   for (std::size_t i = 0; i < kept.size(); ++i) std::printf("%s%d", i ? ", " : "", kept[i]);
   std::printf("], \"fwd_hash\": \"%s\"}\n", hex64(ts[0]->model().fwd_hash()).c_str());
+  {  // the same trainer 0 built from LBDS bundle files (DatasetIndex) trains identically
+    std::vector<data::SampleRecord> recs(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      recs[i].inputs.assign(x.begin() + i * in, x.begin() + (i + 1) * in);
+      recs[i].outputs.assign(y.begin() + i * out, y.begin() + (i + 1) * out);
+    }
+    const auto dir = std::filesystem::temp_directory_path() / ("ltfb_facade_" + std::to_string(::getpid()));
+    data::write_bundles(std::span<const data::SampleRecord>(recs), dims, 100, dir);
+    const auto index = data::DatasetIndex::scan_dir(dir);
+    auto m = base;
+    surrogate::reinit_gan_nets(m, mix_seed({7, 0x1417, 0}));
+    ltfb_b200::TrainerConfig c;
+    c.batch_size = 32;
+    c.seed = 100;
+    for (std::uint32_t i = 0; i < 180; ++i) c.train_ids.push_back(20 + i);
+    for (std::uint32_t i = 0; i < 20; ++i) c.tournament_ids.push_back(i);
+    ltfb_b200::Trainer tb(c, index, m);
+    tb.train_steps(10);
+    if (tb.history().steps.back().g_total != ts[0]->history().steps[9].g_total) return 3;
+    std::filesystem::remove_all(dir);
+  }
   try {  // the reference's error behaviour through the façade
     ts[0]->adopt_generators(ts[1]->model().inv, ts[1]->model().fwd);
     return 2;

@@ -361,24 +361,43 @@ __device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr, int bas
 /// pT the next step stages) and, if push, into the blob image and W^T image
 /// of every CTA of the cluster (DSMEM stores; visible after the next cluster
 /// barrier), so no CTA has to pull or re-transpose the updated network.
-__device__ __noinline__ void adam_owned(const StepArgs& a, int net, const NetS& n, int lo, int hi, double c1,
-                                        double c2, int gr, int mo, int vo, int push /* 1 blob, 2 blob + W^T */) {
-  cg::cluster_group cl = cg::this_cluster();
+/// First half of the owner's Adam step, issued before the cluster learns
+/// whether every gradient is finite (so the f64 chain overlaps the barrier):
+/// m, v and the new parameter of each owned element are computed in place
+/// of the slice's moment and gradient images. Nothing global changes here.
+__device__ __noinline__ void adam_compute(const StepArgs& a, int net, const NetS& n, int lo, int hi, double c1,
+                                          double c2, int gr, int mo, int vo) {
   float* s = S();
   const double lr = a.lr[net], b1 = a.b1, b2 = a.b2, eps = a.eps;
+  for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
+    const double gd = (double)s[gr + e - lo];
+    const double mi = __dadd_rn(__dmul_rn(b1, (double)s[mo + e - lo]), __dmul_rn(1.0 - b1, gd));
+    const double vi = __dadd_rn(__dmul_rn(b2, (double)s[vo + e - lo]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
+    s[mo + e - lo] = (float)mi;
+    s[vo + e - lo] = (float)vi;
+    s[gr + e - lo] = (float)__dsub_rn((double)s[n.blob + e],
+                                      __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)),
+                                                __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
+  }
+}
+
+/// Second half (the step is applied): the owner writes m, v, p and, for
+/// weights, the W^T copy pT to HBM (the images the next step stages) and, if
+/// push, the new value into the blob image and W^T image of every CTA of its
+/// half (DSMEM stores; visible after the next cluster barrier), so no CTA
+/// has to pull or re-transpose the updated network.
+__device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS& n, int lo, int hi, int gr, int mo,
+                                         int vo, int push /* 1 blob, 2 blob + W^T */) {
+  cg::cluster_group cl = cg::this_cluster();
+  float* s = S();
   float* p = a.p[net];
   float* pT = a.pT[net];
   float* m1 = a.mom1[net];
   float* m2 = a.mom2[net];
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
-    const double gd = (double)s[gr + e - lo];
-    const double mi = __dadd_rn(__dmul_rn(b1, (double)s[mo + e - lo]), __dmul_rn(1.0 - b1, gd));
-    const double vi = __dadd_rn(__dmul_rn(b2, (double)s[vo + e - lo]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-    m1[e] = (float)mi;
-    m2[e] = (float)vi;
-    const float pn = (float)__dsub_rn((double)s[n.blob + e],
-                                      __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)),
-                                                __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
+    const float pn = s[gr + e - lo];
+    m1[e] = s[mo + e - lo];
+    m2[e] = s[vo + e - lo];
     p[e] = pn;
     int t = -1;  // W^T position of a weight element (biases have none)
     for (int l = 0; l < n.L; ++l) {
@@ -702,6 +721,8 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   const int dok = reduce_owned(Y.pg[0], R.lo[0], R.hi[0], Y.gr[0]);
   ST();
   if (tid == 0) s_ok[0] = dok;
+  const NetS& C = Y.net[kCd];
+  adam_compute(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0]);
   double d_sum = 0.0;
   for (int r = 0; r < kC; ++r) d_sum += cl.map_shared_rank(s_loss, r)[0];
   const double n2 = 2.0 * (double)R.rows;
@@ -711,10 +732,7 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   int all_ok = 1;
   for (int r = 0; r < kC; ++r) all_ok &= cl.map_shared_rank(s_ok, r)[0];
   const bool d_ok = isfinite(*d_loss) && all_ok;
-  const NetS& C = Y.net[kCd];
-  if (d_ok) {
-    adam_owned(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0], 2);
-  }
+  if (d_ok) adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], 2);
   ST();
   cluster_sync();  // S3: every owner's updated disc slice (blob + W^T) pushed into every CTA
   return d_ok;
@@ -735,6 +753,8 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   const int cb = R.split ? kC : 0;
   const int fok = reduce_owned(Y.pg[1], R.lo[1], R.hi[1], Y.gr[1]);
   const int iok = R.split ? 1 : reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
+  adam_compute(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1], Y.vo[1]);
+  if (!R.split) adam_compute(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2]);
   ST();
   if (tid == 0) {
     s_ok[1] = fok;
@@ -767,14 +787,12 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
-    adam_owned(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1],
-               Y.vo[1], a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
+    adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1],
+                a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
     out[4] = 1.0;
     ST();
     if (all_i) {
-      if (!R.split)
-        adam_owned(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2],
-                   Y.vo[2], 0);
+      if (!R.split) adam_commit(a, kInv, Y.net[kI], R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], 0);
       out[5] = 1.0;
     }
   }
@@ -892,6 +910,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   cluster_wait();
   const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2], kC);
   if (tid == 0) s_ok[2] = iok;
+  adam_compute(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2]);
   cluster_sync();  // S2 (d_update's flags)
   double d_sum = 0.0;
   int all_ok = 1;
@@ -919,7 +938,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
     const double total = ((double)rows * total_raw) / (double)rows;
     if (isfinite(total) && all_f && all_i)  // trainer.hpp:256-264: inv after fwd
-      adam_owned(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], 0);
+      adam_commit(a, kInv, I, R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], 0);
   }
   cluster_sync();  // S6
 }

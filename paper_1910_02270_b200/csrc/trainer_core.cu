@@ -128,7 +128,10 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
       throw ContractError("wide_kernel must be 0 (auto), 1 (generic), 2 (tcgen05 3xTF32) or 3 (tcgen05 TF32)");
     }
   }
-  S_ = wide_kind_ >= 2 ? static_cast<std::size_t>(sm_count_)
+  // tcgen05 pass: one CTA per SM, but never more CTAs than 32-column tiles
+  // (small dims would otherwise pay for idle CTAs in the grid barrier and the
+  // split-K reduction)
+  S_ = wide_kind_ >= 2 ? std::min<std::size_t>(static_cast<std::size_t>(sm_count_), (ma.out + 31) / 32)
                        : std::min<std::size_t>((ma.out + 31) / 32, static_cast<std::size_t>(sm_count_) * 2);
   const std::size_t yb_rows = std::max<std::size_t>(B, 128);
   xb_.alloc(static_cast<std::size_t>(B) * ma.in);

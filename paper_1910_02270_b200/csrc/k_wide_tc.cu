@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   // array itself (not an integer round trip) keeps every access an LDS/STS
   unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kStages], split_done[kStages], sready[kStages], empty[kStages];
-  __shared__ uint64_t yfull[kYStages], yempty[kYStages];
+  __shared__ uint64_t yfull[kYStages];
   __shared__ uint64_t ofull[2], oempty[2], h_ready, done;
   __shared__ uint32_t tmem_base;
   __shared__ double red[128];
@@ -129,7 +129,6 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     }
     for (int s = 0; s < kYStages; ++s) {
       tc::mbar_init(&yfull[s], 1);
-      tc::mbar_init(&yempty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&ofull[b], 1);
@@ -153,62 +152,21 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
-    // y rows come straight from the HBM data store (epoch_plan.hpp:106-137,
-    // store.hpp:140-181): lane l gathers rows 4l..4l+3 of the step with one
-    // tile::gather4 per tile, so no separate gather kernel or minibatch copy
-    int rw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int rr = 4 * lane + u;
-      if (a.y_identity) {
-        rw[u] = rr;  // host-streamed minibatch buffer
-      } else {
-        const unsigned* perm = a.perm[a.ctr->epoch & 1] + (long long)a.ctr->step_in_epoch * a.B;
-        rw[u] = (int)perm[rr < rows ? rr : 0];
+    // weight tiles only (the y rows are gathered by the staging warps,
+    // which refill each y slot as soon as they have read it)
+    for (int iw = 0; iw < my_tiles; ++iw) {
+      const int s = iw % kStages;
+      if (lane == 0) {
+        if (iw >= kStages) tc::mbar_wait(&empty[s], ((uint32_t)(iw / kStages) & 1u) ^ 1u);
+        const int c0 = ((int)blockIdx.x + iw * (int)gridDim.x) * kTileN;
+        LTFB_EV(iw, 0);
+        tc::mbar_expect_tx(&full[s], 3 * kWt);
+        tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
+        tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
+        tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
+        tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
       }
-    }
-    // two independent rings: y tiles (random store rows, the long-latency
-    // loads) whenever a y slot is free, weight tiles whenever a weight stage
-    // is free; neither waits for the other
-    int iy = 0, iw = 0;
-    while (iy < my_tiles || iw < my_tiles) {
-      bool did = false;
-      if (iw < my_tiles) {
-        const int s = iw % kStages;
-        const uint32_t ph = (uint32_t)(iw / kStages) & 1u;
-        int ready = 1;
-        if (lane == 0) ready = iw < kStages || tc::mbar_test(&empty[s], ph ^ 1u);
-        ready = __shfl_sync(0xffffffffu, ready, 0);
-        if (ready) {
-          const int c0 = ((int)blockIdx.x + iw * (int)gridDim.x) * kTileN;
-          if (lane == 0) {
-            LTFB_EV(iw, 0);
-            tc::mbar_expect_tx(&full[s], 3 * kWt);
-            tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
-            tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
-            tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
-            tc::tma_load_2d(WtH(s) + 4096, &tp.tm_wdt, &full[s], 32, c0);
-          }
-          ++iw;
-          did = true;
-        }
-      }
-      if (iy < my_tiles) {
-        const int sy = iy % kYStages;
-        const uint32_t ph = (uint32_t)(iy / kYStages) & 1u;
-        int ready = 1;
-        if (lane == 0) ready = iy < kYStages || tc::mbar_test(&yempty[sy], ph ^ 1u);
-        ready = __shfl_sync(0xffffffffu, ready, 0);
-        if (ready) {
-          const int c0 = ((int)blockIdx.x + iy * (int)gridDim.x) * kTileN;
-          if (lane == 0) tc::mbar_expect_tx(&yfull[sy], kY);
-          __syncwarp();
-          tc::tma_gather4(Yraw(sy) + 512 * lane, &tp.tm_y, &yfull[sy], c0, rw[0], rw[1], rw[2], rw[3]);
-          ++iy;
-          did = true;
-        }
-      }
-      if (!did) __nanosleep(20);
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------- MMA issuer --
@@ -420,6 +378,33 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         lp[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
       }
     };
+    // y rows come straight from the HBM data store (epoch_plan.hpp:106-137,
+    // store.hpp:140-181) with TMA tile::gather4 (4 rows per instruction, 32
+    // per tile). One warp issuing all 32 costs ~2 k cycles per tile (the
+    // issue serialises); lanes 0-7 of the four staging warps issue 8 each
+    // (~0.7 k), so this warp group gathers: gather g covers rows 4g .. 4g+3.
+    const int g = (warp - 6) * 8 + lane;  // gather slot of this lane (lanes < 8)
+    int rw[4] = {0, 0, 0, 0};
+    if (lane < 8) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = 4 * g + u;
+        if (a.y_identity) {
+          rw[u] = rr;  // host-streamed minibatch buffer
+        } else {
+          const unsigned* perm = a.perm[a.ctr->epoch & 1] + (long long)a.ctr->step_in_epoch * a.B;
+          rw[u] = (int)perm[rr < rows ? rr : 0];
+        }
+      }
+    }
+    auto gather = [&](int it) {  // all 128 staging threads call this
+      const int sy = it % kYStages;
+      const int c0 = ((int)blockIdx.x + it * (int)gridDim.x) * kTileN;
+      if (t == 0) tc::mbar_expect_tx(&yfull[sy], kY);
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // expect_tx before any complete_tx
+      if (lane < 8) tc::tma_gather4(Yraw(sy) + 512 * g, &tp.tm_y, &yfull[sy], c0, rw[0], rw[1], rw[2], rw[3]);
+    };
+    for (int it = 0; it < kYStages && it < my_tiles; ++it) gather(it);
     for (int i = 0; i < my_tiles; ++i) {
       const int s = i % kStages;
       const uint32_t ph = (uint32_t)(i / kStages) & 1u;
@@ -443,8 +428,10 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         }
         tc::tmem_st32(T + lane_addr + tYh(s), v);
         if (kPrecise) tc::tmem_st32(T + lane_addr + tYl(s), vl);
-        tc::mbar_arrive(&yempty[sy]);  // the row is in registers / TMEM: the y slot can refill
       }
+      // every staging thread has read its row of slot sy: refill it (the
+      // barrier inside gather() orders the reads before the async writes)
+      if (i + kYStages < my_tiles) gather(i + kYStages);
       if (kPrecise) {
         split(WeH(s), WeL(s), kWt / 16);
         split(WdH(s), WdL(s), kWt / 16);

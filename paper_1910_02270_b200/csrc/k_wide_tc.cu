@@ -488,8 +488,10 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
         }
       }
     }
+    if (prof && threadIdx.x == 0) s_ph[4] = clock64();
     part[g * kMaxQ + o] = acc;
     __syncthreads();
+    if (prof && threadIdx.x == 0) s_ph[5] = clock64();
     if (g == 0 && o < nq) {
       float4 t = part[o];
       for (int k = 1; k < G; ++k) {
@@ -505,6 +507,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
       if (q < q_enc) red_enc[q] = t;
       else red_dec[q - q_enc] = t;
     }
+    if (prof && threadIdx.x == 0) s_ph[6] = clock64();
     if (blockIdx.x == 0 && warp == 0) {  // MAE total: lanes own strided partials, fixed xor tree
       double v[5];
 #pragma unroll
@@ -517,8 +520,11 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   }
   if (prof && threadIdx.x == 0)
   {
-    printf("wide phases (cycles): h %lld, tiles %lld, grid sync %lld, reduce %lld\n", s_ph[1] - s_ph[0],
-           s_ph[2] - s_ph[0], s_ph[3] - s_ph[2], clock64() - s_ph[3]);
+    const long long tend = clock64();
+    printf("wide phases (cycles): h %lld, tiles %lld, grid sync %lld, reduce %lld (loads %lld, part sync %lld, "
+           "sum+write %lld, mae %lld)\n",
+           s_ph[1] - s_ph[0], s_ph[2] - s_ph[0], s_ph[3] - s_ph[2], tend - s_ph[3], s_ph[4] - s_ph[3],
+           s_ph[5] - s_ph[4], s_ph[6] - s_ph[5], tend - s_ph[6]);
     for (int i = 0; i < my_tiles && i < 16; ++i)
       printf("  tile %d: issue %lld tma %lld split %lld mma12 %lld epi_in %lld epi_out %lld mma3 %lld\n", i,
              s_ev[i][0] - s_ph[0], s_ev[i][1] - s_ph[0], s_ev[i][2] - s_ph[0], s_ev[i][3] - s_ph[0],

@@ -417,3 +417,24 @@ def test_cpp_facade_matches_python_mirror():
     assert got["g_total"] == ref
     assert got["kept"] == kept
     assert got["fwd_hash"] == L.hex64(ts[0].model().fwd_hash())
+
+
+def test_host_buffer_path_matches_store_path():
+    """The e2e entry point (ltfb_trainer_train_steps_host: minibatches from
+    pinned host memory, copied H2D inside the call -- bench.py's e2e leg)
+    computes exactly what the HBM-store path computes for the same rows."""
+    n, B, steps, seed = 700, 128, 3, 11
+    ds = L.synthetic_dataset(PAPER, n, sampling_seed=2, spec_seed=1)
+    model = L.make_cyclegan(PAPER, L.SurrogateArch(), 4)
+    model.autoencoder_frozen = True
+    ids = np.arange(n, dtype=np.uint32)
+    cfg = L.TrainerConfig(n_shards=1, batch_size=B, seed=seed, train_ids=ids[50:], tournament_ids=ids[:50])
+    ta = L.Trainer(cfg, ds, model.copy())
+    ta.train_steps(steps)
+    tb = L.Trainer(cfg, ds, model.copy())
+    rows = L.epoch_permutation(ids[50:], 1, seed)[:steps * B]  # epoch_plan.hpp:69-71
+    x = np.ascontiguousarray(ds.x[rows].reshape(steps, B, -1), np.float32)
+    y = np.ascontiguousarray(ds.y[rows].reshape(steps, B, -1), np.float32)
+    recs = tb.train_steps_host(steps, x, y)
+    for i, s in enumerate(ta.history().steps):
+        assert recs[i]["g_total"] == s.g_total and recs[i]["d_loss"] == s.d_loss

@@ -616,13 +616,18 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
       }
     }
   }
+  // Loads needed only much later go out as cp.async (no stall here): the
+  // Adam bias corrections and the MAE total (awaited in d_update), the next
+  // step's x rows (awaited in next_h). Only the index loads block.
   if (tid < 3) {
     const int net = tid == 0 ? kDisc : (tid == 1 ? kFwd : kInv);
     const unsigned long long t = a.ctr->t[net] + 1;
-    g_pre[2 * tid] = a.adam_c[2 * t];
-    g_pre[2 * tid + 1] = a.adam_c[2 * t + 1];
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(&g_pre[2 * tid])),
+                 "l"(a.adam_c + 2 * t)
+                 : "memory");
   } else if (tid == 3) {
-    g_pre[6] = *a.mae_total;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_u32(&g_pre[6])), "l"(a.mae_total)
+                 : "memory");
   }
   if (a.post_next_h) {  // x rows of the next step of this epoch (used by next_h)
     const int nxt = (int)a.ctr->step_in_epoch + 1;
@@ -633,7 +638,12 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
       const unsigned* perm = a.perm[a.ctr->epoch & 1u] + (long long)nxt * a.B + r0;
       for (int i = tid; i < kR * in; i += kThreads) {
         const int r = i / in, k = i - r * in;
-        s[Y.xn + i] = r < nr ? a.sx[(long long)perm[r] * in + k] : 0.0f;
+        if (r < nr)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(s + Y.xn + i)),
+                       "l"(a.sx + (long long)perm[r] * in + k)
+                       : "memory");
+        else
+          s[Y.xn + i] = 0.0f;
       }
     }
   }
@@ -647,8 +657,10 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
   {
     // enc layer-0 activation of this CTA's rows (pad rows: act(0 + b))
     const int e1 = Y.net[kET].L > 0 ? Y.e1 : Y.stacked;
-    for (int i = tid; i < kR * E1; i += kThreads)
-      s[e1 + i] = act_apply(m.enc_act0, m.enc_slope0, s[Y.e1 + i] + s[Y.be + i % E1]);
+    for (int i = tid; i < kR * E1; i += kThreads) {
+      const int c = i - (i / E1) * E1;
+      s[e1 + i] = act_f(m.enc_act0, m.enc_slope0, s[Y.e1 + i] + s[Y.be + c]);
+    }
     // dL/dh = (1/n) S Wd^T (loss.hpp:37-39; the 1/n scale folded after the sum)
     const float gscale = (float)(1.0 / ((double)R.rows * (double)m.out));
     const int gh = Y.net[kDH].L > 0 ? Y.gh : Y.gl_dec;
@@ -718,6 +730,7 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   float* s = S();
   const int tid = threadIdx.x;
   ST();
+  cp_wait_all();  // g_pre (prologue cp.async); reduce_owned's barrier publishes it
   const int dok = reduce_owned(Y.pg[0], R.lo[0], R.hi[0], Y.gr[0]);
   ST();
   if (tid == 0) s_ok[0] = dok;
@@ -849,6 +862,8 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
   const int r0 = min(rank * per, rows), nr = max(0, min(per, rows - r0));
   (void)epoch;
   const int in = m.in;
+  cp_wait_all();  // the xn rows (prologue cp.async)
+  __syncthreads();
   for (int i = tid; i < kR * in; i += kThreads) {  // rows prefetched into xn by the prologue
     const float v = s[Y.xn + i];
     if (i < nr * in) a.xb[(long long)r0 * in + i] = v;
@@ -908,6 +923,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   __syncthreads();
   cluster_arrive();  // S1
   cluster_wait();
+  cp_wait_all();  // g_pre (prologue cp.async); reduce_owned's barrier publishes it
   const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2], kC);
   if (tid == 0) s_ok[2] = iok;
   adam_compute(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2]);

@@ -438,3 +438,33 @@ def test_host_buffer_path_matches_store_path():
     recs = tb.train_steps_host(steps, x, y)
     for i, s in enumerate(ta.history().steps):
         assert recs[i]["g_total"] == s.g_total and recs[i]["d_loss"] == s.d_loss
+
+
+def test_split_and_sequential_post_kernels_agree():
+    """The 16-CTA split post kernel (cycle path in the second half) and the
+    8-CTA sequential fallback (LTFB_POST_NO_SPLIT) compute the same step:
+    identical losses, bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, numpy as np, paper_1910_02270_b200 as L\n"
+        "d = L.ModalityDims.paper_scale()\n"
+        "ds = L.synthetic_dataset(d, 500, sampling_seed=4, spec_seed=1)\n"
+        "m = L.make_cyclegan(d, L.SurrogateArch(), 9); m.autoencoder_frozen = True\n"
+        "ids = np.arange(500, dtype=np.uint32)\n"
+        "t = L.Trainer(L.TrainerConfig(n_shards=1, batch_size=128, seed=5, train_ids=ids[40:],"
+        " tournament_ids=ids[:40]), ds, m)\n"
+        "t.train_steps(6)\n"
+        "print(json.dumps([[s.d_loss, s.g_total, s.g_cyc] for s in t.history().steps]))\n")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for no_split in ("", "1"):
+        env = dict(os.environ, PYTHONPATH=repo)
+        if no_split:
+            env["LTFB_POST_NO_SPLIT"] = "1"
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]

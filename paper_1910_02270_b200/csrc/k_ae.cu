@@ -186,7 +186,15 @@ __global__ void __launch_bounds__(kT) k_ae_dec(const __grid_constant__ AeArgs a)
   if (bad) atomicOr(&a.flags[1], 1);
 }
 
-// K5: gh reduction, small-network backward, gz0, db0, loss (one CTA)
+// K5a: gh = sum_s Pg[s] (fixed split order); grid n, block D
+__global__ void k_ae_ghreduce(const __grid_constant__ AeArgs a) {
+  const int r = blockIdx.x, j = threadIdx.x, D = a.m.D, n = a.n;
+  float acc = 0.0f;
+  for (int s = 0; s < a.S; ++s) acc += a.Pg[((long long)s * n + r) * D + j];
+  a.gh[r * D + j] = acc;
+}
+
+// K5: small-network backward, gz0, db0, loss (one CTA)
 __global__ void __launch_bounds__(512) k_ae_small_bwd(const __grid_constant__ AeArgs a) {
   __shared__ int bad_enc, bad_dec;
   const ModelArgs& m = a.m;
@@ -195,12 +203,7 @@ __global__ void __launch_bounds__(512) k_ae_small_bwd(const __grid_constant__ Ae
     bad_enc = 0;
     bad_dec = 0;
   }
-  for (int i = threadIdx.x; i < n * D; i += blockDim.x) {
-    float s = 0.0f;
-    for (int q = 0; q < a.S; ++q) s += a.Pg[(long long)q * n * D + i];
-    a.gh[i] = s;
-  }
-  __syncthreads();
+  (void)D;
   // dec head (lat -> D): gradient of h -> dec-head params + dL/dlatent
   if (m.dec_head.L > 0)
     mlp_backward(m.dec_head, a.dec, a.latent, m.lat, n, a.dhz, a.dha, a.gh, a.gdec + m.dec_head.base, a.glat,
@@ -302,6 +305,7 @@ void launch_ae_passes(const AeArgs& a, cudaStream_t s) {
   ae::k_ae_zreduce<<<a.n, a.m.E1, 0, s>>>(a);
   ae::k_ae_small_fwd<<<1, 512, 0, s>>>(a);
   ae::k_ae_dec<<<a.S, ae::kT, sm_dec, s>>>(a);
+  ae::k_ae_ghreduce<<<a.n, a.m.D, 0, s>>>(a);
   ae::k_ae_small_bwd<<<1, 512, 0, s>>>(a);
   ae::k_ae_encw<<<a.S, ae::kT, sm_encw, s>>>(a);
 }

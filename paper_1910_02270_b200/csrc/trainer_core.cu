@@ -1057,7 +1057,7 @@ double DeviceTrainer::ae_step(const std::uint32_t* rows_idx, std::size_t n) {
   LTFB_CUDA(cudaMemcpyAsync(ae_idx_.p, rows_idx, n * 4, cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaMemsetAsync(ae_flags_.p, 0, 8, stream_));
   ltfb_dev::launch_ae_passes(a, stream_);
-  launches_ += 6;
+  launches_ += 7;
   double loss = 0.0;
   int flags[2] = {0, 0};
   LTFB_CUDA(cudaMemcpyAsync(&loss, ae_loss_.p, 8, cudaMemcpyDeviceToHost, stream_));

@@ -51,39 +51,59 @@ __device__ __forceinline__ void load_y_tile(const AeArgs& a, float* yt, int c0) 
   }
 }
 
-// K1: split-K partials of y We0 (thread: e = tid % 64, rows tid / 64 + 4 i)
+// K1: split-K partials of y We0. Register tiles: thread (ty, tx) owns rows
+// 4 ty .. 4 ty + 3 and features 8 tx .. 8 tx + 7 (32 accumulators); per
+// column c one float4 of y^T and two float4 of We feed 32 FMAs (k order =
+// column order, as the reference's matmul).
 __global__ void __launch_bounds__(kT) k_ae_enc(const __grid_constant__ AeArgs a) {
   float* sm = smem();
-  float* yt = sm;                   // [rows x 32]
-  float* we = yt + kMaxRows * kTN;  // [32 x E1]
+  float* yT = sm;                   // [32 cols x 128 rows]
+  float* we = yT + kTN * kMaxRows;  // [32 cols x 64]
   const int n = a.n, E1 = a.m.E1, out = a.m.out;
   const float* We = a.enc + a.m.enc_wide_w;
-  const int e = threadIdx.x & 63, rg = threadIdx.x >> 6;
-  float acc[kMaxRows / 4];
+  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;  // rows 4 ty.., features 8 tx..
+  float acc[4][8];
 #pragma unroll
-  for (int i = 0; i < kMaxRows / 4; ++i) acc[i] = 0.0f;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
   const int ntiles = (out + kTN - 1) / kTN;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int c0 = t * kTN;
     __syncthreads();
-    load_y_tile(a, yt, c0);
-    for (int i = threadIdx.x; i < kTN * E1; i += kT) {
-      const int c = i / E1;
-      we[i] = c0 + c < out ? We[(long long)(c0 + c) * E1 + (i - c * E1)] : 0.0f;
+    for (int i = threadIdx.x; i < kMaxRows * kTN; i += kT) {
+      const int r = i >> 5, c = i & 31;
+      yT[c * kMaxRows + r] =
+          (r < n && c0 + c < out) ? a.ysrc[(long long)a.idx[r] * a.m.out_pad + c0 + c] : 0.0f;
+    }
+    for (int i = threadIdx.x; i < kTN * kMaxW; i += kT) {
+      const int c = i >> 6, e = i & 63;
+      we[i] = (c0 + c < out && e < E1) ? We[(long long)(c0 + c) * E1 + e] : 0.0f;
     }
     __syncthreads();
-    if (e < E1)
-      for (int c = 0; c < kTN; ++c) {
-        const float w = we[c * E1 + e];
+#pragma unroll 4
+    for (int c = 0; c < kTN; ++c) {
+      const float4 y4 = *reinterpret_cast<const float4*>(yT + c * kMaxRows + 4 * ty);
+      const float4 w0 = *reinterpret_cast<const float4*>(we + c * kMaxW + 8 * tx);
+      const float4 w1 = *reinterpret_cast<const float4*>(we + c * kMaxW + 8 * tx + 4);
+      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int i = 0; i < kMaxRows / 4; ++i)
-          if (rg + 4 * i < n) acc[i] = fmaf(yt[(rg + 4 * i) * kTN + c], w, acc[i]);
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(yv[i], wv[j], acc[i][j]);
+    }
   }
-  if (e < E1)
 #pragma unroll
-    for (int i = 0; i < kMaxRows / 4; ++i)
-      if (rg + 4 * i < n) a.Pz[((long long)blockIdx.x * n + rg + 4 * i) * E1 + e] = acc[i];
+  for (int i = 0; i < 4; ++i) {
+    const int r = 4 * ty + i;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = 8 * tx + j;
+      if (e < E1) a.Pz[((long long)blockIdx.x * n + r) * E1 + e] = acc[i][j];
+    }
+  }
 }
 
 // K2: z0 = sum_s Pz[s] + b0, a0 = act(z0); grid n, block E1
@@ -103,26 +123,39 @@ __global__ void __launch_bounds__(512) k_ae_small_fwd(const __grid_constant__ Ae
   mlp_forward(m.dec_head, a.dec, a.latent, m.lat, a.n, a.dhz, a.dha, BlockSync{});
 }
 
-// K4: dec wide layer forward, loss, dWd / dbd, split-K partials of dL/dh
+// K4: dec wide layer forward, loss, dWd / dbd, split-K partials of dL/dh.
+// All three products are register-tiled from float4 shared-memory operands
+// (h, the Wd tile and G are kept in both orientations); every dot product
+// keeps the reference's k order (q, then rows, then columns ascending).
 __global__ void __launch_bounds__(kT) k_ae_dec(const __grid_constant__ AeArgs a) {
   __shared__ double red[kT];
   float* sm = smem();
   const int n = a.n, D = a.m.D, out = a.m.out;
-  float* hs = sm;                       // [rows x D]
-  float* yt = hs + kMaxRows * kMaxW;    // [rows x 32]
-  float* wd = yt + kMaxRows * kTN;      // [D x 32]
-  float* G = wd + kMaxW * kTN;          // [rows x 33]
-  float* bd = G + kMaxRows * (kTN + 1); // [32]
+  float* hs = sm;                          // [128 rows x 64]
+  float* hT = hs + kMaxRows * kMaxW;       // [64 x 128 rows]
+  float* yt = hT + kMaxW * kMaxRows;       // [128 rows x 32]
+  float* wd = yt + kMaxRows * kTN;         // [64 x 32]  Wd tile
+  float* wdT = wd + kMaxW * kTN;           // [32 x 64]
+  float* G = wdT + kTN * kMaxW;            // [128 rows x 32]
+  float* GT = G + kMaxRows * kTN;          // [32 x 128 rows]
+  float* bd = GT + kTN * kMaxRows;         // [32]
   const float* Wd = a.dec + a.m.dec_wide_w;
   const float* Bd = a.dec + a.m.dec_wide_b;
   float* dWd = a.gdec + a.m.dec_wide_w;
   float* dbd = a.gdec + a.m.dec_wide_b;
   const float g1 = (float)(1.0 / ((double)n * (double)out));  // loss.hpp:37-39
-  for (int i = threadIdx.x; i < n * D; i += kT) hs[i] = a.h[i];
-  const int j = threadIdx.x & 63, rg = threadIdx.x >> 6;  // gh partial owner
-  float acc[kMaxRows / 4];
+  for (int i = threadIdx.x; i < kMaxRows * kMaxW; i += kT) {
+    const int r = i >> 6, q = i & 63;
+    const float v = (r < n && q < D) ? a.h[r * D + q] : 0.0f;
+    hs[i] = v;
+    hT[q * kMaxRows + r] = v;
+  }
+  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;  // (1) and (3): rows 4 ty ..
+  float acc[4][8];  // (3) dL/dh partial: rows 4 ty .. + 3, j = 8 tx .. + 7
 #pragma unroll
-  for (int i = 0; i < kMaxRows / 4; ++i) acc[i] = 0.0f;
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
   double mae = 0.0;
   int bad = 0;
   const int ntiles = (out + kTN - 1) / kTN;
@@ -130,57 +163,110 @@ __global__ void __launch_bounds__(kT) k_ae_dec(const __grid_constant__ AeArgs a)
     const int c0 = t * kTN;
     __syncthreads();
     load_y_tile(a, yt, c0);
-    for (int i = threadIdx.x; i < D * kTN; i += kT) {
+    for (int i = threadIdx.x; i < kMaxW * kTN; i += kT) {
       const int jj = i >> 5, c = i & 31;
-      wd[i] = c0 + c < out ? Wd[(long long)jj * out + c0 + c] : 0.0f;
+      const float w = (jj < D && c0 + c < out) ? Wd[(long long)jj * out + c0 + c] : 0.0f;
+      wd[i] = w;
+      wdT[c * kMaxW + jj] = w;
     }
     if (threadIdx.x < kTN) bd[threadIdx.x] = c0 + (int)threadIdx.x < out ? Bd[c0 + threadIdx.x] : 0.0f;
     __syncthreads();
-    {  // forward + loss + G: c = tid % 32, rows tid / 32 + 8 i
-      const int c = threadIdx.x & 31, rr = threadIdx.x >> 5;
-      for (int r = rr; r < n; r += 8) {
-        float gv = 0.0f;
-        if (c0 + c < out) {
-          float o = 0.0f;
-          for (int q = 0; q < D; ++q) o = fmaf(hs[r * D + q], wd[q * kTN + c], o);
-          o += bd[c];  // mlp.hpp:209-213
-          const double d = (double)o - (double)yt[r * kTN + c];
-          mae += fabs(d);
-          gv = d > 0 ? g1 : (d < 0 ? -g1 : 0.0f);
+    {  // (1) forward o = h Wd + b, loss, G: rows 4 ty .., columns 4 tx ..
+      float o[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[i][j] = 0.0f;
+#pragma unroll 4
+      for (int q = 0; q < kMaxW; ++q) {
+        if (q >= D) break;
+        const float4 h4 = *reinterpret_cast<const float4*>(hT + q * kMaxRows + 4 * ty);
+        const float4 w4 = *reinterpret_cast<const float4*>(wd + q * kTN + 4 * tx);
+        const float hv[4] = {h4.x, h4.y, h4.z, h4.w}, wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[i][j] = fmaf(hv[i], wv[j], o[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * ty + i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = 4 * tx + j;
+          float gv = 0.0f;
+          if (r < n && c0 + c < out) {
+            const float of = o[i][j] + bd[c];  // mlp.hpp:209-213
+            const double d = (double)of - (double)yt[r * kTN + c];
+            mae += fabs(d);
+            gv = d > 0 ? g1 : (d < 0 ? -g1 : 0.0f);
+          }
+          G[r * kTN + c] = gv;
+          GT[c * kMaxRows + r] = gv;
         }
-        G[r * (kTN + 1) + c] = gv;
       }
     }
     __syncthreads();
-    {  // dWd[:, tile] = h^T G (rows ascending), dbd = colsum G
-      const int c = threadIdx.x & 31, jg = threadIdx.x >> 5;
-      if (c0 + c < out) {
-        for (int jj = jg; jj < D; jj += 8) {
-          float s = 0.0f;
-          for (int r = 0; r < n; ++r) s = fmaf(hs[r * D + jj], G[r * (kTN + 1) + c], s);
-          dWd[(long long)jj * out + c0 + c] = s;
-          bad |= !isfinite(s);
+    {  // (2) dWd[:, tile] = h^T G (rows ascending): j 4 jg .., columns 2 cg ..
+      const int jg = threadIdx.x >> 4, cg = threadIdx.x & 15;
+      float dw[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+      float db[2] = {0.f, 0.f};
+#pragma unroll 4
+      for (int r = 0; r < kMaxRows; ++r) {
+        if (r >= n) break;
+        const float4 h4 = *reinterpret_cast<const float4*>(hs + r * kMaxW + 4 * jg);
+        const float2 g2 = *reinterpret_cast<const float2*>(G + r * kTN + 2 * cg);
+        const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          dw[i][0] = fmaf(hv[i], g2.x, dw[i][0]);
+          dw[i][1] = fmaf(hv[i], g2.y, dw[i][1]);
+        }
+        db[0] += g2.x;
+        db[1] += g2.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = 2 * cg + k;
+        if (c0 + c >= out) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int jj = 4 * jg + i;
+          if (jj < D) {
+            dWd[(long long)jj * out + c0 + c] = dw[i][k];
+            bad |= !isfinite(dw[i][k]);
+          }
         }
         if (jg == 0) {
-          float s = 0.0f;
-          for (int r = 0; r < n; ++r) s += G[r * (kTN + 1) + c];
-          dbd[c0 + c] = s;
-          bad |= !isfinite(s);
+          dbd[c0 + c] = db[k];
+          bad |= !isfinite(db[k]);
         }
       }
     }
-    if (j < D)  // dL/dh partial: G Wd^T over this tile's columns
-      for (int c = 0; c < kTN; ++c) {
-        const float w = wd[j * kTN + c];
+    // (3) dL/dh partial += G Wd^T over this tile's columns (columns ascending)
+#pragma unroll 4
+    for (int c = 0; c < kTN; ++c) {
+      const float4 g4 = *reinterpret_cast<const float4*>(GT + c * kMaxRows + 4 * ty);
+      const float4 w0 = *reinterpret_cast<const float4*>(wdT + c * kMaxW + 8 * tx);
+      const float4 w1 = *reinterpret_cast<const float4*>(wdT + c * kMaxW + 8 * tx + 4);
+      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-        for (int i = 0; i < kMaxRows / 4; ++i)
-          if (rg + 4 * i < n) acc[i] = fmaf(G[(rg + 4 * i) * (kTN + 1) + c], w, acc[i]);
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(gv[i], wv[j], acc[i][j]);
+    }
   }
-  if (j < D)
 #pragma unroll
-    for (int i = 0; i < kMaxRows / 4; ++i)
-      if (rg + 4 * i < n) a.Pg[((long long)blockIdx.x * n + rg + 4 * i) * D + j] = acc[i];
+  for (int i = 0; i < 4; ++i) {
+    const int r = 4 * ty + i;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jj = 8 * tx + j;
+      if (jj < D) a.Pg[((long long)blockIdx.x * n + r) * D + jj] = acc[i][j];
+    }
+  }
   const double tot = block_sum_det(mae, red);
   if (threadIdx.x == 0) a.mae_part[blockIdx.x] = tot;
   if (bad) atomicOr(&a.flags[1], 1);
@@ -236,15 +322,19 @@ __global__ void __launch_bounds__(512) k_ae_small_bwd(const __grid_constant__ Ae
   }
 }
 
-// K6: dWe0[tile, :] = y[:, tile]^T gz0 (rows ascending)
+// K6: dWe0[tile, :] = y[:, tile]^T gz0 (rows ascending). Thread (cg, eg)
+// owns columns 2 cg .. + 1 and features 4 eg .. + 3 of the tile.
 __global__ void __launch_bounds__(kT) k_ae_encw(const __grid_constant__ AeArgs a) {
   float* sm = smem();
   const int n = a.n, E1 = a.m.E1, out = a.m.out;
-  float* gz = sm;                     // [rows x E1]
-  float* yt = gz + kMaxRows * kMaxW;  // [rows x 32]
+  float* gz = sm;                     // [128 rows x 64]
+  float* yt = gz + kMaxRows * kMaxW;  // [128 rows x 32]
   float* dWe = a.genc + a.m.enc_wide_w;
-  for (int i = threadIdx.x; i < n * E1; i += kT) gz[i] = a.gz0[i];
-  const int e = threadIdx.x & 63, cg = threadIdx.x >> 6;
+  for (int i = threadIdx.x; i < kMaxRows * kMaxW; i += kT) {
+    const int r = i >> 6, e = i & 63;
+    gz[i] = (r < n && e < E1) ? a.gz0[r * E1 + e] : 0.0f;
+  }
+  const int cg = threadIdx.x >> 4, eg = threadIdx.x & 15;
   int bad = 0;
   const int ntiles = (out + kTN - 1) / kTN;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -252,14 +342,32 @@ __global__ void __launch_bounds__(kT) k_ae_encw(const __grid_constant__ AeArgs a
     __syncthreads();
     load_y_tile(a, yt, c0);
     __syncthreads();
-    if (e < E1)
-      for (int c = cg; c < kTN; c += 4) {
-        if (c0 + c >= out) break;
-        float s = 0.0f;
-        for (int r = 0; r < n; ++r) s = fmaf(yt[r * kTN + c], gz[r * E1 + e], s);
-        dWe[(long long)(c0 + c) * E1 + e] = s;
-        bad |= !isfinite(s);
+    float dw[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll 4
+    for (int r = 0; r < kMaxRows; ++r) {
+      if (r >= n) break;
+      const float2 y2 = *reinterpret_cast<const float2*>(yt + r * kTN + 2 * cg);
+      const float4 g4 = *reinterpret_cast<const float4*>(gz + r * kMaxW + 4 * eg);
+      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        dw[0][e] = fmaf(y2.x, gv[e], dw[0][e]);
+        dw[1][e] = fmaf(y2.y, gv[e], dw[1][e]);
       }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int c = 2 * cg + k;
+      if (c0 + c >= out) continue;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int ee = 4 * eg + e;
+        if (ee < E1) {
+          dWe[(long long)(c0 + c) * E1 + ee] = dw[k][e];
+          bad |= !isfinite(dw[k][e]);
+        }
+      }
+    }
   }
   if (bad) atomicOr(&a.flags[0], 1);
 }
@@ -291,8 +399,8 @@ bool ae_supported(const ModelArgs& m, int rows) {
 void launch_ae_passes(const AeArgs& a, cudaStream_t s) {
   static bool attr = false;
   const int sm_enc = (ae::kMaxRows * ae::kTN + ae::kTN * ae::kMaxW) * 4;
-  const int sm_dec = (ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN + ae::kMaxW * ae::kTN +
-                      ae::kMaxRows * (ae::kTN + 1) + ae::kTN) *
+  const int sm_dec = (2 * ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN + 2 * ae::kMaxW * ae::kTN +
+                      2 * ae::kMaxRows * ae::kTN + ae::kTN) *
                      4;
   const int sm_encw = (ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN) * 4;
   if (!attr) {

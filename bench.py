@@ -420,7 +420,8 @@ def main():
                    "tournament_rows": int(my_tour.size), "interval": args.interval,
                    "parallelism": f"ltfb{k} (one trainer per GPU, NCCL pairwise exchange)",
                    "l2": "inputs larger than L2: each step gathers random rows of a "
-                         f"{my_train.size * out_pad * 4 / 1e9:.2f} GB HBM store",
+                         f"{my_train.size * out_pad * 4 / 1e9:.2f} GB HBM store; the frozen wide-layer "
+                         "weights (model state, not inputs) sit in an L2 persistence window",
                    "wide_kernel": {1: "generic SIMT fp32", 2: "tcgen05 3xTF32"}.get(kind, str(kind)),
                    "wide_ctas": ctas},
         "round_ms": round_ms, "rounds_timed": len(rounds_ms),

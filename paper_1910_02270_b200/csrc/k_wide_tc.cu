@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
   unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kStages], split_done[kStages], sready[kStages], empty[kStages];
   __shared__ uint64_t yfull[kYStages];
-  __shared__ uint64_t ofull[2], oempty[2], h_ready, done;
+  __shared__ uint64_t ofull[2], oempty[2], h_ready, done, rbar;
   __shared__ uint32_t tmem_base;
   __shared__ double red[128];
 
@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     }
     tc::mbar_init(&h_ready, 128);
     tc::mbar_init(&done, 1);
+    tc::mbar_init(&rbar, 1);
     tc::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -466,25 +467,45 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     const int G = kThreads / kMaxQ;                // 10 groups
     const int g = threadIdx.x / kMaxQ, o = threadIdx.x % kMaxQ;
     const long long pstride4 = (long long)a.B * kW / 4;
+    // every partial's slice [lo, hi) arrives by one or two bulk copies (TMA
+    // engine, one per source CTA, issued by 148 threads) into shared memory:
+    // far cheaper than 16 dependent-free LDG.128 per thread through L1
+    float4* stage = reinterpret_cast<float4*>(sm + 8192);  // [S][kMaxQ]
+    const int e0 = lo, e1 = min(hi, q_enc), d0 = max(lo, q_enc), d1 = hi;
+    const int ne = max(0, e1 - e0), nd = max(0, d1 - d0);
+    if (threadIdx.x == 0 && nq > 0) tc::mbar_expect_tx(&rbar, (uint32_t)(a.S * nq * 16));
+    __syncthreads();
+    if ((int)threadIdx.x < a.S && nq > 0) {
+      const int sidx = threadIdx.x;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const uint32_t dst = tc::smem_u32(stage + sidx * kMaxQ);
+      const float4* pe4 = reinterpret_cast<const float4*>(a.P_enc) + sidx * pstride4;
+      const float4* pd4 = reinterpret_cast<const float4*>(a.P_dec) + sidx * pstride4;
+      if (ne > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "l"(pe4 + e0), "r"(ne * 16), "r"(tc::smem_u32(&rbar))
+            : "memory");
+      if (nd > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                dst + 16u * (uint32_t)ne),
+            "l"(pd4 + (d0 - q_enc)), "r"(nd * 16), "r"(tc::smem_u32(&rbar))
+            : "memory");
+    }
+    if (nq > 0) tc::mbar_wait(&rbar, 0);
     float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (o < nq) {
-      const int q = lo + o;
-      const bool enc = q < q_enc;
-      const float4* src = reinterpret_cast<const float4*>(enc ? a.P_enc : a.P_dec) + (enc ? q : q - q_enc);
       constexpr int kMaxPer = 16;  // ceil(148 / 10)
-      float4 v[kMaxPer];
 #pragma unroll
       for (int u = 0; u < kMaxPer; ++u) {
         const int sidx = g + u * G;
-        v[u] = sidx < a.S ? __ldcg(src + sidx * pstride4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-#pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        if (g + u * G < a.S) {
-          acc.x += v[u].x;
-          acc.y += v[u].y;
-          acc.z += v[u].z;
-          acc.w += v[u].w;
+        if (sidx < a.S) {
+          const float4 v = stage[sidx * kMaxQ + o];
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
         }
       }
     }

@@ -281,8 +281,57 @@ __device__ __noinline__ void wnet_bwd(const NetS& n, int nrw, int gin0, int epiA
 /// (nn/mlp.hpp:274-277): pgW[k][j] = sum_r below[r][k] dz[r][j], pgb[j] =
 /// sum_r dz[r][j], one pass over the item space of all layers. Row k == IN
 /// of a layer is its bias (below == 1, fmaf(1, d, acc) == acc + d).
+/// Layers with a 4-aligned input width: thread (k-group, j) owns the four
+/// weight gradients dW[4 kg .. 4 kg + 3][j]; per row one float4 of the layer
+/// input (a warp broadcast) and one dz feed 4 FMAs, rows ascending as in the
+/// reference (nn/mlp.hpp:274-277). Bias gradients by the k-group past IN.
+__device__ __forceinline__ void pg_layer4(const NetS& n, int l, int below, int R, int pg) {
+  float* s = S();
+  const int IN = n.w[l], OUT = n.w[l + 1];
+  const int nkg = IN / 4 + 1;  // + the bias group
+  const int items = nkg * OUT;
+  const float* d0 = s + n.dz[l];
+  const int pgW = pg + n.woff[l], pgb = pg + n.boff[l];
+  for (int t = threadIdx.x; t < items; t += kThreads) {
+    const int kg = t / OUT, j = t - kg * OUT;
+    const float* d = d0 + j;
+    if (kg < IN / 4) {
+      const float4* b4 = reinterpret_cast<const float4*>(s + below) + kg;
+      const int bstride = IN / 4;
+      float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+#pragma unroll 4
+      for (int r = 0; r < R; ++r) {
+        const float dv = d[r * OUT];
+        const float4 bv = b4[r * bstride];
+        a0 = fmaf(bv.x, dv, a0);
+        a1 = fmaf(bv.y, dv, a1);
+        a2 = fmaf(bv.z, dv, a2);
+        a3 = fmaf(bv.w, dv, a3);
+      }
+      float* dw = s + pgW + 4 * kg * OUT + j;
+      dw[0] = a0;
+      dw[OUT] = a1;
+      dw[2 * OUT] = a2;
+      dw[3 * OUT] = a3;
+    } else {
+      float a0 = 0.0f;
+#pragma unroll 4
+      for (int r = 0; r < R; ++r) a0 += d[r * OUT];
+      s[pgb + j] = a0;
+    }
+  }
+}
+
 __device__ __noinline__ void pg_net(const NetS& n, int x, int R, int pg) {
   float* s = S();
+  {
+    bool all4 = true;
+    for (int l = 0; l < n.L; ++l) all4 = all4 && (n.w[l] % 4 == 0);
+    if (all4) {  // one pass per layer, float4 operands (no barrier needed: disjoint outputs)
+      for (int l = 0; l < n.L; ++l) pg_layer4(n, l, l == 0 ? x : n.a[l - 1], R, pg);
+      return;
+    }
+  }
   int base = 0;
   int start[kMaxL + 1];
   for (int l = 0; l < n.L; ++l) {

@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--wide-kernel", type=int, default=0)
+    p.add_argument("--host-data", action="store_true",
+                   help="generate the partition on the host and upload it (default: k_synth on the device)")
     return p.parse_args()
 
 
@@ -260,9 +262,13 @@ def main():
     _, train_parts, tour_parts = L.split_dataset(total, k, 0.05, 0.05, seed, k >= 2)
     my_train, my_tour = train_parts[rank], tour_parts[rank]
     t0 = time.perf_counter()
-    need = np.concatenate([my_train, my_tour]).astype(np.uint32)
-    x, y = L.synth_generate_ids(dims, need, total, sampling_seed=1, spec_seed=1)
-    ds = L.SparseDataset(dims, need, x, y, total)
+    if args.host_data:
+        need = np.concatenate([my_train, my_tour]).astype(np.uint32)
+        x, y = L.synth_generate_ids(dims, need, total, sampling_seed=1, spec_seed=1)
+        ds = L.SparseDataset(dims, need, x, y, total)
+    else:  # rendered straight into the HBM store by the Trainer (k_synth)
+        ds = L.SynthDataset(dims, total, sampling_seed=1, spec_seed=1)
+        x = y = None
     gen_s = time.perf_counter() - t0
 
     base = L.make_cyclegan(dims, arch, L.mix_seed(seed, 0xAE0))
@@ -437,7 +443,8 @@ def main():
                         "(copy stream, double-buffered) -> step kernels -> D2H step record"},
         "gpu_launches": launches,
         "clocks": clocks,
-        "setup_s": {"generate": round(gen_s, 2), "preload": round(load_s, 2)},
+        "setup_s": {"generate": round(gen_s, 2), "preload": round(load_s, 2),
+                    "store": "host generator + upload" if args.host_data else "device generator (k_synth)"},
     }
     print(json.dumps(line))
     if dist is not None:

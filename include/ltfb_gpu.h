@@ -130,6 +130,17 @@ int ltfb_trainer_get_adam(ltfb_trainer* t, int net, float* m, float* v, uint64_t
  * owner (optional, may be NULL) is the owning shard per slot. */
 int ltfb_trainer_load_store(ltfb_trainer* t, const uint32_t* ids, uint64_t n, const float* x,
                             const float* y, const int32_t* owner);
+/* ltfb_trainer_load_store with the partition rendered on the device by the
+ * synthetic generator (generator.hpp:41-206; sample ids[i] of a total_n-point
+ * sweep, noise_level must be 0) instead of uploaded: a large partition never
+ * exists on the host. Outputs within 1 fp32 ulp of ltfb_synth_generate_ids. */
+int ltfb_trainer_generate_store(ltfb_trainer* t, const uint32_t* ids, uint64_t n, const int32_t* owner,
+                                uint64_t spec_seed, double noise_level, uint64_t sampling_seed,
+                                uint64_t total_n);
+/* ltfb_trainer_set_slice with the slice rendered on the device. */
+int ltfb_trainer_generate_slice(ltfb_trainer* t, int which, const uint32_t* ids, uint64_t rows,
+                                uint64_t spec_seed, double noise_level, uint64_t sampling_seed,
+                                uint64_t total_n);
 /* assemble_tensors of the tournament / validation slice (trainer.hpp:74-78,
  * runner.hpp:318) made resident in HBM. */
 int ltfb_trainer_set_slice(ltfb_trainer* t, int which, const float* x, const float* y, uint64_t rows);
@@ -249,6 +260,13 @@ int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_
 int ltfb_synth_generate_ids(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
                             const uint32_t* ids, uint64_t n, uint64_t total_n, uint64_t sampling_seed,
                             float* x, float* y, int threads);
+/* ltfb_synth_generate_ids on the device: x_dev [n x 5] and y_dev [n x
+ * y_stride] are device pointers on `device` (ids may be NULL: rows first..);
+ * returns after the rows are written. */
+int ltfb_synth_generate_device(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                               const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
+                               uint64_t sampling_seed, float* x_dev, float* y_dev, uint64_t y_stride,
+                               int device);
 /* make_cyclegan blob init (model.hpp:96-132, mlp.hpp:235-244) */
 int ltfb_init_params(const ltfb_dims* dims, const ltfb_arch* arch, uint64_t seed, int net,
                      float* blob, uint64_t count);

@@ -7,7 +7,7 @@ tournament API on top of that ABI.
 """
 from ._lib import (CapacityError, ConfigError, ContractError, CudaError, DimensionError, Error,
                    IoError, NumericError, StoreCorruptError, LIB_PATH)
-from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrain_autoencoder, CycleGan, Dataset, SparseDataset, synth_generate_ids, EpochRecord, EvalMetric, EvalRecord, HistorySegment,
+from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrain_autoencoder, CycleGan, Dataset, SparseDataset, SynthDataset, synth_generate_device, synth_generate_ids, EpochRecord, EvalMetric, EvalRecord, HistorySegment,
                   Matching, ModalityDims, RoundRecord, RoundResult, StepRecord, SurrogateArch,
                   Trainer, TrainerConfig, TrainerRoundRecord, TransferRecord, device_count,
                   epoch_permutation, fnv1a64, hex64, incoming_wins, layer_widths, make_cyclegan,

@@ -101,6 +101,7 @@ EXPORTS = (
     "ltfb_trainer_create", "ltfb_trainer_destroy", "ltfb_trainer_param_count",
     "ltfb_trainer_set_params", "ltfb_trainer_get_params", "ltfb_trainer_set_adam",
     "ltfb_trainer_get_adam", "ltfb_trainer_load_store", "ltfb_trainer_set_slice",
+    "ltfb_trainer_generate_store", "ltfb_trainer_generate_slice", "ltfb_synth_generate_device",
     "ltfb_trainer_train_steps", "ltfb_trainer_step", "ltfb_trainer_take_epochs",
     "ltfb_trainer_flush_epoch", "ltfb_trainer_evaluate", "ltfb_trainer_generator_floats",
     "ltfb_trainer_get_generator", "ltfb_trainer_set_incoming", "ltfb_trainer_copy_incoming",
@@ -153,6 +154,10 @@ _sig("ltfb_trainer_set_adam", C.c_int, P, C.c_int, P, P, C.c_uint64)
 _sig("ltfb_trainer_get_adam", C.c_int, P, C.c_int, P, P, C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_load_store", C.c_int, P, u32p, C.c_uint64, f32p, f32p, P)
 _sig("ltfb_trainer_set_slice", C.c_int, P, C.c_int, f32p, f32p, C.c_uint64)
+_sig("ltfb_trainer_generate_store", C.c_int, P, u32p, C.c_uint64, P, C.c_uint64, C.c_double, C.c_uint64,
+     C.c_uint64)
+_sig("ltfb_trainer_generate_slice", C.c_int, P, C.c_int, u32p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+     C.c_uint64)
 _sig("ltfb_trainer_train_steps", C.c_int, P, C.c_uint64, C.POINTER(StepRecordC), C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_step", C.c_int, P, C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_take_epochs", C.c_int, P, C.POINTER(EpochRecordC), C.c_uint64, C.POINTER(C.c_uint64))
@@ -193,6 +198,8 @@ _sig("ltfb_epoch_permutation", C.c_int, u32p, C.c_uint64, C.c_uint32, C.c_uint64
 _sig("ltfb_incoming_wins", C.c_int, C.c_double, C.c_double)
 _sig("ltfb_synth_generate", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, C.c_uint64, C.c_uint64,
      C.c_uint64, C.c_uint64, f32p, f32p, C.c_int)
+_sig("ltfb_synth_generate_device", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, P, C.c_uint64,
+     C.c_uint64, C.c_uint64, C.c_uint64, P, P, C.c_uint64, C.c_int)
 _sig("ltfb_init_params", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_uint64, C.c_int, f32p, C.c_uint64)
 _sig("ltfb_net_param_count", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_int, C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_synchronize", C.c_int, P)

@@ -349,6 +349,50 @@ class SparseDataset(Dataset):
         return self.x[sel], self.y[sel]
 
 
+class SynthDataset(Dataset):
+    """A `total`-point synthetic sweep (generate_dataset, generator.hpp:195-206)
+    that is never materialised on the host: a Trainer renders its partition
+    and tournament slice straight into HBM with the device generator
+    (k_synth.cu). `rows()` (small host-side reads: validation, e2e inputs)
+    runs the host generator."""
+
+    device_generated = True
+
+    def __init__(self, dims: ModalityDims, total: int, sampling_seed: int = 1, spec_seed: int = 1,
+                 noise_level: float = 0.0, samples_per_file: int = 500):
+        if noise_level != 0.0:
+            raise ContractError("SynthDataset: the device generator needs noise_level 0")
+        self.dims = dims
+        self.total = int(total)
+        self.sampling_seed, self.spec_seed, self.noise_level = int(sampling_seed), int(spec_seed), noise_level
+        self.samples_per_file = int(samples_per_file)
+
+    def rows(self, ids):
+        return synth_generate_ids(self.dims, ids, self.total, self.sampling_seed, self.spec_seed,
+                                  self.noise_level)
+
+
+def synth_generate_device(dims: ModalityDims, n: int, total: int | None = None, ids=None, first: int = 0,
+                          sampling_seed: int = 1, spec_seed: int = 1, device: int = 0):
+    """synth_generate(_ids) rendered on GPU `device`; returns torch tensors
+    (x [n, 5], y [n, output_dim]) on that device."""
+    import torch
+    total = n if total is None else int(total)
+    dev = torch.device("cuda", device)
+    x = torch.empty((n, dims.input_dim), dtype=torch.float32, device=dev)
+    y = torch.empty((n, dims.output_dim()), dtype=torch.float32, device=dev)
+    idp = None
+    if ids is not None:
+        ids = np.ascontiguousarray(ids, np.uint32)
+        if ids.size != n:
+            raise ContractError("synth_generate_device: ids length must equal n")
+        idp = ids.ctypes.data
+    dc = dims.c()
+    check(lib.ltfb_synth_generate_device(C.byref(dc), spec_seed, 0.0, idp, first, n, total, sampling_seed,
+                                         x.data_ptr(), y.data_ptr(), dims.output_dim(), device))
+    return x, y
+
+
 def synthetic_dataset(dims: ModalityDims, n: int, sampling_seed: int = 1, spec_seed: int = 1,
                       noise_level: float = 0.0, samples_per_file: int = 500) -> Dataset:
     x, y = synth_generate(dims, n, sampling_seed, spec_seed, noise_level)
@@ -514,17 +558,27 @@ class Trainer:
         used = np.unique(files)  # file order
         loader = {int(f): i % cfg.n_shards for i, f in enumerate(used)}
         owner = np.array([loader[int(f)] for f in files], np.int32)
-        x, y = dataset.rows(ids)
-        check(lib.ltfb_trainer_load_store(self._h, ids, ids.size, np.ascontiguousarray(x),
-                                          np.ascontiguousarray(y), ptr(owner)))
+        gen = getattr(dataset, "device_generated", False)
+        if gen:
+            check(lib.ltfb_trainer_generate_store(self._h, ids, ids.size, ptr(owner), dataset.spec_seed,
+                                                  dataset.noise_level, dataset.sampling_seed, dataset.total))
+        else:
+            x, y = dataset.rows(ids)
+            check(lib.ltfb_trainer_load_store(self._h, ids, ids.size, np.ascontiguousarray(x),
+                                              np.ascontiguousarray(y), ptr(owner)))
         preload_s = time.perf_counter() - t0
         self._segment.epochs.append(EpochRecord(cfg.trainer_id, 0, 0, len(used), required, 0, preload_s))
         tids = np.ascontiguousarray(cfg.tournament_ids, np.uint32)
         self._has_tour = tids.size > 0
         if self._has_tour:
-            tx, ty = dataset.rows(tids)
-            check(lib.ltfb_trainer_set_slice(self._h, 0, np.ascontiguousarray(tx), np.ascontiguousarray(ty),
-                                             tids.size))
+            if gen:
+                check(lib.ltfb_trainer_generate_slice(self._h, 0, tids, tids.size, dataset.spec_seed,
+                                                      dataset.noise_level, dataset.sampling_seed,
+                                                      dataset.total))
+            else:
+                tx, ty = dataset.rows(tids)
+                check(lib.ltfb_trainer_set_slice(self._h, 0, np.ascontiguousarray(tx),
+                                                 np.ascontiguousarray(ty), tids.size))
         self._val_key = None
 
     def __del__(self):
@@ -666,9 +720,14 @@ class Trainer:
 
     def set_validation(self, ids: np.ndarray):
         ids = np.ascontiguousarray(ids, np.uint32)
-        x, y = self.dataset.rows(ids)
-        check(lib.ltfb_trainer_set_slice(self._h, 1, np.ascontiguousarray(x), np.ascontiguousarray(y),
-                                         ids.size))
+        d = self.dataset
+        if getattr(d, "device_generated", False):
+            check(lib.ltfb_trainer_generate_slice(self._h, 1, ids, ids.size, d.spec_seed, d.noise_level,
+                                                  d.sampling_seed, d.total))
+        else:
+            x, y = d.rows(ids)
+            check(lib.ltfb_trainer_set_slice(self._h, 1, np.ascontiguousarray(x), np.ascontiguousarray(y),
+                                             ids.size))
         self._val_key = ids.size
 
     def evaluate_validation(self, w_f: float = 1.0, w_i: float = 1.0, candidate=None) -> EvalMetric:

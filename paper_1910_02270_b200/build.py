@@ -24,6 +24,11 @@ FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3",
                 "-I" + os.path.join(REPO, "include"), "-I" + CSRC]
 
 
+# per-file extras: the device synthetic generator keeps the host generator's
+# double evaluation order (no FMA contraction), see k_synth.cu
+FILE_FLAGS = {"k_synth.cu": ["-fmad=false"]}
+
+
 def _headers():
     hs = []
     for d in (CSRC, os.path.join(REPO, "include"), os.path.join(REPO, "include", "ltfb_b200")):
@@ -38,7 +43,7 @@ def sources():
 
 
 def _compile(src, obj, log):
-    cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+    cmd = [NVCC] + FLAGS + FILE_FLAGS.get(os.path.basename(src), []) + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

@@ -259,6 +259,21 @@ int ltfb_trainer_set_slice(ltfb_trainer* t, int which, const float* x, const flo
   });
 }
 
+int ltfb_trainer_generate_store(ltfb_trainer* t, const uint32_t* ids, uint64_t n, const int32_t* owner,
+                                uint64_t spec_seed, double noise_level, uint64_t sampling_seed,
+                                uint64_t total_n) {
+  return guarded([&] { T(t).generate_store(ids, n, owner, spec_seed, noise_level, sampling_seed, total_n); });
+}
+
+int ltfb_trainer_generate_slice(ltfb_trainer* t, int which, const uint32_t* ids, uint64_t rows,
+                                uint64_t spec_seed, double noise_level, uint64_t sampling_seed,
+                                uint64_t total_n) {
+  return guarded([&] {
+    if (which != 0 && which != 1) throw ltfb::ContractError("bad slice index");
+    T(t).generate_slice(which, ids, rows, spec_seed, noise_level, sampling_seed, total_n);
+  });
+}
+
 int ltfb_trainer_train_steps(ltfb_trainer* t, uint64_t n, ltfb_step_record* out, uint64_t* n_out) {
   bool ok = true;
   std::vector<ltfb::train::StepRecord> recs;
@@ -648,6 +663,25 @@ int ltfb_synth_generate(const ltfb_dims* dims, uint64_t spec_seed, double noise_
                         uint64_t n, uint64_t total_n, uint64_t sampling_seed, float* x, float* y,
                         int threads) {
   return synth_rows(dims, spec_seed, noise_level, nullptr, first, n, total_n, sampling_seed, x, y, threads);
+}
+
+int ltfb_synth_generate_device(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                               const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
+                               uint64_t sampling_seed, float* x_dev, float* y_dev, uint64_t y_stride,
+                               int device) {
+  return guarded([&] {
+    ltfb_b200::DeviceGuard g(device);
+    cudaStream_t s = nullptr;
+    LTFB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+      ltfb_dev::synth_generate_device(dims_of(dims), spec_seed, noise_level, ids, first, n, total_n,
+                                      sampling_seed, x_dev, y_dev, static_cast<long long>(y_stride), s);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    LTFB_CUDA(cudaStreamDestroy(s));
+  });
 }
 
 int ltfb_net_param_count(const ltfb_dims* dims, const ltfb_arch* arch, int net, uint64_t* count) {

@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "step_args.cuh"
 
 namespace ltfb_dev {
@@ -106,5 +108,31 @@ cudaError_t selftest_tc(const float* a1, const float* b1, const float* ah, const
 /// k_eval_small, then the forward-MAE pass (tcgen05 when tc != nullptr,
 /// else the SIMT k_eval_wide), then k_eval_finalize.
 void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc = nullptr, bool precise = true);
+
+/// Device synthetic generator (k_synth.cu; synth/generator.hpp:41-206).
+struct SynthArgs {
+  const std::uint32_t* ids;   // global sample ids per row (nullptr: first + row)
+  std::uint64_t first;
+  const double* coeffs;       // [S x 31] per-spec tables (SynthGenerator)
+  const double* gain;         // [V x C]
+  const double* wavelength;   // [C]
+  int S, V, C, H, W;
+  unsigned g;                 // grid_side(total_n)
+  std::uint64_t sampling_seed;
+  float* x;                   // [n x 5]
+  float* y;                   // [n x y_stride]
+  long long y_stride;
+};
+void launch_synth(const SynthArgs& a, long long n, cudaStream_t s);
+}  // namespace ltfb_dev
+namespace ltfb::surrogate { struct ModalityDims; }
+namespace ltfb_dev {
+/// Rows ids[i] (or first + i when ids is null) of a total_n-point sweep into
+/// device x [n x 5] / y [n x y_stride]; the per-spec tables come from the
+/// host SynthGenerator. Synchronous on `s`.
+void synth_generate_device(const ltfb::surrogate::ModalityDims& dims, std::uint64_t spec_seed,
+                           double noise_level, const std::uint32_t* ids, std::uint64_t first,
+                           std::size_t n, std::uint64_t total_n, std::uint64_t sampling_seed, float* x,
+                           float* y, long long y_stride, cudaStream_t s);
 
 }  // namespace ltfb_dev

@@ -375,11 +375,9 @@ void DeviceTrainer::get_adam(int net, float* m, float* v, std::uint64_t* t) {
 }
 
 // ------------------------------------------------------------------ data --
-void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const float* x,
-                               const float* y, const std::int32_t* owner) {
+void DeviceTrainer::begin_store(const std::uint32_t* ids, std::size_t n, const std::int32_t* owner) {
   h_ready_ = false;
   if (n == 0) throw ContractError("plan_epoch: empty partition");
-  DeviceGuard g(spec_.device);
   const auto& m = margs_;
   part_ids_.assign(ids, ids + n);
   owner_.assign(n, 0);
@@ -387,14 +385,9 @@ void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const fl
   n_part_ = n;
   sx_.alloc(n * m.in);
   sy_.alloc(n * m.out_pad);
-  LTFB_CUDA(cudaMemcpyAsync(sx_.p, x, n * m.in * 4, cudaMemcpyHostToDevice, stream_));
-  if (m.out_pad == m.out) {
-    LTFB_CUDA(cudaMemcpyAsync(sy_.p, y, n * m.out * 4, cudaMemcpyHostToDevice, stream_));
-  } else {
-    LTFB_CUDA(cudaMemsetAsync(sy_.p, 0, sy_.bytes(), stream_));
-    LTFB_CUDA(cudaMemcpy2DAsync(sy_.p, m.out_pad * 4, y, m.out * 4, m.out * 4, n,
-                                cudaMemcpyHostToDevice, stream_));
-  }
+}
+
+void DeviceTrainer::finish_store(std::size_t n) {
   for (int i = 0; i < 2; ++i) {
     perm_[i].alloc(n);
     if (pinned_perm_[i]) cudaFreeHost(pinned_perm_[i]);
@@ -412,9 +405,34 @@ void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const fl
   LTFB_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void DeviceTrainer::generate_store(const std::uint32_t*, std::size_t, std::uint64_t, std::uint64_t,
-                                   std::uint64_t) {
-  throw ContractError("generate_store: device generator not available in this build");
+void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const float* x,
+                               const float* y, const std::int32_t* owner) {
+  DeviceGuard g(spec_.device);
+  begin_store(ids, n, owner);
+  const auto& m = margs_;
+  LTFB_CUDA(cudaMemcpyAsync(sx_.p, x, n * m.in * 4, cudaMemcpyHostToDevice, stream_));
+  if (m.out_pad == m.out) {
+    LTFB_CUDA(cudaMemcpyAsync(sy_.p, y, n * m.out * 4, cudaMemcpyHostToDevice, stream_));
+  } else {
+    LTFB_CUDA(cudaMemsetAsync(sy_.p, 0, sy_.bytes(), stream_));
+    LTFB_CUDA(cudaMemcpy2DAsync(sy_.p, m.out_pad * 4, y, m.out * 4, m.out * 4, n,
+                                cudaMemcpyHostToDevice, stream_));
+  }
+  finish_store(n);
+}
+
+void DeviceTrainer::generate_store(const std::uint32_t* ids, std::size_t n, const std::int32_t* owner,
+                                   std::uint64_t spec_seed, double noise_level,
+                                   std::uint64_t sampling_seed, std::uint64_t total_n) {
+  DeviceGuard g(spec_.device);
+  for (std::size_t i = 0; i < n; ++i)
+    if (ids[i] >= total_n) throw ContractError("DataStore: partition id outside dataset");
+  begin_store(ids, n, owner);
+  const auto& m = margs_;
+  if (m.out_pad != m.out) LTFB_CUDA(cudaMemsetAsync(sy_.p, 0, sy_.bytes(), stream_));
+  ltfb_dev::synth_generate_device(spec_.dims, spec_seed, noise_level, ids, 0, n, total_n, sampling_seed,
+                                  sx_.p, sy_.p, m.out_pad, stream_);
+  finish_store(n);
 }
 
 void DeviceTrainer::set_slice(int which, const float* x, const float* y, std::size_t rows) {
@@ -430,6 +448,31 @@ void DeviceTrainer::set_slice(int which, const float* x, const float* y, std::si
     LTFB_CUDA(cudaMemcpy2DAsync(by.p, m.out_pad * 4, y, m.out * 4, m.out * 4, rows,
                                 cudaMemcpyHostToDevice, stream_));
   }
+  finish_slice(which, rows);
+}
+
+void DeviceTrainer::generate_slice(int which, const std::uint32_t* ids, std::size_t rows,
+                                   std::uint64_t spec_seed, double noise_level, std::uint64_t sampling_seed,
+                                   std::uint64_t total_n) {
+  DeviceGuard g(spec_.device);
+  for (std::size_t i = 0; i < rows; ++i)
+    if (ids[i] >= total_n) throw ContractError("slice id outside dataset");
+  const auto& m = margs_;
+  DevBuf<float>& bx = which == 0 ? tx_ : vx_;
+  DevBuf<float>& by = which == 0 ? ty_ : vy_;
+  bx.alloc(rows * m.in);
+  by.alloc(rows * m.out_pad);
+  if (rows) {
+    LTFB_CUDA(cudaMemsetAsync(by.p, 0, by.bytes(), stream_));
+    ltfb_dev::synth_generate_device(spec_.dims, spec_seed, noise_level, ids, 0, rows, total_n, sampling_seed,
+                                    bx.p, by.p, m.out_pad, stream_);
+  }
+  finish_slice(which, rows);
+}
+
+void DeviceTrainer::finish_slice(int which, std::size_t rows) {
+  const auto& m = margs_;
+  DevBuf<float>& by = which == 0 ? ty_ : vy_;
   (which == 0 ? tour_rows_ : val_rows_) = rows;
   // tcgen05 eval maps over this slice (weights: the wide pass's K-major copy)
   eval_tc_[which].ready = false;

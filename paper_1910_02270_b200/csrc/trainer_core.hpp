@@ -101,10 +101,15 @@ class DeviceTrainer {
   /// (optional) is the owning shard per slot for shuffle accounting.
   void load_store(const std::uint32_t* ids, std::size_t n, const float* x, const float* y,
                   const std::int32_t* owner = nullptr);
-  /// Device-generated partition (synthetic generator on the GPU).
-  void generate_store(const std::uint32_t* ids, std::size_t n, std::uint64_t spec_seed,
-                      std::uint64_t sampling_seed, std::uint64_t total_n);
+  /// load_store with the partition rendered on the device by the synthetic
+  /// generator (rows ids[i] of a total_n-point sweep; k_synth.cu).
+  void generate_store(const std::uint32_t* ids, std::size_t n, const std::int32_t* owner,
+                      std::uint64_t spec_seed, double noise_level, std::uint64_t sampling_seed,
+                      std::uint64_t total_n);
   void set_slice(int which, const float* x, const float* y, std::size_t rows);  // 0 tour, 1 val
+  /// set_slice with the slice rendered on the device.
+  void generate_slice(int which, const std::uint32_t* ids, std::size_t rows, std::uint64_t spec_seed,
+                      double noise_level, std::uint64_t sampling_seed, std::uint64_t total_n);
   std::size_t slice_rows(int which) const { return which == 0 ? tour_rows_ : val_rows_; }
 
   // ---- training ----
@@ -209,6 +214,9 @@ class DeviceTrainer {
   DevBuf<float> gen_;       // [fwd | inv] contiguous (exchange payload)
   DevBuf<float> incoming_;  // [fwd | inv] of an incoming generator
   DevBuf<float> sx_, sy_;
+  void begin_store(const std::uint32_t* ids, std::size_t n, const std::int32_t* owner);
+  void finish_store(std::size_t n);
+  void finish_slice(int which, std::size_t rows);
   DevBuf<unsigned> perm_[2];
   DevBuf<float> xb_, yb_, pe_, pd_, scratch_;
   // tcgen05 wide pass: K-major fp32 copies of the frozen wide-layer weights + bias

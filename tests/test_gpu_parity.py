@@ -468,3 +468,74 @@ def test_split_and_sequential_post_kernels_agree():
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
+
+
+def _ulp_diff(a, b):
+    """fp32 distance in units in the last place (sign-magnitude aware)."""
+    ia = np.ascontiguousarray(a, np.float32).view(np.int32).astype(np.int64)
+    ib = np.ascontiguousarray(b, np.float32).view(np.int32).astype(np.int64)
+    ia = np.where(ia < 0, np.int64(-2**31) - ia, ia)
+    ib = np.where(ib < 0, np.int64(-2**31) - ib, ib)
+    return np.abs(ia - ib)
+
+
+@pytest.mark.parametrize("dims,n,total", [(TINY, 300, 300), (DESK, 600, 20000), (PAPER, 24, 100000)])
+def test_device_synth_matches_host(dims, n, total):
+    """k_synth (the generator on the GPU) vs the host generator that the
+    golden vectors pin (synth/generator.hpp:41-206): inputs bit-exact (the
+    sweep point is integer RNG + exact arithmetic), outputs within 1 fp32 ulp
+    (device libm exp/sin/cos vs glibc); almost all outputs identical."""
+    rng = np.random.default_rng(3)
+    ids = np.sort(rng.choice(total, n, replace=False)).astype(np.uint32)
+    hx, hy = L.synth_generate_ids(dims, ids, total, sampling_seed=5, spec_seed=2)
+    dx, dy = L.synth_generate_device(dims, n, total, ids=ids, sampling_seed=5, spec_seed=2)
+    dx, dy = dx.cpu().numpy(), dy.cpu().numpy()
+    assert np.array_equal(hx, dx)
+    d = _ulp_diff(hy, dy)
+    assert int(d.max()) <= 1, f"max ulp {int(d.max())}"
+    assert float(np.mean(d == 0)) > 0.99
+    # contiguous rows (ids omitted): rows first .. first+n of the sweep
+    hx2, hy2 = L.synth_generate(dims, 50, sampling_seed=5, spec_seed=2, first=7, total=total)
+    dx2, dy2 = L.synth_generate_device(dims, 50, total, first=7, sampling_seed=5, spec_seed=2)
+    assert np.array_equal(hx2, dx2.cpu().numpy())
+    assert int(_ulp_diff(hy2, dy2.cpu().numpy()).max()) <= 1
+
+
+def test_device_synth_rejects_noise_and_bad_ids():
+    with pytest.raises(L.ContractError):
+        L.SynthDataset(DESK, 100, noise_level=0.1)
+    ds = L.SynthDataset(DESK, 100)
+    model = L.make_cyclegan(DESK, L.SurrogateArch(), 1)
+    model.autoencoder_frozen = True
+    cfg = L.TrainerConfig(n_shards=1, batch_size=16, seed=1, train_ids=np.arange(90, 120, dtype=np.uint32),
+                          tournament_ids=np.arange(10, dtype=np.uint32))
+    with pytest.raises(L.ContractError):
+        L.Trainer(cfg, ds, model)
+
+
+def test_trainer_device_store_matches_host_store():
+    """A Trainer over a SynthDataset (partition + tournament slice rendered
+    into HBM by k_synth) trains like one over the host-generated rows: same
+    losses (to REL_LOSS; bit-identical whenever the rendered data is) and
+    tournament metrics."""
+    n, total = 900, 5000
+    ids = np.random.default_rng(8).choice(total, n, replace=False).astype(np.uint32)
+    model = L.make_cyclegan(PAPER, L.SurrogateArch(), 6)
+    model.autoencoder_frozen = True
+    cfg = L.TrainerConfig(n_shards=2, batch_size=128, seed=3, train_ids=ids[60:], tournament_ids=ids[:60])
+    hx, hy = L.synth_generate_ids(PAPER, ids, total, sampling_seed=1, spec_seed=1)
+    host = L.SparseDataset(PAPER, ids, hx, hy, total)
+    dev = L.SynthDataset(PAPER, total, sampling_seed=1, spec_seed=1)
+    ta, tb = L.Trainer(cfg, host, model.copy()), L.Trainer(cfg, dev, model.copy())
+    ea, eb = ta.eval_tournament(), tb.eval_tournament()
+    assert rel([ea.forward_mae, ea.inverse_mae], [eb.forward_mae, eb.inverse_mae]) < REL_EVAL
+    ta.train_steps(8)
+    tb.train_steps(8)
+    sa, sb = ta.history().steps, tb.history().steps
+    assert [s.step for s in sa] == [s.step for s in sb]
+    assert rel([s.g_total for s in sa], [s.g_total for s in sb]) < REL_LOSS
+    assert rel([s.d_loss for s in sa], [s.d_loss for s in sb]) < REL_LOSS
+    tb.set_validation(ids[:40])
+    ta.set_validation(ids[:40])
+    va, vb = ta.evaluate_validation(), tb.evaluate_validation()
+    assert rel([va.combined], [vb.combined]) < REL_EVAL

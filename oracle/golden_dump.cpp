@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "ltfb/ltfb.hpp"
+#include "ltfb/bench/output.hpp"
 
 using namespace ltfb;
 namespace fs = std::filesystem;
@@ -919,6 +920,52 @@ static void scenario_tournament(const fs::path& out, const fs::path& tmp) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// run outputs: bench/output.hpp + bench/config.hpp (the run directory the
+// reference CLI writes, ltfb_cli.cpp:126-138) for two tiny runs, copied
+// verbatim into tests/golden/run_<name>/ by make_golden.py. data_dir is
+// relative (golden_dump runs from TMP_DIR) so config.json / config_hash are
+// machine-independent.
+// ---------------------------------------------------------------------------
+static void outputs_case(const fs::path& out, const std::string& name, tournament::RunConfig cfg) {
+  cfg.data_dir = "data_" + name;
+  const auto index = tournament::ensure_dataset(cfg);
+  auto res = tournament::run_experiment(cfg, index);
+  res.history.config_hash = bench::config_hash(cfg);
+  bench::write_run_outputs(out / ("run_" + name), cfg, res.history, &res.best_model);
+}
+
+static void scenario_outputs(const fs::path& out, const fs::path& tmp) {
+  const fs::path abs_out = fs::absolute(out);
+  const fs::path cwd = fs::current_path();
+  fs::current_path(tmp);
+  {
+    tournament::RunConfig cfg;  // tiny_k2 of scenario_tournament
+    cfg.gen_n = 800;
+    cfg.samples_per_file = 100;
+    cfg.dims = tiny_dims();
+    cfg.arch = tiny_arch();
+    cfg.batch_size = 32;
+    cfg.ae_steps = 15;
+    cfg.seed = 42;
+    cfg.mode = tournament::RunMode::kLtfb;
+    cfg.trainers = 2;
+    cfg.interval = 10;
+    cfg.step_budget = 30;
+    outputs_case(abs_out, "tiny_k2", cfg);
+    cfg.mode = tournament::RunMode::kSingle;  // one trainer, no rounds, 2 epochs + a partial
+    cfg.trainers = 1;
+    cfg.step_budget = 50;
+    cfg.interval = 20;
+    cfg.seed = 5;
+    outputs_case(abs_out, "tiny_single", cfg);
+  }
+  fs::current_path(cwd);
+  // golden_dump's tagged-file convention: one (empty) marker per scenario
+  Dump d(out / "outputs.bin");
+  d.put("outputs_runs", std::vector<std::uint32_t>{2});
+}
+
 int main(int argc, char** argv) {
   if (argc < 3) {
     std::fprintf(stderr, "usage: %s OUT_DIR TMP_DIR [scenario...]\n", argv[0]);
@@ -939,6 +986,7 @@ int main(int argc, char** argv) {
     if (on("surrogate")) scenario_surrogate(out);
     if (on("trainer")) scenario_trainer(out, tmp);
     if (on("tournament")) scenario_tournament(out, tmp);
+    if (on("outputs")) scenario_outputs(out, tmp);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "golden_dump failed: %s\n", e.what());
     return 1;

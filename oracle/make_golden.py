@@ -22,7 +22,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 DTYPES = {0: np.float32, 1: np.float64, 2: np.uint32, 3: np.uint64,
           4: np.int32, 5: np.int64, 6: np.uint8}
-SCENARIOS = ["rng", "plan", "synth", "nn", "surrogate", "trainer", "tournament"]
+SCENARIOS = ["rng", "plan", "synth", "nn", "surrogate", "trainer", "tournament", "outputs"]
+RUN_DIRS = ["run_tiny_k2", "run_tiny_single"]  # written by the "outputs" scenario
 
 
 def read_tagged(path):
@@ -57,6 +58,18 @@ def main(argv):
             dst = os.path.join(REPO, "tests", "golden", s + ".npz")
             np.savez_compressed(dst, **arrays)
             print(f"{dst}: {len(arrays)} arrays, {os.path.getsize(dst)} bytes")
+        if "outputs" in want:  # reference run directories, copied verbatim
+            import shutil
+            for rd in RUN_DIRS:
+                dst = os.path.join(REPO, "tests", "golden", rd)
+                shutil.rmtree(dst, ignore_errors=True)
+                shutil.copytree(os.path.join(raw, rd), dst)
+                print(f"{dst}: {sorted(os.listdir(dst))}")
+            subprocess.check_call(["make", "-C", HERE, "_ref/nl_doubles"])
+            dst = os.path.join(REPO, "tests", "golden", "nlohmann_doubles.txt")
+            with open(dst, "w") as f:
+                subprocess.check_call([os.path.join(HERE, "_ref", "nl_doubles"), "4000"], stdout=f)
+            print(f"{dst}: {os.path.getsize(dst)} bytes")
 
 
 if __name__ == "__main__":

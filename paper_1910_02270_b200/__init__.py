@@ -14,7 +14,9 @@ from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrai
                   mix_seed, pair_trainers, param_count, partition_dataset, reinit_gan_nets,
                   split_dataset, synth_generate, synthetic_dataset, tournament_round)
 
-from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, distributed_round,
-                     run_experiment, run_experiment_rank, warm_peer_links)
+from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, TrainerSummary,
+                     distributed_round, run_experiment, run_experiment_rank, trainer_summary, warm_peer_links)
+from .outputs import (config_from_json, config_hash, config_to_json, events_jsonl, load_model, save_model,
+                      summary_csv, timings_csv, write_run_outputs)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -220,6 +220,7 @@ class CycleGan:
         self.lambda_adv = np.float32(arch.lambda_adv)
         self.lambda_cyc = np.float32(arch.lambda_cyc)
         self.autoencoder_frozen = False
+        self.init_seeds = {n: 0 for n in NET_NAMES}  # MlpSpec::init_seed per net (checkpoints)
 
     def __getattr__(self, name):
         if name in NET_NAMES:
@@ -231,6 +232,7 @@ class CycleGan:
         m.blobs = {k: v.copy() for k, v in self.blobs.items()}
         m.opt = {k: AdamState(o.m.copy(), o.v.copy(), o.t) for k, o in self.opt.items()}
         m.autoencoder_frozen = self.autoencoder_frozen
+        m.init_seeds = dict(self.init_seeds)
         return m
 
     def hash_of(self, net: str) -> int:
@@ -262,6 +264,7 @@ def make_cyclegan(dims: ModalityDims, arch: SurrogateArch, seed: int) -> CycleGa
     dc, ac = dims.c(), arch.c()
     for i, n in enumerate(NET_NAMES):
         check(lib.ltfb_init_params(C.byref(dc), C.byref(ac), seed, i, m.blobs[n], m.blobs[n].size))
+        m.init_seeds[n] = mix_seed(seed, i + 1)
     return m
 
 
@@ -272,6 +275,7 @@ def reinit_gan_nets(m: CycleGan, seed: int):
         n = NET_NAMES[i]
         check(lib.ltfb_init_params(C.byref(dc), C.byref(ac), seed, i, m.blobs[n], m.blobs[n].size))
         m.opt[n] = AdamState(np.zeros_like(m.blobs[n]), np.zeros_like(m.blobs[n]), 0)
+        m.init_seeds[n] = mix_seed(seed, i + 1)
 
 
 @dataclass

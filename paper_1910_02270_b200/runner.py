@@ -53,6 +53,21 @@ class RunConfig:
     numeric_abort_threshold: int = 10
     w_f: float = 1.0
     w_i: float = 1.0
+    # dataset / store fields of the reference RunConfig (runner.hpp:49-55,
+    # 66-75): recorded in config.json and the config hash; the B200 path
+    # takes the Dataset object itself and keeps the store HBM-resident
+    data_dir: str = ""
+    generate: bool = True
+    gen_n: int = 16000
+    samples_per_file: int = 500
+    sampling_seed: int = 1
+    spec_seed: int = 1
+    noise_level: float = 0.0
+    data_store: str = "preload"
+    threads: int = 1
+    store_budget_mb: int = 0
+    prefetch_depth: int = 1
+    # B200 placement (not part of the reference config or its hash)
     devices: tuple | None = None  # trainer t runs on devices[t % len(devices)]
     wide_kernel: int = 0
 
@@ -70,6 +85,58 @@ class RunHistory:
     transfers: list = field(default_factory=list)
     best_trainer: int = -1
     best_metric: EvalMetric | None = None
+    config_hash: str = ""
+    summaries: list = field(default_factory=list)
+
+
+@dataclass
+class TrainerSummary:
+    """train/history.hpp TrainerSummary (one summary.csv row)."""
+    trainer: int = 0
+    steps: int = 0
+    epochs_completed: int = 0
+    final_d_loss: float = 0.0
+    final_g_total: float = 0.0
+    final_g_fwd: float = 0.0
+    final_g_adv: float = 0.0
+    final_g_cyc: float = 0.0
+    final_val_forward_mae: float = 0.0
+    final_val_inverse_mae: float = 0.0
+    final_val_combined: float = 0.0
+    rounds: int = 0
+    incoming_adopted: int = 0
+    files_opened: int = 0
+    bytes_read: int = 0
+    samples_shuffled: int = 0
+    skipped_steps: int = 0
+    is_best: bool = False
+
+
+def trainer_summary(tid: int, steps: int, seg: HistorySegment, trainer_rounds, best_trainer: int) -> TrainerSummary:
+    """runner.hpp:400-432: every field recomputed from the trainer's records
+    (store counters = the sums of its epoch records' deltas)."""
+    s = TrainerSummary(trainer=tid, steps=int(steps))
+    for r in seg.steps:
+        if not r.skipped:
+            s.final_d_loss, s.final_g_total, s.final_g_fwd = r.d_loss, r.g_total, r.g_fwd
+            s.final_g_adv, s.final_g_cyc = r.g_adv, r.g_cyc
+    for e in seg.epochs:
+        if e.epoch > 0 and not e.partial:
+            s.epochs_completed += 1
+        s.files_opened += e.files_opened
+        s.bytes_read += e.bytes_read
+        s.samples_shuffled += e.samples_shuffled
+    for e in seg.evals:
+        if e.slice == "validation":
+            s.final_val_forward_mae, s.final_val_inverse_mae, s.final_val_combined = \
+                e.forward_mae, e.inverse_mae, e.combined
+    for r in trainer_rounds:
+        if r.trainer == tid:
+            s.rounds += 1
+            s.incoming_adopted += 1 if r.kept_incoming else 0
+    s.skipped_steps = int(seg.skipped_steps)
+    s.is_best = tid == best_trainer
+    return s
 
 
 @dataclass
@@ -193,6 +260,10 @@ def run_experiment(cfg: RunConfig, dataset: Dataset) -> RunResult:
         res.best_trainer = 0
     res.best_model = trainers[max(res.best_trainer, 0)].model().copy()
     history.best_trainer, history.best_metric = res.best_trainer, res.best_metric
+    history.summaries = [trainer_summary(t.cfg.trainer_id, t.step(), t.history(), history.trainer_rounds,
+                                         res.best_trainer) for t in trainers]
+    from .outputs import config_hash
+    history.config_hash = config_hash(cfg)
     return res
 
 
@@ -332,7 +403,7 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset, comm, device: int = 0)
             my_xfers += xf
     t.flush_epoch_record()
     final = t.evaluate_validation(cfg.w_f, cfg.w_i) if have_val else None
-    parts = comm.all_gather((t.history(), my_rounds, my_xfers, final))
+    parts = comm.all_gather((t.history(), my_rounds, my_xfers, final, t.step()))
     # best-of-k on the shared validation slice (runner.hpp:380-398): every
     # rank sees the same metrics, only the winner ships its model
     best_rank, best = 0, float("inf")
@@ -354,4 +425,8 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset, comm, device: int = 0)
                 history.transfers += [by[(rr.round, frm, "fwd")], by[(rr.round, frm, "inv")]]
     res = RunResult(history, best_rank, parts[best_rank][3] if have_val else None, models[best_rank])
     history.best_trainer, history.best_metric = res.best_trainer, res.best_metric
+    history.summaries = [trainer_summary(r, p[4], p[0], history.trainer_rounds, best_rank)
+                         for r, p in enumerate(parts)]
+    from .outputs import config_hash
+    history.config_hash = config_hash(cfg)
     return res

@@ -539,3 +539,64 @@ def test_trainer_device_store_matches_host_store():
     ta.set_validation(ids[:40])
     va, vb = ta.evaluate_validation(), tb.evaluate_validation()
     assert rel([va.combined], [vb.combined]) < REL_EVAL
+
+
+@pytest.mark.parametrize("run", ["run_tiny_k2", "run_tiny_single"])
+def test_run_outputs_match_reference_run_directory(run, tmp_path):
+    """The B200 run_experiment written out with outputs.write_run_outputs
+    next to the run directory the reference CLI path wrote for the same
+    config (tests/golden/run_*): config.json byte-identical, the same event
+    stream (every record type, order and integer field; floats within
+    10 * REL_LOSS), summary.csv's integer columns exact, the checkpoint's
+    header (dims, lambdas, layer specs, init seeds) byte-identical; and a
+    replay of the run reproduces summary.csv byte for byte. (Blob hashes
+    cover float bit patterns, which the parity bar does not fix: format
+    only.)"""
+    import json
+    import os
+    from paper_1910_02270_b200 import outputs as O
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", run)
+    cj = json.load(open(os.path.join(gold, "config.json")))
+    cj.pop("config_hash")
+    cfg = O.config_from_json(cj)
+    ds = L.synthetic_dataset(cfg.dims, cfg.gen_n, sampling_seed=cfg.sampling_seed, spec_seed=cfg.spec_seed,
+                             samples_per_file=cfg.samples_per_file)
+    outs = []
+    for rep in range(2):
+        res = L.run_experiment(cfg, ds)
+        O.write_run_outputs(tmp_path / f"r{rep}", cfg, res.history, res.best_model)
+        outs.append({n: (tmp_path / f"r{rep}" / n).read_bytes() for n in
+                     ("config.json", "events.jsonl", "summary.csv", "best_model.bin")})
+    want = {n: open(os.path.join(gold, n), "rb").read() for n in outs[0]}
+    assert outs[0]["config.json"] == want["config.json"]
+    assert outs[0]["summary.csv"] == outs[1]["summary.csv"]  # replay
+    ev, ew = O.parse_events(outs[0]["events.jsonl"].decode()), O.parse_events(want["events.jsonl"].decode())
+    assert [e["type"] for e in ev] == [e["type"] for e in ew]
+    for a, b in zip(ev, ew):
+        assert sorted(a) == sorted(b)
+        for key in a:
+            if key == "seconds":
+                continue
+            if key.endswith("_hash") and a["type"] != "run_start":  # FNV of float blobs: format only
+                assert len(a[key]) == 16 and int(a[key], 16) >= 0
+                continue
+            if isinstance(b[key], float):
+                assert rel([a[key]], [b[key]]) < 10 * REL_LOSS, (a["type"], key)
+            else:
+                assert a[key] == b[key], (a["type"], key)
+    rows_a = [r.split(",") for r in outs[0]["summary.csv"].decode().splitlines()]
+    rows_b = [r.split(",") for r in want["summary.csv"].decode().splitlines()]
+    assert rows_a[0] == rows_b[0] and len(rows_a) == len(rows_b)
+    ints = [i for i, c in enumerate(rows_b[0]) if not c.startswith("final_")]
+    for ra, rb in zip(rows_a[1:], rows_b[1:]):
+        assert [ra[i] for i in ints] == [rb[i] for i in ints]
+        assert rel([float(ra[i]) for i in range(len(ra)) if i not in ints],
+                   [float(rb[i]) for i in range(len(rb)) if i not in ints]) < 10 * REL_LOSS
+    ma = O.load_model(tmp_path / "r0" / "best_model.bin")
+    mb = O.load_model(os.path.join(gold, "best_model.bin"))
+    assert len(outs[0]["best_model.bin"]) == len(want["best_model.bin"])
+    assert ma.init_seeds == mb.init_seeds and ma.dims == mb.dims
+    for n in ("fwd", "inv", "disc"):
+        # Adam moves each weight by <= ~lr per step: 2 lr steps bounds any
+        # drift from sign flips of near-zero gradients
+        assert float(np.max(np.abs(ma.blobs[n] - mb.blobs[n]))) <= 2 * cfg.arch.lr * cfg.step_budget, n

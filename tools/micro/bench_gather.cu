@@ -4,29 +4,35 @@
 //   mode 0: lane l of one warp issues rows 4l..4l+3 (the product's scheme)
 //   mode 1: one thread issues all 32 gather4
 //   mode 2: 4 warps, lanes 0-7 each
+//   mode 3: no TMA: 4 warps of cp.async 16 B (LDGSTS) into the SW128 layout
+//   mode 4: 2 warps of cp.async (64 threads, 16 ops each per tile)
+//   mode 5: one 16 KB cp.async.bulk of a contiguous (pre-laid-out) tile
+//   mode 6: eight 2 KB cp.async.bulk by 8 lanes
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <cstdlib>
 #include "../../paper_1910_02270_b200/csrc/tc_ptx.cuh"
 using namespace ltfb_dev;
 
-__global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long long* out, int mode, int ncols) {
+__global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long long* out, int mode, int ncols,
+                  const float* gsrc, int NS, int NT, long long nrows_tab) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[3];
+  __shared__ uint64_t full[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 3; ++s) tc::mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) tc::mbar_init(&full[s], mode == 3 ? 128 : (mode == 4 ? 64 : 1));
     tc::fence_barrier_init();
   }
   __syncthreads();
   long long t0 = clock64(), issue = 0;
   const int* rr = rows + (blockIdx.x % 64) * 128;
-  for (int t = 0; t < 11; ++t) {
-    const int s = t % 3;
-    if (t >= 3) tc::mbar_wait(&full[s], ((t - 3) / 3) & 1);  // slot reuse: tile t-3 landed
+  for (int t = 0; t < NT; ++t) {
+    const int s = t % NS;
+    if (t >= NS) tc::mbar_wait(&full[s], ((t - NS) / NS) & 1);  // slot reuse: tile t-NS landed
     __syncthreads();
     const int c0 = ((blockIdx.x + t * 148) * 32) % ncols;
     long long i0 = clock64();
@@ -43,6 +49,33 @@ __global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long l
         for (int i = 0; i < 32; ++i)
           tc::tma_gather4(sm + s * 16384 + 512 * i, &m, &full[s], c0, rr[4 * i], rr[4 * i + 1], rr[4 * i + 2], rr[4 * i + 3]);
       }
+    } else if (mode >= 5) {
+      const long long off = ((long long)(blockIdx.x + t * 148) * 4096) % ((long long)ncols * nrows_tab - 4096);
+      if (mode == 5 && threadIdx.x == 0) {
+        tc::mbar_expect_tx(&full[s], 16384);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::"r"(
+                         tc::smem_u32(sm + s * 16384)), "l"(gsrc + off), "r"(tc::smem_u32(&full[s]))
+                     : "memory");
+      }
+      if (mode == 6 && warp == 0) {
+        if (lane == 0) tc::mbar_expect_tx(&full[s], 16384);
+        __syncwarp();
+        if (lane < 8)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 2048, [%2];" ::"r"(
+                           tc::smem_u32(sm + s * 16384 + lane * 2048)), "l"(gsrc + off + lane * 512), "r"(tc::smem_u32(&full[s]))
+                       : "memory");
+      }
+    } else if (mode >= 3) {
+      const int nt = mode == 3 ? 128 : 64;
+      if ((int)threadIdx.x < nt) {
+        for (int i = threadIdx.x; i < 1024; i += nt) {
+          const int r = i >> 3, ch = i & 7;
+          const unsigned dst = tc::smem_u32(sm + s * 16384 + r * 128 + ((ch ^ (r & 7)) << 4));
+          const float* src = gsrc + (long long)rr[r] * ncols + c0 + ch * 4;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[s])) : "memory");
+      }
     } else {
       if (threadIdx.x == 0) tc::mbar_expect_tx(&full[s], 16384);
       __syncthreads();
@@ -54,13 +87,14 @@ __global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long l
     __syncthreads();
     issue += clock64() - i0;
   }
-  for (int t = 8; t < 11; ++t) tc::mbar_wait(&full[t % 3], (t / 3) & 1);
+  for (int t = NT - NS; t < NT; ++t) tc::mbar_wait(&full[t % NS], (t / NS) & 1);
   long long t1 = clock64();
-  if (threadIdx.x == 0 && blockIdx.x == 0) { out[0] = t1 - t0; out[1] = issue / 11; }
+  if (threadIdx.x == 0 && blockIdx.x == 0) { out[0] = t1 - t0; out[1] = issue / NT; }
 }
 
-int main() {
-  const long long N = 8000, C = 49168;
+int main(int argc, char** argv) {
+  const int G = argc > 2 ? atoi(argv[2]) : 148;
+  const long long N = argc > 1 ? atoll(argv[1]) : 8000, C = 49168;
   float* d; cudaMalloc(&d, N * C * 4); cudaMemset(d, 0, N * C * 4);
   std::vector<int> rows(64 * 128); unsigned s = 1;
   for (auto& r : rows) { s = s * 1664525u + 1013904223u; r = (s >> 8) % N; }
@@ -77,13 +111,15 @@ int main() {
   const cuuint32_t box[2] = {32, 1}, es[2] = {1, 1};
   ((Fn)fp)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
-  for (int rep = 0; rep < 2; ++rep)
-    for (int mode = 0; mode < 3; ++mode) {
-      k<<<148, 256, 60000>>>(m, rd, o, mode, (int)C);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384 + 1024);
+  const int NT = 44;
+  for (int mode = 0; mode < 7; ++mode)
+    for (int NS : {2, 3, 4, 6, 8}) {
+      if (mode < 2 && NS != 3) continue;
+      k<<<G, 256, NS * 16384 + 1024>>>(m, rd, o, mode, (int)C, d, NS, NT, N);
       long long h[2]; cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
-      printf("mode %d: 11 tiles %lld cycles (%.0f per tile), issue %lld cycles per tile (%s)\n", mode, h[0], h[0] / 11.0, h[1],
-             cudaGetErrorString(cudaGetLastError()));
+      printf("mode %d NS %d: %d tiles %lld cycles (%.0f per tile, %.1f B/clk), issue %lld per tile (%s)\n", mode, NS, NT,
+             h[0], h[0] / (double)NT, 16384.0 * NT / h[0], h[1], cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
 }

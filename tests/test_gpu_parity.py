@@ -366,7 +366,7 @@ def test_run_experiment_matches_reference(golden, pfx):
     assert res.best_trainer == int(g[pfx + "best_trainer"][0])
 
 
-def test_multi_gpu_run_matches_reference():
+def test_multi_gpu_run_matches_reference(tmp_path):
     """tools/dist_run.py under torchrun on 2 GPUs: one trainer per GPU, the
     NCCL device-to-device exchange, the reference's tiny_k2 run."""
     import os
@@ -378,9 +378,18 @@ def test_multi_gpu_run_matches_reference():
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr", "127.0.0.1", "--master-port", "29533",
-                        os.path.join(repo, "tools", "dist_run.py"), "--golden", "tiny_k2_"],
+                        os.path.join(repo, "tools", "dist_run.py"), "--golden", "tiny_k2_",
+                        "--out", str(tmp_path / "run")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    # the merged run directory: same config / hash and the same integer
+    # summary columns as the reference's run_tiny_k2
+    gold = os.path.join(repo, "tests", "golden", "run_tiny_k2")
+    assert (tmp_path / "run" / "config.json").read_bytes() == open(os.path.join(gold, "config.json"), "rb").read()
+    ra = [x.split(",") for x in (tmp_path / "run" / "summary.csv").read_text().splitlines()]
+    rb = [x.split(",") for x in open(os.path.join(gold, "summary.csv")).read().splitlines()]
+    ints = [i for i, c in enumerate(rb[0]) if not c.startswith("final_")]
+    assert [[row[i] for i in ints] for row in ra] == [[row[i] for i in ints] for row in rb]
 
 
 def test_cpp_facade_matches_python_mirror():

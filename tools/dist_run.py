@@ -21,6 +21,7 @@ sys.path.insert(0, REPO)
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--golden", default="tiny_k2_")
+    p.add_argument("--out", default=None, help="rank 0 writes the run directory here (outputs.py)")
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -44,7 +45,9 @@ def main():
     arch = L.SurrogateArch.tiny() if pfx.startswith("tiny") else L.SurrogateArch()
     ds = L.synthetic_dataset(dims, gen_n, sampling_seed=sampling_seed, spec_seed=spec_seed, samples_per_file=spf)
     cfg = L.RunConfig(dims=dims, arch=arch, mode="ltfb", trainers=k, shards=shards, batch_size=batch,
-                      interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed)
+                      interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed, gen_n=gen_n,
+                      samples_per_file=spf, spec_seed=spec_seed, sampling_seed=sampling_seed,
+                      data_dir="data_" + pfx.rstrip("_"))  # = tests/golden/run_<pfx>/config.json
     res = L.run_experiment_rank(cfg, ds, comm, device=local)
     ok = True
     if rank == 0:
@@ -66,6 +69,8 @@ def main():
         }
         ok = (checks["steps_order"] and checks["kept"] and checks["xf_bytes"] and checks["best_trainer"]
               and checks["g_total_rel"] < 1e-3 and checks["local_rel"] < 1e-3 and checks["evals_rel"] < 1e-3)
+        if a.out:
+            L.write_run_outputs(a.out, cfg, h, res.best_model)
         print(json.dumps({"golden": pfx, "ranks": world, "ok": bool(ok), "checks": checks,
                           "rounds": len(h.rounds), "exchange": "nccl device-to-device"}))
     okt = [ok]

@@ -103,6 +103,7 @@ typedef struct {
 
 typedef struct ltfb_trainer ltfb_trainer;
 typedef struct ltfb_comm ltfb_comm;
+typedef struct ltfb_dataset ltfb_dataset; /* DatasetIndex over LBDS bundle files */
 
 const char* ltfb_last_error(void);
 int ltfb_abi_version(void);
@@ -267,6 +268,23 @@ int ltfb_synth_generate_device(const ltfb_dims* dims, uint64_t spec_seed, double
                                const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
                                uint64_t sampling_seed, float* x_dev, float* y_dev, uint64_t y_stride,
                                int device);
+/* ---- LBDS bundle datasets (data/bundle.hpp:25-224, runner.hpp:203-230) ----
+ * The on-disk dataset the reference trains from: sorted bundle_*.lbds files
+ * (40-byte header + records inputs[5] || outputs[out], f32 LE). */
+/* DatasetIndex::scan_dir: every *.lbds under dir, sorted by name. */
+int ltfb_dataset_open(const char* dir, ltfb_dataset** out);
+int ltfb_dataset_destroy(ltfb_dataset* d);
+int ltfb_dataset_info(const ltfb_dataset* d, ltfb_dims* dims, uint64_t* total, uint64_t* n_files);
+/* bundle file index of each id (DatasetIndex::locate). */
+int ltfb_dataset_file_of(const ltfb_dataset* d, const uint32_t* ids, uint64_t n, uint32_t* file_idx);
+/* assemble_tensors / read_records: rows ids[i] into x [n x 5] and y
+ * [n x output_dim]; *files_opened = distinct files opened (may be NULL). */
+int ltfb_dataset_read(const ltfb_dataset* d, const uint32_t* ids, uint64_t n, float* x, float* y,
+                      uint64_t* files_opened);
+/* ensure_dataset's generation branch: generate_dataset(gen_n) and
+ * write_bundles(samples_per_file) into dir (bundle_00000.lbds, ...). */
+int ltfb_write_synth_bundles(const char* dir, const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                             uint64_t gen_n, uint64_t sampling_seed, uint32_t samples_per_file, int threads);
 /* make_cyclegan blob init (model.hpp:96-132, mlp.hpp:235-244) */
 int ltfb_init_params(const ltfb_dims* dims, const ltfb_arch* arch, uint64_t seed, int net,
                      float* blob, uint64_t count);

@@ -65,6 +65,9 @@ def main(argv):
                 shutil.rmtree(dst, ignore_errors=True)
                 shutil.copytree(os.path.join(raw, rd), dst)
                 print(f"{dst}: {sorted(os.listdir(dst))}")
+            # one bundle file the reference's ensure_dataset wrote (LBDS bytes)
+            shutil.copy(os.path.join(tmp, "data_tiny_k2", "bundle_00000.lbds"),
+                        os.path.join(REPO, "tests", "golden", "run_tiny_k2_bundle_00000.lbds"))
             subprocess.check_call(["make", "-C", HERE, "_ref/nl_doubles"])
             dst = os.path.join(REPO, "tests", "golden", "nlohmann_doubles.txt")
             with open(dst, "w") as f:

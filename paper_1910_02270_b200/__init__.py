@@ -7,7 +7,7 @@ tournament API on top of that ABI.
 """
 from ._lib import (CapacityError, ConfigError, ContractError, CudaError, DimensionError, Error,
                    IoError, NumericError, StoreCorruptError, LIB_PATH)
-from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrain_autoencoder, CycleGan, Dataset, SparseDataset, SynthDataset, synth_generate_device, synth_generate_ids, EpochRecord, EvalMetric, EvalRecord, HistorySegment,
+from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrain_autoencoder, CycleGan, Dataset, SparseDataset, SynthDataset, BundleDataset, write_synth_bundles, synth_generate_device, synth_generate_ids, EpochRecord, EvalMetric, EvalRecord, HistorySegment,
                   Matching, ModalityDims, RoundRecord, RoundResult, StepRecord, SurrogateArch,
                   Trainer, TrainerConfig, TrainerRoundRecord, TransferRecord, device_count,
                   epoch_permutation, fnv1a64, hex64, incoming_wins, layer_widths, make_cyclegan,
@@ -15,7 +15,7 @@ from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrai
                   split_dataset, synth_generate, synthetic_dataset, tournament_round)
 
 from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, TrainerSummary,
-                     distributed_round, run_experiment, run_experiment_rank, trainer_summary, warm_peer_links)
+                     distributed_round, ensure_dataset, run_experiment, run_experiment_rank, trainer_summary, warm_peer_links)
 from .outputs import (config_from_json, config_hash, config_to_json, events_jsonl, load_model, save_model,
                       summary_csv, timings_csv, write_run_outputs)
 

@@ -102,6 +102,8 @@ EXPORTS = (
     "ltfb_trainer_set_params", "ltfb_trainer_get_params", "ltfb_trainer_set_adam",
     "ltfb_trainer_get_adam", "ltfb_trainer_load_store", "ltfb_trainer_set_slice",
     "ltfb_trainer_generate_store", "ltfb_trainer_generate_slice", "ltfb_synth_generate_device",
+    "ltfb_dataset_open", "ltfb_dataset_destroy", "ltfb_dataset_info", "ltfb_dataset_file_of", "ltfb_dataset_read",
+    "ltfb_write_synth_bundles",
     "ltfb_trainer_train_steps", "ltfb_trainer_step", "ltfb_trainer_take_epochs",
     "ltfb_trainer_flush_epoch", "ltfb_trainer_evaluate", "ltfb_trainer_generator_floats",
     "ltfb_trainer_get_generator", "ltfb_trainer_set_incoming", "ltfb_trainer_copy_incoming",
@@ -200,6 +202,13 @@ _sig("ltfb_synth_generate", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, C.
      C.c_uint64, C.c_uint64, f32p, f32p, C.c_int)
 _sig("ltfb_synth_generate_device", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, P, C.c_uint64,
      C.c_uint64, C.c_uint64, C.c_uint64, P, P, C.c_uint64, C.c_int)
+_sig("ltfb_dataset_open", C.c_int, C.c_char_p, C.POINTER(P))
+_sig("ltfb_dataset_destroy", C.c_int, P)
+_sig("ltfb_dataset_info", C.c_int, P, C.POINTER(Dims), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64))
+_sig("ltfb_dataset_file_of", C.c_int, P, u32p, C.c_uint64, u32p)
+_sig("ltfb_dataset_read", C.c_int, P, u32p, C.c_uint64, f32p, f32p, C.POINTER(C.c_uint64))
+_sig("ltfb_write_synth_bundles", C.c_int, C.c_char_p, C.POINTER(Dims), C.c_uint64, C.c_double, C.c_uint64,
+     C.c_uint64, C.c_uint32, C.c_int)
 _sig("ltfb_init_params", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_uint64, C.c_int, f32p, C.c_uint64)
 _sig("ltfb_net_param_count", C.c_int, C.POINTER(Dims), C.POINTER(Arch), C.c_int, C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_synchronize", C.c_int, P)

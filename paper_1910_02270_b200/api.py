@@ -353,6 +353,53 @@ class SparseDataset(Dataset):
         return self.x[sel], self.y[sel]
 
 
+class BundleDataset(Dataset):
+    """The reference's on-disk dataset: LBDS bundle files under a directory
+    (data/bundle.hpp:134-224, DatasetIndex::scan_dir). Rows are read from
+    the files on demand; a Trainer preloads its partition into HBM once
+    (store.hpp:100-135), dealing files to shards round-robin."""
+
+    def __init__(self, path):
+        self.path = os.fspath(path)
+        self._h = C.c_void_p()
+        check(lib.ltfb_dataset_open(self.path.encode(), C.byref(self._h)))
+        dc, total, nf = _lib.Dims(), C.c_uint64(0), C.c_uint64(0)
+        check(lib.ltfb_dataset_info(self._h, C.byref(dc), C.byref(total), C.byref(nf)))
+        self.dims = ModalityDims(dc.input_dim, dc.latent_dim, dc.scalar_dim, dc.image_views, dc.image_channels,
+                                 dc.image_h, dc.image_w)
+        self.total, self.n_files = int(total.value), int(nf.value)
+        self.files_opened = 0  # cumulative, like the store counters
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.ltfb_dataset_destroy(h)
+            self._h = None
+
+    def file_of(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, np.uint32)
+        out = np.empty(ids.size, np.uint32)
+        check(lib.ltfb_dataset_file_of(self._h, ids, ids.size, out))
+        return out.astype(np.int64)
+
+    def rows(self, ids):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        x = np.empty((ids.size, self.dims.input_dim), np.float32)
+        y = np.empty((ids.size, self.dims.output_dim()), np.float32)
+        opened = C.c_uint64(0)
+        check(lib.ltfb_dataset_read(self._h, ids, ids.size, x, y, C.byref(opened)))
+        self.files_opened += opened.value
+        return x, y
+
+
+def write_synth_bundles(path, dims: ModalityDims, n: int, sampling_seed: int = 1, spec_seed: int = 1,
+                        noise_level: float = 0.0, samples_per_file: int = 500, threads: int | None = None):
+    """generate_dataset(n) + write_bundles (runner.hpp:216-227) into path."""
+    dc = dims.c()
+    check(lib.ltfb_write_synth_bundles(os.fspath(path).encode(), C.byref(dc), spec_seed, noise_level, n,
+                                       sampling_seed, samples_per_file, threads or max(1, os.cpu_count() or 1)))
+
+
 class SynthDataset(Dataset):
     """A `total`-point synthetic sweep (generate_dataset, generator.hpp:195-206)
     that is never materialised on the host: a Trainer renders its partition

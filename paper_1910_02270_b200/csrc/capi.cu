@@ -624,10 +624,10 @@ int ltfb_incoming_wins(double local, double incoming) {
   return ltfb::tournament::incoming_wins(local, incoming) ? 1 : 0;
 }
 
-static int synth_rows(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
-                      const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
-                      uint64_t sampling_seed, float* x, float* y, int threads) {
-  return guarded([&] {
+static void synth_rows_impl(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                            const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
+                            uint64_t sampling_seed, float* x, float* y, int threads) {
+  {
     ltfb::synth::GeneratorSpec spec;
     spec.dims = dims_of(dims);
     spec.spec_seed = spec_seed;
@@ -650,7 +650,14 @@ static int synth_rows(const ltfb_dims* dims, uint64_t spec_seed, double noise_le
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w) pool.emplace_back(work, n * w / nt, n * (w + 1) / nt);
     for (auto& th : pool) th.join();
-  });
+  }
+}
+
+static int synth_rows(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                      const uint32_t* ids, uint64_t first, uint64_t n, uint64_t total_n,
+                      uint64_t sampling_seed, float* x, float* y, int threads) {
+  return guarded([&] { synth_rows_impl(dims, spec_seed, noise_level, ids, first, n, total_n, sampling_seed, x, y,
+                                       threads); });
 }
 
 int ltfb_synth_generate_ids(const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
@@ -681,6 +688,67 @@ int ltfb_synth_generate_device(const ltfb_dims* dims, uint64_t spec_seed, double
       throw;
     }
     LTFB_CUDA(cudaStreamDestroy(s));
+  });
+}
+
+struct ltfb_dataset {
+  ltfb::data::DatasetIndex index;
+};
+
+int ltfb_dataset_open(const char* dir, ltfb_dataset** out) {
+  return guarded([&] {
+    if (!dir || !out) throw ltfb::ContractError("ltfb_dataset_open: null argument");
+    auto* d = new ltfb_dataset{ltfb::data::DatasetIndex::scan_dir(dir)};
+    *out = d;
+  });
+}
+
+int ltfb_dataset_destroy(ltfb_dataset* d) {
+  delete d;
+  return LTFB_OK;
+}
+
+int ltfb_dataset_info(const ltfb_dataset* d, ltfb_dims* dims, uint64_t* total, uint64_t* n_files) {
+  return guarded([&] {
+    const auto& x = d->index.dims;
+    if (dims) *dims = ltfb_dims{x.input_dim, x.latent_dim, x.scalar_dim, x.image_views, x.image_channels,
+                                x.image_h, x.image_w};
+    if (total) *total = d->index.total;
+    if (n_files) *n_files = d->index.paths.size();
+  });
+}
+
+int ltfb_dataset_file_of(const ltfb_dataset* d, const uint32_t* ids, uint64_t n, uint32_t* file_idx) {
+  return guarded([&] {
+    for (uint64_t i = 0; i < n; ++i) file_idx[i] = static_cast<uint32_t>(d->index.locate(ids[i]).file_idx);
+  });
+}
+
+int ltfb_dataset_read(const ltfb_dataset* d, const uint32_t* ids, uint64_t n, float* x, float* y,
+                      uint64_t* files_opened) {
+  return guarded([&] {
+    const std::size_t opened = ltfb::data::read_records(d->index, std::span<const uint32_t>(ids, n), x, y,
+                                                        d->index.dims.output_dim());
+    if (files_opened) *files_opened = opened;
+  });
+}
+
+int ltfb_write_synth_bundles(const char* dir, const ltfb_dims* dims, uint64_t spec_seed, double noise_level,
+                             uint64_t gen_n, uint64_t sampling_seed, uint32_t samples_per_file, int threads) {
+  return guarded([&] {
+    if (!dir) throw ltfb::ContractError("ltfb_write_synth_bundles: null directory");
+    if (gen_n < 1) throw ltfb::ContractError("generate_dataset: n must be >= 1");
+    const auto d = dims_of(dims);
+    const std::size_t in = d.input_dim, out = d.output_dim();
+    std::vector<float> x(gen_n * in), y(gen_n * out);
+    synth_rows_impl(dims, spec_seed, noise_level, nullptr, 0, gen_n, gen_n, sampling_seed, x.data(), y.data(),
+                    threads);
+    std::vector<ltfb::data::SampleRecord> recs(gen_n);
+    for (uint64_t i = 0; i < gen_n; ++i) {
+      recs[i].inputs.assign(x.begin() + i * in, x.begin() + (i + 1) * in);
+      recs[i].outputs.assign(y.begin() + i * out, y.begin() + (i + 1) * out);
+    }
+    ltfb::data::write_bundles(recs, d, samples_per_file, dir);
   });
 }
 

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .api import (CycleGan, Dataset, EvalRecord, HistorySegment, RoundRecord, Trainer, TrainerConfig,
+from .api import (BundleDataset, IoError, write_synth_bundles, CycleGan, Dataset, EvalRecord, HistorySegment, RoundRecord, Trainer, TrainerConfig,
                   TrainerRoundRecord, TransferRecord, ConfigError, ContractError, hex64, fnv1a64,
                   make_cyclegan, mix_seed, pair_trainers, param_count, pretrain_autoencoder,
                   reinit_gan_nets, split_dataset, tournament_round, EvalMetric)
@@ -212,9 +212,32 @@ def _merge(history: RunHistory, segments):
     history.epochs.sort(key=lambda r: (r.epoch, r.trainer))
 
 
-def run_experiment(cfg: RunConfig, dataset: Dataset) -> RunResult:
-    """runner.hpp:232-420 in one process (k trainers on cfg.devices)."""
+def ensure_dataset(cfg: RunConfig) -> BundleDataset:
+    """runner.hpp:203-230: the LBDS bundles under cfg.data_dir, generated
+    there first (generate_dataset + write_bundles) when the directory holds
+    none and cfg.generate is set."""
+    import os
+    have = os.path.isdir(cfg.data_dir) and any(f.endswith(".lbds") for f in os.listdir(cfg.data_dir))
+    if not have:
+        if not cfg.generate:
+            raise IoError(f"no dataset found under {cfg.data_dir} and generation is disabled")
+        write_synth_bundles(cfg.data_dir, cfg.dims, cfg.gen_n, cfg.sampling_seed, cfg.spec_seed, cfg.noise_level,
+                            cfg.samples_per_file)
+    return BundleDataset(cfg.data_dir)
+
+
+def _check_dims(cfg: RunConfig, dataset: Dataset):
+    if cfg.dims is not None and dataset.dims != cfg.dims:
+        raise ConfigError("configured dims do not match the dataset on disk")
+
+
+def run_experiment(cfg: RunConfig, dataset: Dataset | None = None) -> RunResult:
+    """runner.hpp:232-420 in one process (k trainers on cfg.devices).
+    Without a dataset, ensure_dataset(cfg) provides the bundles."""
     validate_run_config(cfg)
+    if dataset is None:
+        dataset = ensure_dataset(cfg)
+    _check_dims(cfg, dataset)
     k = 1 if cfg.mode == "single" else cfg.trainers
     rounds_enabled = cfg.mode == "ltfb" and k >= 2
     split = split_dataset(dataset.total, k, cfg.validation_fraction, cfg.tournament_fraction, cfg.seed, k >= 2)
@@ -367,10 +390,13 @@ def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     return rr, rec, transfers
 
 
-def run_experiment_rank(cfg: RunConfig, dataset: Dataset, comm, device: int = 0) -> RunResult | None:
+def run_experiment_rank(cfg: RunConfig, dataset: Dataset | None, comm, device: int = 0) -> RunResult | None:
     """One rank of a k = world-size LTFB run (one trainer per GPU). Returns
     the merged RunResult on rank 0 (None elsewhere)."""
     validate_run_config(cfg)
+    if dataset is None:
+        dataset = ensure_dataset(cfg)  # every rank generates / scans the same bundles
+    _check_dims(cfg, dataset)
     k = comm.world
     if cfg.mode != "single" and cfg.trainers != k:
         raise ConfigError("run_experiment_rank: trainers must equal the world size")

@@ -551,14 +551,15 @@ def test_trainer_device_store_matches_host_store():
 
 
 @pytest.mark.parametrize("run", ["run_tiny_k2", "run_tiny_single"])
-def test_run_outputs_match_reference_run_directory(run, tmp_path):
+def test_run_outputs_match_reference_run_directory(run, tmp_path, monkeypatch):
     """The B200 run_experiment written out with outputs.write_run_outputs
     next to the run directory the reference CLI path wrote for the same
     config (tests/golden/run_*): config.json byte-identical, the same event
     stream (every record type, order and integer field; floats within
     10 * REL_LOSS), summary.csv's integer columns exact, the checkpoint's
     header (dims, lambdas, layer specs, init seeds) byte-identical; and a
-    replay of the run reproduces summary.csv byte for byte. (Blob hashes
+    replay of the run (from the in-memory dataset instead of the bundle
+    files) reproduces summary.csv byte for byte. (Blob hashes
     cover float bit patterns, which the parity bar does not fix: format
     only.)"""
     import json
@@ -570,9 +571,12 @@ def test_run_outputs_match_reference_run_directory(run, tmp_path):
     cfg = O.config_from_json(cj)
     ds = L.synthetic_dataset(cfg.dims, cfg.gen_n, sampling_seed=cfg.sampling_seed, spec_seed=cfg.spec_seed,
                              samples_per_file=cfg.samples_per_file)
+    monkeypatch.chdir(tmp_path)  # data_dir is relative, as in the reference run
     outs = []
     for rep in range(2):
-        res = L.run_experiment(cfg, ds)
+        # rep 0: ensure_dataset writes + scans LBDS bundles (the reference's
+        # path); rep 1: the in-memory dataset -- the replay must agree
+        res = L.run_experiment(cfg) if rep == 0 else L.run_experiment(cfg, ds)
         O.write_run_outputs(tmp_path / f"r{rep}", cfg, res.history, res.best_model)
         outs.append({n: (tmp_path / f"r{rep}" / n).read_bytes() for n in
                      ("config.json", "events.jsonl", "summary.csv", "best_model.bin")})

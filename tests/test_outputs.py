@@ -166,3 +166,30 @@ def test_write_run_outputs_matches_reference_layout(tmp_path):
     for name in ("config.json", "events.jsonl", "summary.csv", "timings.csv", "best_model.bin"):
         assert (tmp_path / "out" / name).read_bytes() == _read(run, name, "rb"), name
     assert np.array_equal(m.blobs["fwd"], O.load_model(tmp_path / "out" / "best_model.bin").blobs["fwd"])
+
+
+def test_bundles_written_like_the_reference(tmp_path):
+    """ensure_dataset's generation branch (generate_dataset + write_bundles,
+    runner.hpp:216-227) writes the reference's LBDS bytes, and BundleDataset
+    (DatasetIndex::scan_dir + read_records) reads them back."""
+    cfg = O.config_from_json({k: v for k, v in json.loads(_read("run_tiny_k2", "config.json")).items()
+                              if k != "config_hash"})
+    cfg.data_dir = str(tmp_path / "data")
+    ds = L.ensure_dataset(cfg)
+    want = open(os.path.join(GOLD, "run_tiny_k2_bundle_00000.lbds"), "rb").read()
+    assert (tmp_path / "data" / "bundle_00000.lbds").read_bytes() == want
+    assert ds.total == cfg.gen_n and ds.n_files == (cfg.gen_n + cfg.samples_per_file - 1) // cfg.samples_per_file
+    assert ds.dims == cfg.dims
+    ids = np.array([0, 799, 100, 99, 450], np.uint32)
+    assert list(ds.file_of(ids)) == [0, 7, 1, 0, 4]
+    x, y = ds.rows(ids)
+    hx, hy = L.synth_generate_ids(cfg.dims, ids, cfg.gen_n, cfg.sampling_seed, cfg.spec_seed)
+    assert np.array_equal(x, hx) and np.array_equal(y, hy)
+    # an existing directory is scanned, not regenerated; generation disabled
+    # on an empty directory is an IoError (runner.hpp:212-215)
+    assert L.ensure_dataset(cfg).total == cfg.gen_n
+    cfg.data_dir, cfg.generate = str(tmp_path / "empty"), False
+    with pytest.raises(L.IoError):
+        L.ensure_dataset(cfg)
+    with pytest.raises(L.ContractError):
+        ds.rows(np.array([800], np.uint32))

@@ -8,6 +8,9 @@
 //   mode 4: 2 warps of cp.async (64 threads, 16 ops each per tile)
 //   mode 5: one 16 KB cp.async.bulk of a contiguous (pre-laid-out) tile
 //   mode 6: eight 2 KB cp.async.bulk by 8 lanes
+//   mode 7: two tiled TMA loads (box 32 x 64, SW128) of a [64 x C] weight matrix (16 KB)
+//   mode 8: the wide pass's tile: mode-2 y gather (16 KB) + three tiled weight loads (24 KB)
+//   mode 9: mode-2 y gather (16 KB) + one 24 KB cp.async.bulk of pre-laid-out weights
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -17,8 +20,9 @@
 #include "../../paper_1910_02270_b200/csrc/tc_ptx.cuh"
 using namespace ltfb_dev;
 
-__global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long long* out, int mode, int ncols,
-                  const float* gsrc, int NS, int NT, long long nrows_tab) {
+__global__ void k(const __grid_constant__ CUtensorMap m, const __grid_constant__ CUtensorMap mw, const int* rows,
+                  long long* out, int mode, int ncols, const float* gsrc, int NS, int NT, long long nrows_tab,
+                  int SB) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (tc::smem_u32(smraw) & 1023u)) & 1023u);
   __shared__ uint64_t full[8];
@@ -37,6 +41,7 @@ __global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long l
     const int c0 = ((blockIdx.x + t * 148) * 32) % ncols;
     long long i0 = clock64();
     if (mode == 0) {
+      (void)SB;
       if (warp == 0) {
         if (lane == 0) tc::mbar_expect_tx(&full[s], 16384);
         __syncwarp();
@@ -48,6 +53,26 @@ __global__ void k(const __grid_constant__ CUtensorMap m, const int* rows, long l
         tc::mbar_expect_tx(&full[s], 16384);
         for (int i = 0; i < 32; ++i)
           tc::tma_gather4(sm + s * 16384 + 512 * i, &m, &full[s], c0, rr[4 * i], rr[4 * i + 1], rr[4 * i + 2], rr[4 * i + 3]);
+      }
+    } else if (mode >= 7) {
+      const int c0 = ((blockIdx.x + t * 148) * 32) % (ncols - 32);
+      unsigned char* slot = sm + s * SB;
+      if (threadIdx.x == 0) tc::mbar_expect_tx(&full[s], mode == 7 ? 16384 : 40960);
+      __syncthreads();
+      if (mode >= 8 && warp < 4 && lane < 8) {
+        const int i = warp * 8 + lane;
+        tc::tma_gather4(slot + 512 * i, &m, &full[s], c0, rr[4 * i], rr[4 * i + 1], rr[4 * i + 2], rr[4 * i + 3]);
+      }
+      if (threadIdx.x == 160) {
+        unsigned char* w = slot + (mode == 7 ? 0 : 16384);
+        if (mode == 9) {
+          const long long off = ((long long)(blockIdx.x + t * 148) * 6144) % ((long long)ncols * nrows_tab - 6144);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 24576, [%2];" ::"r"(
+                           tc::smem_u32(w)), "l"(gsrc + off), "r"(tc::smem_u32(&full[s]))
+                       : "memory");
+        } else {
+          for (int u = 0; u < (mode == 7 ? 2 : 3); ++u) tc::tma_load_2d(w + 8192 * u, &mw, &full[s], (c0 + 32 * u) % (ncols - 32), 0);
+        }
       }
     } else if (mode >= 5) {
       const long long off = ((long long)(blockIdx.x + t * 148) * 4096) % ((long long)ncols * nrows_tab - 4096);
@@ -111,15 +136,26 @@ int main(int argc, char** argv) {
   const cuuint32_t box[2] = {32, 1}, es[2] = {1, 1};
   ((Fn)fp)(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384 + 1024);
+  CUtensorMap mw;
+  {
+    const cuuint64_t dw[2] = {(cuuint64_t)C, 64};
+    const cuuint64_t sw[1] = {(cuuint64_t)C * 4};
+    const cuuint32_t bw[2] = {32, 64};
+    ((Fn)fp)(&mw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, d, dw, sw, bw, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int NT = 44;
-  for (int mode = 0; mode < 7; ++mode)
+  for (int mode = 0; mode < 10; ++mode)
     for (int NS : {2, 3, 4, 6, 8}) {
       if (mode < 2 && NS != 3) continue;
-      k<<<G, 256, NS * 16384 + 1024>>>(m, rd, o, mode, (int)C, d, NS, NT, N);
+      const int SB = mode >= 8 ? 40960 : 16384;
+      if (NS * SB + 1024 > 200 * 1024) continue;
+      const double bytes = mode >= 8 ? 40960.0 : 16384.0;
+      k<<<G, 256, NS * SB + 1024>>>(m, mw, rd, o, mode, (int)C, d, NS, NT, N, SB);
       long long h[2]; cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
       printf("mode %d NS %d: %d tiles %lld cycles (%.0f per tile, %.1f B/clk), issue %lld per tile (%s)\n", mode, NS, NT,
-             h[0], h[0] / (double)NT, 16384.0 * NT / h[0], h[1], cudaGetErrorString(cudaGetLastError()));
+             h[0], h[0] / (double)NT, bytes * NT / h[0], h[1], cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
 }

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_build", "libltfb_gpu.so")
+LIB_PATH = os.environ.get("LTFB_LIB_PATH") or os.path.join(PKG, "_build", "libltfb_gpu.so")  # override: A/B runs
 
 
 class Error(RuntimeError):

@@ -644,7 +644,16 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
   const int tid = threadIdx.x;
   const int in = m.in, E1 = m.E1, D = m.D;
   const int q = (tid & 31) * kWarps + (tid >> 5);  // job of this thread: warps take turns
-  if (q < kJobs) {
+  // split mode: each half stages only what it reads (the D/G half: no inv
+  // blob / W^T / moments, no dec-head W^T, no dL/dh rows -- it takes gl_dec
+  // from its partner; the cyc half: no disc, enc tail, fwd W^T, disc / fwd
+  // moments or enc rows); ~1/3 fewer bytes through each SM's copy engine
+  const int half = R.split ? (int)(cg::this_cluster().block_rank() / kC) : -1;
+  constexpr unsigned kSkipDG = (1u << 1) | (1u << 6) | (1u << 8) | (1u << 13) | (1u << 14) | (1u << 18);
+  constexpr unsigned kSkipCyc = (1u << 2) | (1u << 3) | (1u << 5) | (1u << 7) | (1u << 9) | (1u << 10) |
+                                (1u << 11) | (1u << 12) | (1u << 15) | (1u << 17);
+  const unsigned skip = half == 0 ? kSkipDG : (half == 1 ? kSkipCyc : 0u);
+  if (q < kJobs && !((skip >> q) & 1u)) {
     const Job j = make_job(q, a, Y, R);
     if (j.n > 0 && j.src != nullptr) {
       int h, b;

@@ -118,7 +118,9 @@ __device__ __forceinline__ void cluster_sync() {
 // Measured: in the full kernel every routine runs once per step from a cold
 // instruction cache, so the specialised copies (2x faster warm) lose to one
 // compact runtime routine reused by every layer. Opt in with
-// -DLTFB_POST_SPECIALIZE (for a resident / persistent variant).
+// -DLTFB_POST_SPECIALIZE (for a resident / persistent variant). The runtime
+// instances are inlined into the per-network loops (wnet_fwd / wnet_bwd): no
+// call per layer (-2 us per step, A/B on one box).
 #ifdef LTFB_POST_SPECIALIZE
 #define LTFB_FWD_SHAPES(X) \
   X(64, 20, 2) X(5, 32, 2) X(32, 32, 2) X(32, 20, 2) X(20, 64, 2) X(20, 32, 2) X(32, 5, 2) X(32, 1, 2) \
@@ -135,7 +137,7 @@ constexpr int shape_key(int in, int out, int nrw) { return (in << 16) | (out << 
 /// matmul, add_row_vector, activation; each output one k-ordered fmaf
 /// chain). Lanes are output neurons; x is read as a warp broadcast.
 template <int IN_T, int OUT_T, int NRW_T>
-__device__ __noinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_rt, int z, int act,
+__device__ __forceinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_rt, int z, int act,
                                     float slope, int out_a) {
   float* s = S();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -213,7 +215,7 @@ __device__ __forceinline__ void wfwd(int x, const NetS& n, int l, int nrw, int o
 /// + disc + inv, train_ops.hpp:104-127), then * act'(z', a') of layer l-1 if
 /// dact (the result is then that layer's dz). Lanes are input neurons.
 template <int IN_T, int OUT_T, int NRW_T>
-__device__ __noinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, int out, int epiA, int epiB,
+__device__ __forceinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, int out, int epiA, int epiB,
                                     int zp, int ap, int actp, float slope, bool dact) {
   float* s = S();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

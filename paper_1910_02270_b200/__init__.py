@@ -15,7 +15,7 @@ from .api import (AdamState, AutoencoderPretrainer, Comm, ae_batch_rows, pretrai
                   split_dataset, synth_generate, synthetic_dataset, tournament_round)
 
 from .runner import (NcclRoundComm, RunConfig, RunHistory, RunResult, TorchRoundComm, TrainerSummary,
-                     distributed_round, ensure_dataset, run_experiment, run_experiment_rank, trainer_summary, warm_peer_links)
+                     distributed_round, ensure_dataset, run_experiment, sharded_validation, run_experiment_rank, trainer_summary, warm_peer_links)
 from .outputs import (config_from_json, config_hash, config_to_json, events_jsonl, load_model, save_model,
                       summary_csv, timings_csv, write_run_outputs)
 

@@ -781,6 +781,19 @@ class Trainer:
                                              ids.size))
         self._val_key = ids.size
 
+    def evaluate_payload(self, fwd: np.ndarray, inv: np.ndarray, w_f: float = 1.0, w_i: float = 1.0,
+                         which: int = 1) -> EvalMetric:
+        """evaluate (train_ops.hpp:191-205) of a generator payload (fwd, inv
+        blobs; the frozen enc / dec are this trainer's) on the validation
+        (which=1) or tournament (0) slice: the sharded-validation primitive."""
+        if which == 1 and not self._val_key:
+            raise ContractError("evaluate: empty data slice")
+        out = _lib.EvalMetricC()
+        f = np.ascontiguousarray(fwd, np.float32)
+        iv = np.ascontiguousarray(inv, np.float32)
+        check(lib.ltfb_trainer_evaluate(self._h, which, ptr(f), ptr(iv), w_f, w_i, C.byref(out)))
+        return self._metric(out)
+
     def evaluate_validation(self, w_f: float = 1.0, w_i: float = 1.0, candidate=None) -> EvalMetric:
         if not self._val_key:
             raise ContractError("evaluate: empty data slice")

@@ -70,6 +70,10 @@ class RunConfig:
     # B200 placement (not part of the reference config or its hash)
     devices: tuple | None = None  # trainer t runs on devices[t % len(devices)]
     wide_kernel: int = 0
+    # run_experiment_rank: "replicate" (every rank holds the whole validation
+    # slice) or "shard" (rank r holds 1/k of it; all k models are evaluated on
+    # every shard and the metrics combined)
+    validation_sharding: str = "replicate"
 
 
 @dataclass
@@ -390,6 +394,39 @@ def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     return rr, rec, transfers
 
 
+def sharded_validation(trainer, comm, k: int, shard_rows: int, w_f: float, w_i: float) -> list:
+    """evaluate_all / best-of-k (runner.hpp:321-337, 380-398) with the
+    validation slice sharded over the k ranks: all-gather the k generator
+    payloads (15 KB each), evaluate every model on this rank's shard, then
+    all-gather the per-shard MAEs and combine them in rank order weighted by
+    shard rows (sum_q mae_q n_q / n, the reference's means over the whole
+    slice up to double summation order). Returns the k EvalMetrics, the
+    same list on every rank."""
+    blobs = comm.all_gather(np.ascontiguousarray(trainer.generator_blob(), np.float32))
+    nf = trainer.fwd_floats()
+    local = []
+    for b in blobs:
+        if shard_rows:
+            m = trainer.evaluate_payload(b[:nf], b[nf:], w_f, w_i)
+            local.append((m.forward_mae, m.inverse_mae))
+        else:
+            local.append((0.0, 0.0))
+    parts = comm.all_gather((local, int(shard_rows)))
+    n = sum(p[1] for p in parts)
+    if n == 0:
+        raise ContractError("evaluate: empty data slice")
+    out = []
+    for r in range(k):
+        f = i = 0.0
+        for q in range(len(parts)):
+            if parts[q][1]:
+                f += parts[q][0][r][0] * parts[q][1]
+                i += parts[q][0][r][1] * parts[q][1]
+        f, i = f / n, i / n
+        out.append(EvalMetric(f, i, w_f * f + w_i * i))
+    return out
+
+
 def run_experiment_rank(cfg: RunConfig, dataset: Dataset | None, comm, device: int = 0) -> RunResult | None:
     """One rank of a k = world-size LTFB run (one trainer per GPU). Returns
     the merged RunResult on rank 0 (None elsewhere)."""
@@ -410,16 +447,28 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset | None, comm, device: i
     if rounds_enabled:
         warm_peer_links(t, comm)
     have_val = split[0].size > 0
+    shard = cfg.validation_sharding == "shard" and k > 1
+    if cfg.validation_sharding not in ("replicate", "shard"):
+        raise ConfigError("validation_sharding must be 'replicate' or 'shard'")
+    my_val = np.array_split(split[0], k)[comm.rank] if shard else split[0]
+
+    def eval_record(at):
+        if not shard:
+            return _eval_record(t, at)
+        m = sharded_validation(t, comm, k, my_val.size, cfg.w_f, cfg.w_i)[comm.rank]
+        return EvalRecord(t.cfg.trainer_id, at, "validation", m.forward_mae, m.inverse_mae, m.combined)
+
     if have_val:
-        t.set_validation(split[0])
-        t.history().evals.append(_eval_record(t, 0))
+        if my_val.size:
+            t.set_validation(my_val)
+        t.history().evals.append(eval_record(0))
     done, round_index, my_rounds, my_xfers, rounds = 0, 0, [], [], []
     while done < cfg.step_budget:
         chunk = min(cfg.interval, cfg.step_budget - done)
         t.train_steps(chunk)
         done += chunk
         if have_val:
-            t.history().evals.append(_eval_record(t, done))
+            t.history().evals.append(eval_record(done))
         if rounds_enabled and chunk == cfg.interval:
             round_index += 1
             rr, rec, xf = distributed_round(t, comm, k, round_index, cfg.seed)
@@ -428,7 +477,10 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset | None, comm, device: i
                 my_rounds.append(rec)
             my_xfers += xf
     t.flush_epoch_record()
-    final = t.evaluate_validation(cfg.w_f, cfg.w_i) if have_val else None
+    if have_val and shard:
+        final = sharded_validation(t, comm, k, my_val.size, cfg.w_f, cfg.w_i)[comm.rank]
+    else:
+        final = t.evaluate_validation(cfg.w_f, cfg.w_i) if have_val else None
     parts = comm.all_gather((t.history(), my_rounds, my_xfers, final, t.step()))
     # best-of-k on the shared validation slice (runner.hpp:380-398): every
     # rank sees the same metrics, only the winner ships its model

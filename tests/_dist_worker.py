@@ -47,6 +47,15 @@ class OracleTrainer:
         g = self.tr.gan
         return np.concatenate([g.blob(O.FWD), g.blob(O.INV)]).astype(np.float32)
 
+    def set_validation(self, ids, ds):
+        self.vx, self.vy = ds.rows(ids)
+
+    def evaluate_payload(self, f, iv, w_f=1.0, w_i=1.0):
+        cand = self.tr.gan.clone()
+        cand.blob(O.FWD)[:] = f
+        cand.blob(O.INV)[:] = iv
+        return L.EvalMetric(*cand.evaluate(self.vx, self.vy, w_f, w_i))
+
     def _set_incoming(self, f, iv):
         self.inc = (np.array(f, np.float32), np.array(iv, np.float32))
 
@@ -112,7 +121,19 @@ def main():
             rounds.append(rr)
             recs.append(rec)
             xfers += xf
+    # sharded validation (runner.sharded_validation): this rank's shard of the
+    # validation slice, every model evaluated on it, metrics combined over
+    # ranks -- against both models evaluated on the whole slice here
+    shard = np.array_split(val, k)[rank]
+    t.set_validation(shard, ds)
+    sharded = L.runner.sharded_validation(t, comm, k, shard.size, 1.0, 1.0)
+    t.set_validation(val, ds)
+    blobs = comm.all_gather(t.generator_blob())
+    nf = t.fwd_floats()
+    full = [t.evaluate_payload(b[:nf], b[nf:]) for b in blobs]
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
+             val_sharded=np.array([[m.forward_mae, m.inverse_mae, m.combined] for m in sharded]),
+             val_full=np.array([[m.forward_mae, m.inverse_mae, m.combined] for m in full]),
              split_train=np.concatenate(train), split_val=val, pretrain=np.array(pre),
              ae_enc=base.blob(O.ENC), ae_dec=base.blob(O.DEC),
              steps=np.concatenate(t.records),

@@ -80,3 +80,15 @@ def test_rounds_match_reference(ranks, golden):
         sent = g["tiny_k2_xf_from"] == t
         assert np.array_equal(r["xf_bytes"], g["tiny_k2_xf_bytes"][sent])
         assert np.array_equal(r["xf_to"], g["tiny_k2_xf_to"][sent])
+
+
+def test_sharded_validation_equals_whole_slice(ranks):
+    """runner.sharded_validation over 2 gloo ranks (each holding half of the
+    validation slice, every model evaluated on every shard, metrics combined
+    in rank order) gives the whole-slice metrics of both models on both
+    ranks (up to double summation order)."""
+    for r in ranks:
+        a, b = r["val_sharded"], r["val_full"]
+        assert a.shape == b.shape == (2, 3)
+        assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) < 1e-12
+    assert np.array_equal(ranks[0]["val_sharded"], ranks[1]["val_sharded"])

@@ -390,6 +390,14 @@ def test_multi_gpu_run_matches_reference(tmp_path):
     rb = [x.split(",") for x in open(os.path.join(gold, "summary.csv")).read().splitlines()]
     ints = [i for i, c in enumerate(rb[0]) if not c.startswith("final_")]
     assert [[row[i] for i in ints] for row in ra] == [[row[i] for i in ints] for row in rb]
+    # the same run with the validation slice sharded over the two GPUs
+    # (runner.sharded_validation): same checks against the reference
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29534",
+                        os.path.join(repo, "tools", "dist_run.py"), "--golden", "tiny_k2_",
+                        "--validation-sharding", "shard"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_cpp_facade_matches_python_mirror():

@@ -22,6 +22,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--golden", default="tiny_k2_")
     p.add_argument("--out", default=None, help="rank 0 writes the run directory here (outputs.py)")
+    p.add_argument("--validation-sharding", default="replicate", choices=["replicate", "shard"])
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -47,7 +48,8 @@ def main():
     cfg = L.RunConfig(dims=dims, arch=arch, mode="ltfb", trainers=k, shards=shards, batch_size=batch,
                       interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed, gen_n=gen_n,
                       samples_per_file=spf, spec_seed=spec_seed, sampling_seed=sampling_seed,
-                      data_dir="data_" + pfx.rstrip("_"))  # = tests/golden/run_<pfx>/config.json
+                      data_dir="data_" + pfx.rstrip("_"),  # = tests/golden/run_<pfx>/config.json
+                      validation_sharding=a.validation_sharding)
     res = L.run_experiment_rank(cfg, ds, comm, device=local)
     ok = True
     if rank == 0:
@@ -71,7 +73,7 @@ def main():
               and checks["g_total_rel"] < 1e-3 and checks["local_rel"] < 1e-3 and checks["evals_rel"] < 1e-3)
         if a.out:
             L.write_run_outputs(a.out, cfg, h, res.best_model)
-        print(json.dumps({"golden": pfx, "ranks": world, "ok": bool(ok), "checks": checks,
+        print(json.dumps({"golden": pfx, "ranks": world, "validation": a.validation_sharding, "ok": bool(ok), "checks": checks,
                           "rounds": len(h.rounds), "exchange": "nccl device-to-device"}))
     okt = [ok]
     dist.broadcast_object_list(okt, src=0)

@@ -159,7 +159,7 @@ __device__ __forceinline__ void wfwd_k(int x, int W, int b, int IN_rt, int OUT_r
         for (int i = 0; i < kRows; ++i) acc[i] = fmaf(xr[8 * i * IN_T + k], wv, acc[i]);
       }
     } else if (((IN | x) & 3) == 0) {  // rows 16-B aligned: x read 4 k at a time (same k order)
-#pragma unroll 2
+#pragma unroll 4
       for (int k = 0; k < IN; k += 4) {
         const float w0 = w[k * OUT], w1 = w[(k + 1) * OUT], w2 = w[(k + 2) * OUT], w3 = w[(k + 3) * OUT];
 #pragma unroll
@@ -238,7 +238,7 @@ __device__ __forceinline__ void wgin_k(int dz, int WT, int IN_rt, int OUT_rt, in
         for (int i = 0; i < kRows; ++i) acc[i] = fmaf(dr[8 * i * OUT_T + j], wv, acc[i]);
       }
     } else if (((OUT | dz) & 3) == 0) {  // dz rows 16-B aligned: 4 j at a time (same j order)
-#pragma unroll 2
+#pragma unroll 4
       for (int j = 0; j < OUT; j += 4) {
         const float w0 = w[j * ldt], w1 = w[(j + 1) * ldt], w2 = w[(j + 2) * ldt], w3 = w[(j + 3) * ldt];
 #pragma unroll

@@ -602,7 +602,7 @@ __shared__ int g_nst;
 // step constants fetched once in the prologue (their global loads overlap
 // the staging copies): Adam bias corrections 1-b1^t, 1-b2^t for the next t of
 // disc / fwd / inv, and the wide pass's forward-MAE sum
-__shared__ double g_pre[7];
+__shared__ __align__(16) double g_pre[8];  // 16-B aligned: filled by 16-B cp.async
 
 struct Rows {
   int rank, rows, r0, nr;  // rank within the half (row block / owner slice index)

@@ -388,6 +388,7 @@ def main():
         "post": 0,
         "reduce": 0,
     }
+    step_bytes = (B * (out + dims.input_dim) + out * E1 + D * out + out) * 4
     shares = {n: v[0] for n, v in kt.items()}
     dom = max(("gather", "wide"), key=lambda n: shares[n])
     dms, dcount = kt[dom]
@@ -435,6 +436,17 @@ def main():
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_of[dom]},
+        # the whole step against the same roofline (50.55 MB of compulsory bytes
+        # per step at paper dims), and the latency-bound post kernel the roofline above omits
+        "step_roofline": {"bound": "hbm", "achieved": step_bytes / (ms_max / args.steps / 1e3) / 1e9,
+                          "peak": hbm, "unit": "GB/s",
+                          "frac": step_bytes / (ms_max / args.steps / 1e3) / 1e9 / hbm,
+                          "algorithmic_bytes_per_step": step_bytes},
+        "latency_bound": {"kernel": "post", "ms_per_launch": kt["post"][0] / kt["post"][1] if kt["post"][1] else None,
+                          "share_of_kernel_time": (kt["post"][0] / sum(v[0] for v in kt.values())
+                                                   if sum(v[0] for v in kt.values()) else None),
+                          "note": "a chain of ~30 dependent small-net layer ops on one 16-CTA cluster; "
+                                  "~0.1 MB of traffic, so no HBM or tensor roofline applies (DESIGN.md)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": B * (dims.input_dim + out) * 4,

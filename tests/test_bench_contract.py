@@ -1,0 +1,47 @@
+"""bench.py's JSON line (the driver's contract): one short N=1 run through the
+product path, checked for the keys and the internal consistency the judge
+reads (value vs ms_per_step, roofline fractions, e2e bytes, launches)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_bench_line_contract():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    steps, warmup = 20, 3
+    p = subprocess.run([sys.executable, "bench.py", "--steps", str(steps), "--warmup", str(warmup),
+                        "--no-cpu-baseline"], cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "step_roofline",
+                "latency_bound", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == steps and d["warmup"] == warmup
+    B = d["config"]["global_batch"]
+    # value = samples of the K timed steps / their device time
+    assert d["value"] == pytest.approx(B / (d["ms_per_step"] / 1e3), rel=1e-6)
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9) and 0 < r["frac"] < 1
+    s = d["step_roofline"]
+    assert s["achieved"] == pytest.approx(s["algorithmic_bytes_per_step"] / (d["ms_per_step"] / 1e3) / 1e9,
+                                          rel=1e-6)
+    assert 0 < s["frac"] < r["frac"]  # the step is slower than its wide pass alone
+    out = d["config"]["output_dim"]
+    e = d["e2e"]
+    assert e["h2d_bytes_per_step"] == B * (5 + out) * 4 and e["d2h_bytes_per_step"] > 0
+    assert 0 < e["value"] < d["value"]
+    # the step graphs launch the wide pass and the post kernel every step
+    assert d["gpu_launches"] >= 2 * steps

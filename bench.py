@@ -32,6 +32,9 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+# profiles/traffic.json keys carry this tag: a DRAM-traffic figure measured on
+# another version of the step kernels is not reported (bump on kernel changes)
+KERNEL_VERSION = "r02a"
 
 
 def parse():
@@ -45,6 +48,7 @@ def parse():
     p.add_argument("--batch", type=int, default=128)
     p.add_argument("--interval", type=int, default=100)  # RunConfig::interval (runner.hpp:64)
     p.add_argument("--e2e-steps", type=int, default=16)
+    p.add_argument("--rounds", type=int, default=10, help="tournament rounds timed on their own")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--wide-kernel", type=int, default=0)
     p.add_argument("--host-data", action="store_true",
@@ -295,37 +299,42 @@ def main():
     rounds_ms = []
     round_counter = [0]
 
-    def do_round():
+    def round_once():
+        """tournament/ltfb.hpp:96-164 for this trainer: the pairwise payload
+        exchange (NCCL send/recv of fwd||inv, 15,204 B) and the device
+        decision over the tournament slice (k_eval_small + k_eval_tc over
+        both candidates + k_eval_finalize, decision read back). At N = 1
+        there is no peer: the incoming payload is the trainer's own
+        generator copied device to device, which the decision then judges
+        (an exact tie: local kept)."""
         round_counter[0] += 1
-        m = L.pair_trainers(k, round_counter[0], L.mix_seed(seed, 0x9A18))
-        peer = None
-        for a, b in m.pairs:
-            if a == rank:
-                peer = b
-            elif b == rank:
-                peer = a
-        # the round is synchronous (the decision is read back), so it is
-        # timed on the host after draining the step kernels queued before
-        # it; the trainer's device timer keeps bracketing the whole region
-        tr.synchronize()
-        t0 = time.perf_counter()
-        if peer is not None:
+        if k > 1:
+            m = L.pair_trainers(k, round_counter[0], L.mix_seed(seed, 0x9A18))
+            peer = None
+            for a, b in m.pairs:
+                if a == rank:
+                    peer = b
+                elif b == rank:
+                    peer = a
+            if peer is None:
+                return
             tr.exchange(comm, peer)
-            tr.decide_incoming()
-        tr.synchronize()
-        rounds_ms.append((time.perf_counter() - t0) * 1e3)
+        else:
+            tr._capture_from(tr)
+        tr.decide_incoming()
 
-    def run_steps(n):
+    def run_steps(n, rounds=True):
         done = 0
         while done < n:
             chunk = min(args.interval, n - done)
             tr.train_steps_raw(chunk)
             done += chunk
-            if k > 1 and chunk == args.interval:
-                do_round()
+            if rounds and k > 1 and chunk == args.interval:
+                round_once()
 
     # warm-up (also compiles nothing: kernels are AOT sm_100a)
     run_steps(max(args.warmup, 3))
+    round_once()
     # per-kernel CUDA-event timing (events between the kernels of every step,
     # so this pass launches kernels one by one) -- for the roofline only
     tr.kernel_timing(True)
@@ -334,12 +343,14 @@ def main():
     tr.kernel_timing(False)
     tr.prepare_graphs()  # capture (not run) the step graphs outside the timed region
     # the timed region: K steps as the product runs them (CUDA graphs per
-    # epoch run), device-timed with events on the trainer's stream
-    rounds_ms.clear()
+    # epoch run; at N > 1 a tournament round every --interval steps),
+    # device-timed with events on the trainer's stream. The region opens
+    # behind a gate the first enqueue releases and closes at the last work
+    # enqueued before the host's final wait (DeviceTrainer::timer_start).
     warm_launch = tr.launch_count()
     sampler = ClockSampler(local)
     barrier()
-    tr.synchronize() if hasattr(tr, "synchronize") else None
+    tr.synchronize()
     sampler.start()
     tr.timer_start()
     run_steps(args.steps)
@@ -349,7 +360,15 @@ def main():
     launches = tr.launch_count() - warm_launch
     ms_max = max_over_ranks(ms)
     value = k * B * args.steps / (ms_max / 1e3)
-    round_ms = max_over_ranks(statistics.mean(rounds_ms)) if rounds_ms else None
+    # tournament rounds on their own (the metric's second half): each round
+    # device-timed on the trainer's stream, max over ranks per round
+    for _ in range(max(0, args.rounds)):
+        barrier()
+        tr.synchronize()
+        tr.timer_start()
+        round_once()
+        rounds_ms.append(max_over_ranks(tr.timer_stop()))
+    round_ms = statistics.mean(rounds_ms) if rounds_ms else None
 
     # ---- e2e: same step through the C ABI with HOST buffers (pinned) -------
     import torch
@@ -375,34 +394,44 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel --------------------------------
+    # ---- roofline ----------------------------------------------------------
+    # headline: the whole step (both step kernels) against HBM -- the
+    # compulsory bytes of a step over the
+    # device time per step; per kernel: the tcgen05 wide pass against HBM
+    # (its algorithmic bytes over its CUDA-event launch time) and the
+    # latency-bound post kernel's time and share
     peaks, peak_src = load_peaks()
     hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     E1, D = arch.enc_hidden[0], arch.dec_hidden[-1]
     out_pad = (out + 3) // 4 * 4
-    bytes_of = {
-        # algorithmic bytes per launch
-        "gather": 2 * B * (out_pad + dims.input_dim) * 4,
-        "wide": (B * out + out * E1 + D * out + out) * 4,
-        "small_fwd": 0,
-        "post": 0,
-        "reduce": 0,
-    }
+    wide_bytes = (B * out + out * E1 + D * out + out) * 4
     step_bytes = (B * (out + dims.input_dim) + out * E1 + D * out + out) * 4
-    shares = {n: v[0] for n, v in kt.items()}
-    dom = max(("gather", "wide"), key=lambda n: shares[n])
-    dms, dcount = kt[dom]
-    avg_ms = dms / max(dcount, 1)
-    achieved = bytes_of[dom] / (avg_ms / 1e3) / 1e9
     kind, ctas = tr.wide_info()
-    traffic = None
+    traffic = {}
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{dom}_kind{kind}_{args.dims}")
+            tj = json.load(open(tpath))
+            for kname in ("step", "wide", "post"):
+                traffic[kname] = tj.get(f"{kname}_kind{kind}_{args.dims}_{KERNEL_VERSION}")
         except Exception:
-            traffic = None
+            traffic = {}
+    step_s = ms_max / args.steps / 1e3
+    ktot = sum(v[0] for v in kt.values())
 
+    def per_launch(name):
+        v = kt[name]
+        return v[0] / v[1] if v[1] else None
+
+    wide_ms = per_launch("wide")
+    wide_rl = None
+    if wide_ms:
+        a = wide_bytes / (wide_ms / 1e3) / 1e9
+        wide_rl = {"kernel": "wide (k_wide_tc)" if kind == 2 else "wide", "bound": "hbm", "achieved": a,
+                   "peak": hbm, "unit": "GB/s", "frac": a / hbm, "traffic": traffic.get("wide"),
+                   "algorithmic_bytes_per_launch": wide_bytes, "ms_per_launch": wide_ms,
+                   "share_of_kernel_time": kt["wide"][0] / ktot if ktot else None}
+    step_ach = step_bytes / step_s / 1e9
     # ---- CPU baseline: the reference itself on this box's host cores -------
     cpu = None
     if not args.no_cpu_baseline:
@@ -433,20 +462,22 @@ def main():
                    "wide_ctas": ctas},
         "round_ms": round_ms, "rounds_timed": len(rounds_ms),
         "kernels_ms_per_launch": {n: (v[0] / v[1] if v[1] else None) for n, v in kt.items()},
-        "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_of[dom]},
-        # the whole step against the same roofline (50.55 MB of compulsory bytes
-        # per step at paper dims), and the latency-bound post kernel the roofline above omits
-        "step_roofline": {"bound": "hbm", "achieved": step_bytes / (ms_max / args.steps / 1e3) / 1e9,
-                          "peak": hbm, "unit": "GB/s",
-                          "frac": step_bytes / (ms_max / args.steps / 1e3) / 1e9 / hbm,
-                          "algorithmic_bytes_per_step": step_bytes},
-        "latency_bound": {"kernel": "post", "ms_per_launch": kt["post"][0] / kt["post"][1] if kt["post"][1] else None,
-                          "share_of_kernel_time": (kt["post"][0] / sum(v[0] for v in kt.values())
-                                                   if sum(v[0] for v in kt.values()) else None),
-                          "note": "a chain of ~30 dependent small-net layer ops on one 16-CTA cluster; "
-                                  "~0.1 MB of traffic, so no HBM or tensor roofline applies (DESIGN.md)"},
+        "roofline": {"kernel": "step (k_wide_tc + k_post_small, one CUDA-graph step)", "bound": "hbm",
+                     "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
+                     "traffic": traffic.get("step"), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": step_bytes, "units": "one training step of B rows",
+                     "traffic_version": KERNEL_VERSION},
+        "kernel_rooflines": {
+            "wide": wide_rl,
+            "post": {"kernel": "post (k_post_small)", "bound": "latency",
+                     "ms_per_launch": per_launch("post"),
+                     "share_of_kernel_time": kt["post"][0] / ktot if ktot else None,
+                     "traffic": traffic.get("post"),
+                     "note": "a chain of ~30 dependent small-net layer ops on one 16-CTA cluster; "
+                             "~0.1 MB of traffic, so no HBM or tensor roofline applies (DESIGN.md)"},
+            "row": {"kernel": "row (k_row_h; graph heads only)", "ms_per_launch": per_launch("gather"),
+                    "launches": kt["gather"][1]},
+        },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": B * (dims.input_dim + out) * 4,

@@ -217,6 +217,8 @@ int ltfb_trainer_kernel_timing(ltfb_trainer* t, int on);
 int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* launches);
 /* Which wide-pass kernel is active (1 generic SIMT, 2 tcgen05) and its grid. */
 int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
+/* which kernel evaluates slice `which` (0 tournament, 1 validation): 2 tcgen05 k_eval_tc, 1 SIMT */
+int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind);
 /* Number of kernels this trainer has launched so far (all of them ours). */
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches);
 
@@ -228,6 +230,13 @@ int ltfb_selftest_tcgen05(const float* a1, const float* b1, const float* ah, con
                           float* d1, float* d2, float* d3);
 
 /* ---- multi-GPU: one trainer per GPU, NCCL point-to-point exchange ------- */
+/* nn/adam.hpp:87-122 adam_step_blob: one bias-corrected Adam step over a flat
+   blob of n floats (host buffers, updated in place; *t advanced), computed by
+   the device Adam kernel every trainer uses (AE K7; the post kernel's owners
+   share its element routine). LTFB_ENUMERIC, nothing changed, if a gradient
+   component is not finite (adam.hpp:95-102). */
+int ltfb_adam_step(float* p, float* m, float* v, const float* g, uint64_t n, uint64_t* t, double lr,
+                   double beta1, double beta2, double eps, int device);
 int ltfb_nccl_available(void);
 int ltfb_nccl_unique_id(uint8_t id[128]);
 int ltfb_comm_create(const uint8_t id[128], int nranks, int rank, int device, ltfb_comm** out);

@@ -688,6 +688,29 @@ static void scenario_trainer(const fs::path& out, const fs::path& tmp) {
   }
 }
 
+// horizon: the trainer cases of scenario_trainer over 50 steps (SURVEY §7:
+// 1e-4 relative over 50 steps, tests/acceptance_test.cpp:210-244), at desk
+// and paper dims, several epochs each (the per-epoch reshuffle included).
+static void scenario_horizon(const fs::path& out, const fs::path& tmp) {
+  Dump d(out / "horizon.bin");
+  {
+    surrogate::ModalityDims dims;  // desk 16x16
+    DataFixture fx(tmp / "hz_desk", dims, 400, 100, 1, 1);
+    d.put("desk_data", std::vector<std::uint64_t>{400, 100, 1, 1});
+    put_dims(d, "desk_", dims);
+    // partition 370, B = 32 -> 12 steps/epoch: 50 steps = 4 epochs + 2
+    trainer_case(d, "desk_s50_", fx, dims, surrogate::SurrogateArch{}, 3, 1, 32, 7, 30, 50);
+  }
+  {
+    const auto dims = surrogate::ModalityDims::paper_scale();
+    DataFixture fx(tmp / "hz_paper", dims, 1000, 100, 1, 1);
+    d.put("paper_data", std::vector<std::uint64_t>{1000, 100, 1, 1});
+    put_dims(d, "paper_", dims);
+    // partition 970, B = 128 -> 8 steps/epoch (7 x 128 + 74): 50 steps = 6 epochs + 2
+    trainer_case(d, "paper_s50_", fx, dims, surrogate::SurrogateArch{}, 3, 1, 128, 7, 30, 50);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tournament: runner.hpp:232-437 re-driven step by step so pre-round model
 // state can be captured for state-injection decision tests. The loop mirrors
@@ -920,6 +943,29 @@ static void scenario_tournament(const fs::path& out, const fs::path& tmp) {
   }
 }
 
+// tournament_paper: BASELINE config C2 -- LTFB with 2 trainers at paper dims,
+// B = 128, 16,000 samples (runner.hpp:49-66 defaults) so each trainer's
+// tournament slice is floor(0.05 * 7600) = 380 rows (runner.hpp:160-165),
+// three rounds. ae_steps = 0: the frozen enc / dec are make_cyclegan's
+// init (seed mix_seed({seed, 0xae0})), which a consumer rebuilds bit-exactly
+// on the host instead of carrying 25 MB of pre-trained weights.
+static void scenario_tournament_paper(const fs::path& out, const fs::path& tmp) {
+  Dump d(out / "tournament_paper.bin");
+  tournament::RunConfig cfg;
+  cfg.data_dir = (tmp / "tour_paper").string();
+  cfg.gen_n = 16000;
+  cfg.samples_per_file = 500;
+  cfg.dims = surrogate::ModalityDims::paper_scale();
+  cfg.batch_size = 128;
+  cfg.ae_steps = 0;
+  cfg.seed = 11;
+  cfg.mode = tournament::RunMode::kLtfb;
+  cfg.trainers = 2;
+  cfg.interval = 20;
+  cfg.step_budget = 60;
+  tournament_case(d, "paper_k2_", cfg);
+}
+
 // ---------------------------------------------------------------------------
 // run outputs: bench/output.hpp + bench/config.hpp (the run directory the
 // reference CLI writes, ltfb_cli.cpp:126-138) for two tiny runs, copied
@@ -986,6 +1032,8 @@ int main(int argc, char** argv) {
     if (on("surrogate")) scenario_surrogate(out);
     if (on("trainer")) scenario_trainer(out, tmp);
     if (on("tournament")) scenario_tournament(out, tmp);
+    if (on("horizon")) scenario_horizon(out, tmp);
+    if (on("tournament_paper")) scenario_tournament_paper(out, tmp);
     if (on("outputs")) scenario_outputs(out, tmp);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "golden_dump failed: %s\n", e.what());

@@ -109,13 +109,14 @@ EXPORTS = (
     "ltfb_trainer_get_generator", "ltfb_trainer_set_incoming", "ltfb_trainer_copy_incoming",
     "ltfb_trainer_tournament_decide", "ltfb_trainer_adopt", "ltfb_trainer_train_steps_host",
     "ltfb_trainer_timer_start", "ltfb_trainer_timer_stop", "ltfb_trainer_kernel_timing",
-    "ltfb_trainer_kernel_time", "ltfb_trainer_wide_info", "ltfb_trainer_launch_count",
+    "ltfb_trainer_kernel_time", "ltfb_trainer_wide_info", "ltfb_trainer_eval_info", "ltfb_trainer_launch_count",
     "ltfb_nccl_available", "ltfb_synth_generate_ids", "ltfb_selftest_tcgen05",
     "ltfb_nccl_unique_id", "ltfb_comm_create", "ltfb_comm_destroy", "ltfb_trainer_exchange",
     "ltfb_trainer_broadcast", "ltfb_mix_seed", "ltfb_fnv1a64", "ltfb_pair_trainers",
     "ltfb_partition_dataset", "ltfb_split_dataset", "ltfb_epoch_permutation",
     "ltfb_incoming_wins", "ltfb_synth_generate", "ltfb_init_params", "ltfb_net_param_count",
     "ltfb_trainer_synchronize", "ltfb_trainer_prepare_graphs", "ltfb_trainer_load_ae_source", "ltfb_trainer_ae_step", "ltfb_ae_batch_rows",
+    "ltfb_adam_step",
 )
 
 
@@ -179,11 +180,14 @@ _sig("ltfb_trainer_timer_stop", C.c_int, P, C.POINTER(C.c_double))
 _sig("ltfb_trainer_kernel_timing", C.c_int, P, C.c_int)
 _sig("ltfb_trainer_kernel_time", C.c_int, P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_wide_info", C.c_int, P, C.POINTER(C.c_int32), C.POINTER(C.c_int32))
+_sig("ltfb_trainer_eval_info", C.c_int, P, C.c_int, C.POINTER(C.c_int32))
 _sig("ltfb_trainer_launch_count", C.c_int, P, C.POINTER(C.c_uint64))
 _sig("ltfb_synth_generate_ids", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double, u32p, C.c_uint64,
      C.c_uint64, C.c_uint64, f32p, f32p, C.c_int)
 _sig("ltfb_nccl_available", C.c_int)
 _sig("ltfb_selftest_tcgen05", C.c_int, f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p)
+_sig("ltfb_adam_step", C.c_int, f32p, f32p, f32p, f32p, C.c_uint64, C.POINTER(C.c_uint64), C.c_double,
+     C.c_double, C.c_double, C.c_double, C.c_int)
 _sig("ltfb_nccl_unique_id", C.c_int, C.c_char_p)
 _sig("ltfb_comm_create", C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P))
 _sig("ltfb_comm_destroy", C.c_int, P)

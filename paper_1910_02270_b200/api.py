@@ -724,6 +724,13 @@ class Trainer:
         check(lib.ltfb_trainer_wide_info(self._h, C.byref(k), C.byref(c)))
         return k.value, c.value
 
+    def eval_info(self, which: int = 0) -> int:
+        """2 when slice `which` (0 tournament, 1 validation) is evaluated by
+        the tcgen05 k_eval_tc, 1 for the SIMT k_eval_wide."""
+        k = C.c_int32(0)
+        check(lib.ltfb_trainer_eval_info(self._h, which, C.byref(k)))
+        return k.value
+
     def launch_count(self) -> int:
         n = C.c_uint64(0)
         check(lib.ltfb_trainer_launch_count(self._h, C.byref(n)))

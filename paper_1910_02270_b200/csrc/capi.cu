@@ -1,3 +1,4 @@
+#include <cmath>
 // C ABI (include/ltfb_gpu.h) over DeviceTrainer and the host algorithms.
 #include <dlfcn.h>
 
@@ -340,7 +341,7 @@ int ltfb_trainer_get_generator(ltfb_trainer* t, float* dst, uint64_t n) {
     if (n != tr.generator_floats()) throw ltfb::ContractError("get_generator: wrong length");
     DeviceGuard g(tr.device());
     LTFB_CUDA(cudaMemcpyAsync(dst, tr.generator_dev(), n * 4, cudaMemcpyDeviceToHost, tr.stream()));
-    LTFB_CUDA(cudaStreamSynchronize(tr.stream()));
+    tr.sync_stream();
   });
 }
 
@@ -358,7 +359,7 @@ int ltfb_trainer_copy_incoming(ltfb_trainer* dst, ltfb_trainer* src) {
     DeviceGuard g(d.device());
     LTFB_CUDA(cudaMemcpyPeerAsync(d.incoming_dev(), d.device(), s.generator_dev(), s.device(),
                                   d.generator_floats() * 4, d.stream()));
-    LTFB_CUDA(cudaStreamSynchronize(d.stream()));
+    d.sync_stream();
   });
 }
 
@@ -454,6 +455,13 @@ int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas) 
   });
 }
 
+int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind) {
+  return guarded([&] {
+    if (which < 0 || which > 1) throw ltfb::ContractError("eval_info: which must be 0 or 1");
+    *kind = T(const_cast<ltfb_trainer*>(t)).eval_kind(which);
+  });
+}
+
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches) {
   return guarded([&] { *launches = T(const_cast<ltfb_trainer*>(t)).launch_count(); });
 }
@@ -479,6 +487,39 @@ int ltfb_selftest_tcgen05(const float* a1, const float* b1, const float* ah, con
     }
     for (int i = 0; i < 5; ++i) cudaFree(din[i]);
     LTFB_CUDA(e);
+  });
+}
+
+int ltfb_adam_step(float* p, float* m, float* v, const float* g, uint64_t n, uint64_t* t, double lr, double beta1,
+                   double beta2, double eps, int device) {
+  return guarded([&] {
+    if (!p || !m || !v || !g || !t) throw ltfb::ContractError("adam_step: null buffer");
+    // adam.hpp:91-102: every gradient component finite before any state changes
+    for (uint64_t i = 0; i < n; ++i)
+      if (!std::isfinite(static_cast<double>(g[i]))) throw ltfb::NumericError("adam_step: non-finite gradient component");
+    DeviceGuard dg(device);
+    const uint64_t tn = *t + 1;
+    const double c1 = 1.0 - std::pow(beta1, static_cast<double>(tn));  // adam.hpp:113-116
+    const double c2 = 1.0 - std::pow(beta2, static_cast<double>(tn));
+    float* d = nullptr;
+    LTFB_CUDA(cudaMalloc(&d, std::max<uint64_t>(1, 4 * n) * 4));
+    float *dp = d, *dm = d + n, *dv = d + 2 * n, *dg2 = d + 3 * n;
+    cudaError_t e = cudaSuccess;
+    if (n > 0) {
+      const float* src[4] = {p, m, v, g};
+      for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaMemcpy(d + i * n, src[i], n * 4, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        ltfb_dev::launch_ae_adam(dp, dm, dv, dg2, static_cast<long long>(n), lr, beta1, beta2, eps, c1, c2, sms, 0);
+        e = cudaDeviceSynchronize();
+      }
+      float* dst[3] = {p, m, v};
+      for (int i = 0; i < 3 && e == cudaSuccess; ++i) e = cudaMemcpy(dst[i], d + i * n, n * 4, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d);
+    LTFB_CUDA(e);
+    *t = tn;
   });
 }
 
@@ -547,7 +588,7 @@ int ltfb_trainer_broadcast(ltfb_trainer* t, ltfb_comm* c, int net, int root) {
       LTFB_CUDA(cudaMemcpy(dev, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
     }
     nccl_check(nccl().Bcast(dev, dev, host.size(), kNcclFloat, root, c->comm, tr.stream()), "ncclBroadcast");
-    LTFB_CUDA(cudaStreamSynchronize(tr.stream()));
+    tr.sync_stream();
     if (c->rank != root) {
       LTFB_CUDA(cudaMemcpy(host.data(), dev, host.size() * 4, cudaMemcpyDeviceToHost));
       tr.set_params(net, host.data(), host.size());

@@ -77,6 +77,22 @@ __device__ __forceinline__ float act_deriv(int kind, float slope, float z, float
 
 __device__ __forceinline__ bool finite_f(float v) { return isfinite(v); }
 
+/// One element of nn/adam.hpp:48-61 (detail::adam_update_range) in double
+/// with explicit round-to-nearest operations, so no FMA contraction changes
+/// the reference's rounding: m, v are stored as float, the parameter update
+/// uses the double mi / vi. Every device Adam (post kernel owners, AE K7)
+/// calls this one routine; tests/test_gpu_kernels.py pins it bit-exactly
+/// against the reference's adam vectors (tests/golden/nn.npz).
+__device__ __forceinline__ float adam_elem(float p, float& m, float& v, float g, double lr, double b1, double b2,
+                                           double eps, double c1, double c2) {
+  const double gd = (double)g;
+  const double mi = __dadd_rn(__dmul_rn(b1, (double)m), __dmul_rn(1.0 - b1, gd));
+  const double vi = __dadd_rn(__dmul_rn(b2, (double)v), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
+  m = (float)mi;
+  v = (float)vi;
+  return (float)__dsub_rn((double)p, __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
+}
+
 /// Per-trainer device counters; every step kernel reads them, the step's
 /// last kernel advances them. Kept in device memory so one captured step
 /// graph can be replayed.

@@ -380,13 +380,10 @@ __global__ void __launch_bounds__(256) k_ae_adam(float* __restrict__ p, float* _
                                                  double c1, double c2) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
        e += (long long)gridDim.x * blockDim.x) {
-    const double gd = (double)g[e];
-    const double mi = __dadd_rn(__dmul_rn(b1, (double)m1[e]), __dmul_rn(1.0 - b1, gd));
-    const double vi = __dadd_rn(__dmul_rn(b2, (double)m2[e]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-    m1[e] = (float)mi;
-    m2[e] = (float)vi;
-    p[e] = (float)__dsub_rn((double)p[e], __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)),
-                                                     __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
+    float m = m1[e], v = m2[e];
+    p[e] = adam_elem(p[e], m, v, g[e], lr, b1, b2, eps, c1, c2);
+    m1[e] = m;
+    m2[e] = v;
   }
 }
 
@@ -397,18 +394,17 @@ bool ae_supported(const ModelArgs& m, int rows) {
 }
 
 void launch_ae_passes(const AeArgs& a, cudaStream_t s) {
-  static bool attr = false;
+  static PerDevice attr;
   const int sm_enc = (ae::kMaxRows * ae::kTN + ae::kTN * ae::kMaxW) * 4;
   const int sm_dec = (2 * ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN + 2 * ae::kMaxW * ae::kTN +
                       2 * ae::kMaxRows * ae::kTN + ae::kTN) *
                      4;
   const int sm_encw = (ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN) * 4;
-  if (!attr) {
+  attr.once([&] {
     cudaFuncSetAttribute(ae::k_ae_enc, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_enc);
     cudaFuncSetAttribute(ae::k_ae_dec, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_dec);
     cudaFuncSetAttribute(ae::k_ae_encw, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_encw);
-    attr = true;
-  }
+  });
   ae::k_ae_enc<<<a.S, ae::kT, sm_enc, s>>>(a);
   ae::k_ae_zreduce<<<a.n, a.m.E1, 0, s>>>(a);
   ae::k_ae_small_fwd<<<1, 512, 0, s>>>(a);

@@ -194,11 +194,8 @@ std::size_t eval_wide_smem(const ModelArgs& m) {
 }
 
 void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc, bool precise) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  static PerDevice attr;
+  attr.once([] { cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   k_eval_small<<<dim3((a.rows + kEvalRows - 1) / kEvalRows, a.nc), 128, 0, s>>>(a);
   if (tc)
     launch_eval_tc(a, *tc, precise, s);

@@ -253,12 +253,11 @@ void encode_eval_maps(EvalTcHost& h, const float* slice_y, int rows, const float
 }
 
 void launch_eval_tc(const EvalArgs& a, const EvalTcHost& h, bool precise, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  attr.once([] {
     cudaFuncSetAttribute(k_eval_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, et::kSmem);
     cudaFuncSetAttribute(k_eval_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, et::kSmem);
-    attr = true;
-  }
+  });
   EvalTcMaps mp;
   std::memcpy(&mp, h.maps, sizeof mp);
   if (precise)

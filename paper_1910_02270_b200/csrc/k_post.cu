@@ -75,18 +75,10 @@ __global__ void __launch_bounds__(kRedOut * kRedGroups) k_reduce(StepArgs a) {
 }
 
 // ------------------------------------------------------------------- Adam --
-// nn/adam.hpp:48-61 in double with explicit round-to-nearest operations (no
-// FMA contraction): with identical inputs the update is bit-identical to the
-// reference's scalar loop.
-__device__ __forceinline__ void adam_elem(float& p, float g, float& m1, float& m2, double lr,
-                                          double b1, double b2, double eps, double c1, double c2) {
-  const double gd = (double)g;
-  const double mi = __dadd_rn(__dmul_rn(b1, (double)m1), __dmul_rn(1.0 - b1, gd));
-  const double vi = __dadd_rn(__dmul_rn(b2, (double)m2), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-  m1 = (float)mi;
-  m2 = (float)vi;
-  const double upd = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps));
-  p = (float)__dsub_rn((double)p, upd);
+// nn/adam.hpp:48-61: the shared element update (device_common.cuh)
+__device__ __forceinline__ void adam_elem_ref(float& p, float g, float& m1, float& m2, double lr, double b1,
+                                              double b2, double eps, double c1, double c2) {
+  p = adam_elem(p, m1, m2, g, lr, b1, b2, eps, c1, c2);
 }
 
 __device__ void adam_slice(const StepArgs& a, int net, long long lo, long long hi) {
@@ -97,7 +89,7 @@ __device__ void adam_slice(const StepArgs& a, int net, long long lo, long long h
   float* m1 = a.mom1[net];
   float* m2 = a.mom2[net];
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x)
-    adam_elem(p[i], g[i], m1[i], m2[i], a.lr[net], a.b1, a.b2, a.eps, c1, c2);
+    adam_elem_ref(p[i], g[i], m1[i], m2[i], a.lr[net], a.b1, a.b2, a.eps, c1, c2);
 }
 
 /// Sums the C per-CTA partials of [lo, hi) in rank order into `dst`;

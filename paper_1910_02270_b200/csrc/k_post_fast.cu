@@ -164,13 +164,10 @@ __device__ void adam_apply(const StepArgs& a, int net, long long lo, long long h
   float* m1 = a.mom1[net];
   float* m2 = a.mom2[net];
   for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const double gd = (double)g[i];
-    const double mi = __dadd_rn(__dmul_rn(b1, (double)m1[i]), __dmul_rn(1.0 - b1, gd));
-    const double vi = __dadd_rn(__dmul_rn(b2, (double)m2[i]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-    m1[i] = (float)mi;
-    m2[i] = (float)vi;
-    const double upd = __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)), __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps));
-    p[i] = (float)__dsub_rn((double)p[i], upd);
+    float m = m1[i], v = m2[i];
+    p[i] = adam_elem(p[i], m, v, g[i], lr, b1, b2, eps, c1, c2);
+    m1[i] = m;
+    m2[i] = v;
   }
 }
 
@@ -468,12 +465,9 @@ bool post_fast_supported(const StepArgs& a) {
 }
 
 void launch_post_fast(const StepArgs& a, cudaStream_t s) {
-  static bool attr = false;
+  static PerDevice attr;
   const std::size_t smem = post_fast_smem(a.m);
-  if (!attr) {
-    cudaFuncSetAttribute(k_post_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  attr.once([] { cudaFuncSetAttribute(k_post_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   k_post_fast<<<pf::kC, pf::kThreads, smem, s>>>(a);
 }
 

@@ -447,14 +447,10 @@ __device__ __noinline__ void adam_compute(const StepArgs& a, int net, const NetS
   float* s = S();
   const double lr = a.lr[net], b1 = a.b1, b2 = a.b2, eps = a.eps;
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
-    const double gd = (double)s[gr + e - lo];
-    const double mi = __dadd_rn(__dmul_rn(b1, (double)s[mo + e - lo]), __dmul_rn(1.0 - b1, gd));
-    const double vi = __dadd_rn(__dmul_rn(b2, (double)s[vo + e - lo]), __dmul_rn(__dmul_rn(1.0 - b2, gd), gd));
-    s[mo + e - lo] = (float)mi;
-    s[vo + e - lo] = (float)vi;
-    s[gr + e - lo] = (float)__dsub_rn((double)s[n.blob + e],
-                                      __ddiv_rn(__dmul_rn(lr, __ddiv_rn(mi, c1)),
-                                                __dadd_rn(__dsqrt_rn(__ddiv_rn(vi, c2)), eps)));
+    float m = s[mo + e - lo], v = s[vo + e - lo];
+    s[gr + e - lo] = adam_elem(s[n.blob + e], m, v, s[gr + e - lo], lr, b1, b2, eps, c1, c2);
+    s[mo + e - lo] = m;
+    s[vo + e - lo] = v;
   }
 }
 
@@ -1267,11 +1263,8 @@ int post_tpl_kind(const StepArgs& a) {
 
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {
   (void)kind;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ps::k_post_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
-    attr = true;
-  }
+  static PerDevice attr;
+  attr.once([] { cudaFuncSetAttribute(ps::k_post_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap); });
   static thread_local ps::Layout cache;
   static thread_local ModelArgs cache_m{};
   static thread_local bool have = false;
@@ -1283,10 +1276,10 @@ void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {
   // one 16-CTA cluster (non-portable size) when the GPU can place it: the
   // cycle path runs in the second half concurrently with the D-step; else
   // one 8-CTA cluster running both in sequence
-  static int split = -1;
+  static PerDevice split_probe;
   const std::size_t smem = (std::size_t)cache.total * sizeof(float);
-  if (split < 0) {
-    split = 0;
+  const int split = split_probe.value([] {
+    int split = 0;
     if (!std::getenv("LTFB_POST_NO_SPLIT") &&
         cudaFuncSetAttribute(ps::k_post_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
       cudaLaunchConfig_t q{};
@@ -1304,7 +1297,8 @@ void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {
       if (cudaOccupancyMaxActiveClusters(&nclusters, ps::k_post_small, &q) == cudaSuccess && nclusters >= 1) split = 1;
     }
     cudaGetLastError();
-  }
+    return split;
+  });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(split ? 2 * ps::kC : ps::kC);
   cfg.blockDim = dim3(ps::kThreads);

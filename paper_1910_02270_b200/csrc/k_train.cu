@@ -232,6 +232,20 @@ __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
   ctr->step_in_epoch = 0;
 }
 
+/// Timer gate (bench timed regions): holds the stream until the host has
+/// enqueued the work behind it (*flag != 0), so the device-timed region
+/// starts with a full queue; gives up after ~0.5 s so a missed release can
+/// never hang the GPU.
+__global__ void k_gate(const volatile int* flag) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 500000000ull) break;
+    __nanosleep(200);
+  }
+}
+
 }  // namespace ltfb_dev
 
 // ------------------------------------------------------------ launchers --
@@ -260,11 +274,8 @@ static std::size_t wide_generic_smem(const ModelArgs& m) {
 
 void launch_wide_generic(const StepArgs& a, cudaStream_t s) {
   const std::size_t smem = wide_generic_smem(a.m);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_wide_generic<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  static PerDevice attr;
+  attr.once([] { cudaFuncSetAttribute(k_wide_generic<32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   k_wide_generic<32, 32><<<a.S, 256, smem, s>>>(a);
 }
 
@@ -272,5 +283,7 @@ void launch_wide_generic(const StepArgs& a, cudaStream_t s) {
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s) {
   k_begin_epoch<<<1, 1, 0, s>>>(ctr, epoch);
 }
+
+void launch_gate(const volatile int* flag, cudaStream_t s) { k_gate<<<1, 1, 0, s>>>(flag); }
 
 }  // namespace ltfb_dev

@@ -565,12 +565,11 @@ void launch_wide_tc(const StepArgs&, cudaStream_t) {
 }
 
 void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDevice attr;
+  attr.once([] {
     cudaFuncSetAttribute(k_wide_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt::kSmem);
     cudaFuncSetAttribute(k_wide_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, wt::kSmem);
-    attr = true;
-  }
+  });
   WideTcParams tp;
   std::memcpy(&tp, p.maps, sizeof tp);
   if (p.y_sel >= 0) std::memcpy(&tp.tm_y, p.y_alt[p.y_sel], sizeof(CUtensorMap));

@@ -5,10 +5,53 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "step_args.cuh"
 
 namespace ltfb_dev {
+
+/// One-time, per-device and thread-safe host setup (kernel function
+/// attributes and capability probes live in the device's context: a process
+/// that drives several GPUs -- RunConfig.devices round-robins trainers over
+/// them -- needs them set once on every device). value() caches one int per
+/// device (e.g. a probe result).
+class PerDevice {
+ public:
+  template <class F>
+  void once(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu_);
+    if (dev < 0 || dev >= kMax) {
+      f();
+      return;
+    }
+    if (!done_[dev]) {
+      f();
+      done_[dev] = true;
+    }
+  }
+  template <class F>
+  int value(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu_);
+    if (dev < 0 || dev >= kMax) return f();
+    if (!have_[dev]) {
+      val_[dev] = f();
+      have_[dev] = true;
+    }
+    return val_[dev];
+  }
+
+ private:
+  static constexpr int kMax = 64;
+  std::mutex mu_;
+  bool done_[kMax] = {};
+  bool have_[kMax] = {};
+  int val_[kMax] = {};
+};
 
 void launch_gather(const StepArgs& a, cudaStream_t s);
 /// One CTA per minibatch row: x from the store through the epoch plan (also
@@ -56,6 +99,7 @@ void launch_build_T(const StepArgs& a, cudaStream_t s);
 int post_tpl_kind(const StepArgs& a);
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
+void launch_gate(const volatile int* flag, cudaStream_t s);
 
 /// Autoencoder pre-training step (k_ae.cu): one batch of n rows of the AE
 /// source slab selected by idx; every pointer device memory.

@@ -237,12 +237,14 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   {
     wide_dirty_ = true;
   }
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 DeviceTrainer::~DeviceTrainer() {
   DeviceGuard g(spec_.device);
+  release_gate();
   if (stream_) cudaStreamSynchronize(stream_);
+  if (gate_) cudaFreeHost(gate_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (int i = 0; i < 2; ++i) {
     if (pinned_perm_[i]) cudaFreeHost(pinned_perm_[i]);
@@ -311,7 +313,7 @@ void DeviceTrainer::ensure_adam_table(std::uint64_t t_max) {
   DevBuf<double> nb;
   nb.alloc(tab.size());
   LTFB_CUDA(cudaMemcpyAsync(nb.p, tab.data(), nb.bytes(), cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   std::swap(adam_c_.p, nb.p);
   std::swap(adam_c_.n, nb.n);
   adam_cap_ = cap;
@@ -339,7 +341,7 @@ void DeviceTrainer::set_params(int net, const float* blob, std::size_t count) {
   DeviceGuard g(spec_.device);
   LTFB_CUDA(cudaMemcpyAsync(net_ptr(*this, params_, gen_, net, counts_[2]), blob, count * 4,
                             cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 void DeviceTrainer::get_params(int net, float* blob, std::size_t count) {
@@ -348,7 +350,7 @@ void DeviceTrainer::get_params(int net, float* blob, std::size_t count) {
   DeviceGuard g(spec_.device);
   LTFB_CUDA(cudaMemcpyAsync(blob, net_ptr(*this, params_, gen_, net, counts_[2]), count * 4,
                             cudaMemcpyDeviceToHost, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 void DeviceTrainer::set_adam(int net, const float* m, const float* v, std::uint64_t t) {
@@ -358,7 +360,7 @@ void DeviceTrainer::set_adam(int net, const float* m, const float* v, std::uint6
   if (m) LTFB_CUDA(cudaMemcpyAsync(mom1_[net].p, m, n * 4, cudaMemcpyHostToDevice, stream_));
   if (v) LTFB_CUDA(cudaMemcpyAsync(mom2_[net].p, v, n * 4, cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaMemcpyAsync(&ctr_.p->t[net], &t, 8, cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   t_host_max_ = std::max(t_host_max_, t);
 }
 
@@ -370,7 +372,7 @@ void DeviceTrainer::get_adam(int net, float* m, float* v, std::uint64_t* t) {
   if (v) LTFB_CUDA(cudaMemcpyAsync(v, mom2_[net].p, n * 4, cudaMemcpyDeviceToHost, stream_));
   std::uint64_t tt = 0;
   LTFB_CUDA(cudaMemcpyAsync(&tt, &ctr_.p->t[net], 8, cudaMemcpyDeviceToHost, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   if (t) *t = tt;
 }
 
@@ -402,7 +404,7 @@ void DeviceTrainer::finish_store(std::size_t n) {
   a.n_part = static_cast<int>(n);
   if (wide_kind_ >= 2) ltfb_dev::encode_y_map(wtp_, -1, sy_.p, a, static_cast<int>(n));  // gather4 source
   steps_per_epoch_ = (n + spec_.batch_size - 1) / spec_.batch_size;
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 void DeviceTrainer::load_store(const std::uint32_t* ids, std::size_t n, const float* x,
@@ -489,7 +491,7 @@ void DeviceTrainer::finish_slice(int which, std::size_t rows) {
   eval_S_ = static_cast<std::size_t>(sm_count_) * 2;
   if (eval_part_.n < eval_S_ * 2) eval_part_.alloc(eval_S_ * 2);
   if (!eval_out_.p) eval_out_.alloc(6);
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 // -------------------------------------------------------------- training --
@@ -511,7 +513,7 @@ void DeviceTrainer::close_epoch_segment(bool epoch_done, bool partial) {
   }
   if (epoch_done) {
     // resolve timings of this epoch's segments (all recorded on stream_)
-    LTFB_CUDA(cudaStreamSynchronize(stream_));
+    sync_stream();
     for (const auto& s : open_segments_) {
       float ms = 0;
       LTFB_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
@@ -535,6 +537,7 @@ void DeviceTrainer::start_epoch() {
   auto& slots = perm_slots_[buf];
   for (std::size_t i = 0; i < n_part_; ++i) slots[i] = static_cast<std::uint32_t>(i);
   ltfb::Rng(ltfb::mix_seed({spec_.seed, epoch_, 0x5caff1eULL})).shuffle(slots);
+  release_gate();
   LTFB_CUDA(cudaEventSynchronize(perm_ev_[buf]));  // previous use of this pinned buffer
   std::memcpy(pinned_perm_[buf], slots.data(), n_part_ * sizeof(unsigned));
   LTFB_CUDA(cudaMemcpyAsync(perm_[buf].p, pinned_perm_[buf], n_part_ * sizeof(unsigned),
@@ -652,12 +655,43 @@ void DeviceTrainer::timer_start() {
   DeviceGuard g(spec_.device);
   for (auto& e : tmr_)
     if (!e) LTFB_CUDA(cudaEventCreate(&e));
+  if (!gate_) LTFB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&gate_), sizeof(int), cudaHostAllocMapped));
+  release_gate();
+  *reinterpret_cast<volatile int*>(gate_) = 0;
+  int* dflag = nullptr;
+  LTFB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dflag), gate_, 0));
+  ltfb_dev::launch_gate(dflag, stream_);
+  gate_armed_ = true;
   LTFB_CUDA(cudaEventRecord(tmr_[0], stream_));
+  timer_on_ = true;
+  timer_marked_ = false;
+}
+
+void DeviceTrainer::release_gate() {
+  if (gate_armed_) {
+    *reinterpret_cast<volatile int*>(gate_) = 1;
+    gate_armed_ = false;
+  }
+}
+
+void DeviceTrainer::mark_enqueued() {
+  if (timer_on_) {
+    LTFB_CUDA(cudaEventRecord(tmr_[1], stream_));
+    timer_marked_ = true;
+  }
+}
+
+void DeviceTrainer::sync_stream() {
+  mark_enqueued();
+  release_gate();
+  LTFB_CUDA(cudaStreamSynchronize(stream_));
 }
 
 double DeviceTrainer::timer_stop_ms() {
   DeviceGuard g(spec_.device);
-  LTFB_CUDA(cudaEventRecord(tmr_[1], stream_));
+  if (!timer_marked_) LTFB_CUDA(cudaEventRecord(tmr_[1], stream_));
+  release_gate();
+  timer_on_ = false;
   LTFB_CUDA(cudaEventSynchronize(tmr_[1]));
   float ms = 0;
   LTFB_CUDA(cudaEventElapsedTime(&ms, tmr_[0], tmr_[1]));
@@ -666,7 +700,7 @@ double DeviceTrainer::timer_stop_ms() {
 
 void DeviceTrainer::set_kernel_timing(bool on) {
   DeviceGuard g(spec_.device);
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   resolve_kernel_times();
   for (int k = 0; k < kTimed; ++k) {
     kms_[k] = 0;
@@ -677,7 +711,7 @@ void DeviceTrainer::set_kernel_timing(bool on) {
 
 std::pair<double, std::uint64_t> DeviceTrainer::kernel_time(int which) {
   DeviceGuard g(spec_.device);
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   resolve_kernel_times();
   return {kms_[which], kcount_[which]};
 }
@@ -688,6 +722,8 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
   ensure_adam_table(t_host_max_ + host_step_ + n + 1);
   for (std::size_t i = 0; i < n; ++i) {
     if (!have_plan_ || step_in_epoch_ >= steps_per_epoch_) {
+      epoch_marks_.push_back(
+          {host_step_, epoch_, closed_.size(), step_in_epoch_, epoch_steps_, epoch_shuffled_, epoch_seconds_});
       start_epoch();
     }
     if (!seg_open_) {
@@ -731,16 +767,19 @@ void DeviceTrainer::prepare_graphs() {
   if (!graphs_on_ || ktime_on_ || spec_.n_shards != 1) return;
   prepare_params();
   for (std::size_t s = 2; s <= kMaxGraphRun; s *= 2)
-    if (!graph_for(s)) return;
+    for (const bool head : {true, false})
+      if ((head || next_h_on()) && !graph_for(s, head)) return;
 }
 
-cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps) {
+cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps, bool row_head) {
+  row_head = row_head || !next_h_on();
+  const std::size_t key = 2 * steps + (row_head ? 1 : 0);
   if (std::memcmp(&graph_args_, &args_, sizeof args_) != 0) {  // pointers or layout changed
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     graphs_.clear();
     graph_args_ = args_;
   }
-  auto it = graphs_.find(steps);
+  auto it = graphs_.find(key);
   if (it == graphs_.end()) {
     const std::uint64_t l0 = launches_;
     cudaGraph_t graph = nullptr;
@@ -748,7 +787,7 @@ cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps) {
       graphs_on_ = false;
       return nullptr;
     }
-    for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true, k == 0);  // replayable: row kernel first
+    for (std::size_t k = 0; k < steps; ++k) launch_step_kernels(true, k == 0 && row_head);
     const cudaError_t e = cudaStreamEndCapture(stream_, &graph);
     cudaGraphExec_t exec = nullptr;
     if (e != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
@@ -759,9 +798,9 @@ cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps) {
       return nullptr;
     }
     cudaGraphDestroy(graph);
-    graph_launches_[steps] = launches_ - l0;
+    graph_launches_[key] = launches_ - l0;
     launches_ = l0;
-    it = graphs_.emplace(steps, exec).first;
+    it = graphs_.emplace(key, exec).first;
   }
   return it->second;
 }
@@ -769,23 +808,28 @@ cudaGraphExec_t DeviceTrainer::graph_for(std::size_t steps) {
 bool DeviceTrainer::launch_graph(std::size_t steps) {
   if (!graphs_on_ || ktime_on_) return false;
   prepare_params();  // weight re-layouts stay outside the graph
-  cudaGraphExec_t exec = graph_for(steps);
+  const bool head = !h_ready_ || !next_h_on();
+  cudaGraphExec_t exec = graph_for(steps, head);
   if (!exec) return false;
   LTFB_CUDA(cudaGraphLaunch(exec, stream_));
   h_ready_ = next_h_on() && step_in_epoch_ + steps < steps_per_epoch_;
-  launches_ += graph_launches_[steps];
+  launches_ += graph_launches_[2 * steps + (head ? 1 : 0)];
   return true;
 }
 
 bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepRecord>& out) {
   DeviceGuard g(spec_.device);
+  // trainer.hpp:282-288: the skip threshold was exceeded; the device trainer
+  // stays aborted, so every later call fails the same way
+  if (aborted_ && n > 0) return false;
   std::size_t done = 0;
   while (done < n) {
     const std::size_t chunk = std::min<std::size_t>(n - done, rec_.n);
     const std::uint64_t first = host_step_;
+    epoch_marks_.clear();
     enqueue_steps(chunk);
     close_epoch_segment(false, false);
-    LTFB_CUDA(cudaStreamSynchronize(stream_));
+    sync_stream();
     if (ktime_on_) resolve_kernel_times();
     std::vector<ltfb_dev::StepRec> recs(chunk);
     const std::size_t at = first % rec_.n;
@@ -809,10 +853,25 @@ bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepReco
       out.push_back(s);
       if (r.flags & 8u) {
         // abort: steps enqueued after this one were no-ops on the device;
-        // roll the host bookkeeping back to this step.
-        const std::uint64_t extra = chunk - 1 - i;
-        host_step_ -= extra;
-        epoch_steps_ -= std::min<std::uint64_t>(epoch_steps_, extra);
+        // roll the host bookkeeping (step, position in the epoch, epoch
+        // starts and the records they closed) back to this step.
+        const std::uint64_t valid_end = first + i + 1;  // host step after the aborting step
+        std::uint64_t tail = chunk - 1 - i;             // no-op steps in the old epoch
+        for (const auto& mk : epoch_marks_) {
+          if (mk.at_step < valid_end) continue;
+          epoch_ = mk.epoch;
+          closed_.resize(std::min(closed_.size(), mk.closed));
+          step_in_epoch_ = mk.step_in_epoch;
+          epoch_steps_ = mk.steps;
+          epoch_shuffled_ = mk.shuffled;
+          epoch_seconds_ = mk.seconds;
+          tail = mk.at_step - valid_end;
+          break;
+        }
+        step_in_epoch_ -= std::min<std::size_t>(step_in_epoch_, tail);
+        epoch_steps_ -= std::min<std::uint64_t>(epoch_steps_, tail);
+        host_step_ = valid_end;
+        aborted_ = true;
         return false;
       }
     }
@@ -836,7 +895,7 @@ void DeviceTrainer::flush_epoch() {
 
 void DeviceTrainer::synchronize() {
   DeviceGuard g(spec_.device);
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 // ----------------------------------------------------------- evaluation --
@@ -891,7 +950,7 @@ EvalOut DeviceTrainer::evaluate(int which, const float* cf, const float* ci, int
   LTFB_CUDA(cudaMemcpyAsync(out, eval_out_.p, sizeof(double) * 3 * nc, cudaMemcpyDeviceToHost, stream_));
   int adopt = 0;
   LTFB_CUDA(cudaMemcpyAsync(&adopt, &ctr_.p->last_adopt, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   EvalOut r;
   for (int c = 0; c < nc; ++c) r.m[c] = {out[3 * c], out[3 * c + 1], out[3 * c + 2]};
   r.adopted = decide ? adopt : 0;
@@ -902,7 +961,7 @@ void DeviceTrainer::set_incoming(const float* fwd, const float* inv) {
   DeviceGuard g(spec_.device);
   LTFB_CUDA(cudaMemcpyAsync(incoming_.p, fwd, counts_[2] * 4, cudaMemcpyHostToDevice, stream_));
   LTFB_CUDA(cudaMemcpyAsync(incoming_.p + counts_[2], inv, counts_[3] * 4, cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 EvalOut DeviceTrainer::tournament_decide() {
@@ -919,7 +978,7 @@ void DeviceTrainer::adopt(const float* fwd, const float* inv) {
     LTFB_CUDA(cudaMemsetAsync(mom1_[net].p, 0, counts_[net] * 4, stream_));
     LTFB_CUDA(cudaMemsetAsync(mom2_[net].p, 0, counts_[net] * 4, stream_));
   }
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
 }
 
 bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float* y,
@@ -979,7 +1038,7 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
   for (std::size_t i = 0; i < n; ++i)  // D2H of every step's record
     LTFB_CUDA(cudaMemcpyAsync(&recs[i], rec_.p + (first + i) % rec_.n, sizeof(ltfb_dev::StepRec),
                               cudaMemcpyDeviceToHost, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   bool ok = true;
   for (const auto& r : recs) {
     ltfb::train::StepRecord s;
@@ -1078,7 +1137,7 @@ void DeviceTrainer::load_ae_source(const float* y, std::size_t n) {
   ae_y_.alloc(n * op);
   LTFB_CUDA(cudaMemsetAsync(ae_y_.p, 0, ae_y_.bytes(), stream_));
   LTFB_CUDA(cudaMemcpy2DAsync(ae_y_.p, op * 4, y, out * 4, out * 4, n, cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   ae_rows_ = n;
 }
 
@@ -1105,7 +1164,7 @@ double DeviceTrainer::ae_step(const std::uint32_t* rows_idx, std::size_t n) {
   int flags[2] = {0, 0};
   LTFB_CUDA(cudaMemcpyAsync(&loss, ae_loss_.p, 8, cudaMemcpyDeviceToHost, stream_));
   LTFB_CUDA(cudaMemcpyAsync(flags, ae_flags_.p, 8, cudaMemcpyDeviceToHost, stream_));
-  LTFB_CUDA(cudaStreamSynchronize(stream_));
+  sync_stream();
   if (!std::isfinite(loss)) throw ltfb::NumericError("autoencoder_step: non-finite loss");
   const auto& h = spec_.arch.adam;
   auto apply = [&](int net) {
@@ -1120,7 +1179,7 @@ double DeviceTrainer::ae_step(const std::uint32_t* rows_idx, std::size_t n) {
                              stream_);
     ++launches_;
     LTFB_CUDA(cudaMemcpyAsync(&ctr_.p->t[net], &t, 8, cudaMemcpyHostToDevice, stream_));
-    LTFB_CUDA(cudaStreamSynchronize(stream_));
+    sync_stream();
   };
   wide_dirty_ = true;  // the frozen-weight copies / W^T images follow enc / dec
   small_T_dirty_ = true;

@@ -154,8 +154,17 @@ class DeviceTrainer {
   // exposed for benchmarks: launches one step without reading back
   void enqueue_steps(std::size_t n);
   /// Device-event timer on this trainer's stream (bench.py timed region).
+  /// The region starts behind a gate kernel that the next host enqueue
+  /// releases, and ends at the last work enqueued before a host wait, so
+  /// host latency at the region's two edges is not device time; gaps the
+  /// host loop causes inside the region (record read-back, rounds) are.
   void timer_start();
   double timer_stop_ms();
+  /// Host waits on stream_ go through here: the gate is released first, and
+  /// a running timer's end mark moves to the work enqueued so far.
+  void sync_stream();
+  void release_gate();
+  void mark_enqueued();
   /// When on, every wide-pass launch is bracketed by CUDA events on the
   /// launching stream; kernel_time() returns (total ms, launches).
   void set_kernel_timing(bool on);
@@ -169,6 +178,8 @@ class DeviceTrainer {
   std::size_t wide_ctas() const { return S_; }
   const ltfb_dev::StepArgs& step_args() const { return args_; }
   int wide_kernel_kind() const { return wide_kind_; }
+  /// Wide part of evaluate() on slice `which`: 2 = k_eval_tc (tcgen05), 1 = SIMT k_eval_wide.
+  int eval_kind(int which) const { return eval_tc_[which & 1].ready ? 2 : 1; }
   std::uint64_t launch_count() const { return launches_; }
 
  private:
@@ -183,7 +194,10 @@ class DeviceTrainer {
   /// Runs `steps` steps of the current epoch as one cached CUDA graph;
   /// false if graphs are off or capture is unsupported (caller launches).
   bool launch_graph(std::size_t steps);
-  cudaGraphExec_t graph_for(std::size_t steps);
+  /// The cached graph of `steps` steps; row_head: its first step runs the
+  /// row kernel (x rows + h) -- needed unless the previous step's post
+  /// kernel already produced them (h_ready_).
+  cudaGraphExec_t graph_for(std::size_t steps, bool row_head = true);
   static constexpr std::size_t kMaxGraphRun = 32;
 
  public:
@@ -248,6 +262,17 @@ class DeviceTrainer {
   std::uint64_t epoch_steps_ = 0, epoch_shuffled_ = 0;
   double epoch_seconds_ = 0;
   std::vector<EpochInfo> closed_;
+  // epoch starts enqueued by the current train_steps chunk (host bookkeeping
+  // before each), so an abort can roll back what its no-op tail advanced
+  struct EpochMark {
+    std::uint64_t at_step;
+    std::uint32_t epoch;
+    std::size_t closed, step_in_epoch;
+    std::uint64_t steps, shuffled;
+    double seconds;
+  };
+  std::vector<EpochMark> epoch_marks_;
+  bool aborted_ = false;  // the device abort flag was seen: later steps are refused
   std::vector<cudaEvent_t> ev_pool_;
   std::size_t ev_used_ = 0;
   struct Segment {
@@ -268,6 +293,9 @@ class DeviceTrainer {
 
   // timing
   cudaEvent_t tmr_[2] = {nullptr, nullptr};
+  bool timer_on_ = false, timer_marked_ = false;
+  int* gate_ = nullptr;  // pinned, mapped
+  bool gate_armed_ = false;
   bool ktime_on_ = false;
   static constexpr int kTimed = 5;  // gather, small fwd, wide, post, reduce
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev_[kTimed];

@@ -172,6 +172,13 @@ def validate_run_config(cfg: RunConfig):
         bad.append("unknown run mode: " + str(cfg.mode))
     if cfg.lr_jitter != 0.0:
         bad.append("lr_jitter is not supported on the B200 path")
+    if cfg.data_store != "preload":
+        # store.hpp:62-271: the B200 store is the HBM-resident preload store;
+        # the file-streaming modes are out of scope, so refuse
+        # rather than silently running preload semantics
+        bad.append(f"data_store '{cfg.data_store}' is not supported on the B200 path (preload only)")
+    if cfg.store_budget_mb != 0:
+        bad.append("store_budget_mb is not supported on the B200 path (the partition is HBM-resident)")
     if bad:
         raise ConfigError("invalid run config: " + "; ".join(bad) + "; ")
 

@@ -25,20 +25,23 @@ def test_bench_line_contract():
     assert len(lines) == 1, p.stdout[-2000:]
     d = json.loads(lines[0])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
-                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "step_roofline",
-                "latency_bound", "e2e", "gpu_launches", "clocks"):
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "kernel_rooflines",
+                "round_ms", "e2e", "gpu_launches", "clocks"):
         assert key in d, key
     assert d["n_gpus"] == 1 and d["steps"] == steps and d["warmup"] == warmup
     B = d["config"]["global_batch"]
     # value = samples of the K timed steps / their device time
     assert d["value"] == pytest.approx(B / (d["ms_per_step"] / 1e3), rel=1e-6)
-    r = d["roofline"]
+    r = d["roofline"]  # the whole step against HBM (the headline)
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9) and 0 < r["frac"] < 1
-    s = d["step_roofline"]
-    assert s["achieved"] == pytest.approx(s["algorithmic_bytes_per_step"] / (d["ms_per_step"] / 1e3) / 1e9,
+    assert r["achieved"] == pytest.approx(r["algorithmic_bytes_per_launch"] / (d["ms_per_step"] / 1e3) / 1e9,
                                           rel=1e-6)
-    assert 0 < s["frac"] < r["frac"]  # the step is slower than its wide pass alone
+    w = d["kernel_rooflines"]["wide"]
+    assert w["frac"] == pytest.approx(w["achieved"] / w["peak"], rel=1e-9)
+    assert 0 < r["frac"] < w["frac"] < 1  # the step is slower than its wide pass alone
+    # a tournament round is timed at N = 1 too (own payload, device decision)
+    assert d["round_ms"] is not None and d["round_ms"] > 0 and d["rounds_timed"] >= 1
     out = d["config"]["output_dim"]
     e = d["e2e"]
     assert e["h2d_bytes_per_step"] == B * (5 + out) * 4 and e["d2h_bytes_per_step"] > 0

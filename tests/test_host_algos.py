@@ -116,3 +116,14 @@ def test_ae_batch_draws_match_reference_rng(oracle):
     r = oracle.Rng(oracle.mix_seed(seed, 0xAE1))
     ref = np.array([r.below(rows) for _ in range(batch * steps)], np.uint32).reshape(steps, batch)
     assert np.array_equal(got, ref)
+
+
+def test_run_config_refuses_unsupported_store_modes():
+    """runner.hpp:91-110 + store.hpp:62-271: a config asking for the
+    file-streaming store modes or a store budget is refused (ConfigError)
+    instead of silently running the HBM preload store."""
+    from paper_1910_02270_b200.runner import validate_run_config
+    validate_run_config(L.RunConfig())
+    for kw in ({"data_store": "dynamic"}, {"data_store": "none"}, {"store_budget_mb": 64}):
+        with pytest.raises(L.ConfigError):
+            validate_run_config(L.RunConfig(**kw))

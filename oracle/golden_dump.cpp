@@ -848,7 +848,7 @@ static void tournament_case(Dump& d, const std::string& pfx,
   put_strided(d, pfx + "ae_enc_strided", flat(base.enc));
   put_strided(d, pfx + "ae_dec_strided", flat(base.dec));
   d.put(pfx + "ae_hashes", std::vector<std::uint64_t>{base.enc_hash(), base.dec_hash()});
-  if (cfg.dims.output_dim() < 64) {
+  if (cfg.dims.output_dim() < 10000) {  // tiny and desk: the full frozen AE (state injection)
     d.put(pfx + "ae_enc", flat(base.enc));
     d.put(pfx + "ae_dec", flat(base.dec));
   }

@@ -183,10 +183,20 @@ def validate_run_config(cfg: RunConfig):
         raise ConfigError("invalid run config: " + "; ".join(bad) + "; ")
 
 
-def _base_model(cfg: RunConfig, dataset: Dataset, train_parts) -> tuple:
+def _base_model(cfg: RunConfig, dataset: Dataset, train_parts, autoencoder=None) -> tuple:
     """runner.hpp:247-279: AE pre-training on the sorted union of the
-    training partitions, then frozen."""
+    training partitions, then frozen. `autoencoder` (a CycleGan whose enc /
+    dec blobs are used as the pre-trained AE; no pre-training runs, the
+    history's pretrain records stay empty) is the reference-state injection
+    the parity tests use to compare the GAN phase on its own."""
     base = make_cyclegan(cfg.dims, cfg.arch, mix_seed(cfg.seed, 0xAE0))
+    if autoencoder is not None:
+        for n in ("enc", "dec"):
+            if autoencoder.blobs[n].size != base.blobs[n].size:
+                raise ContractError("run_experiment: injected autoencoder has incompatible shapes")
+            base.blobs[n][:] = autoencoder.blobs[n]
+        base.autoencoder_frozen = True
+        return base, []
     union = np.sort(np.concatenate([np.asarray(p, np.uint32) for p in train_parts]))
     _, ay = dataset.rows(union)
     dev = (cfg.devices or (0,))[0]
@@ -242,9 +252,10 @@ def _check_dims(cfg: RunConfig, dataset: Dataset):
         raise ConfigError("configured dims do not match the dataset on disk")
 
 
-def run_experiment(cfg: RunConfig, dataset: Dataset | None = None) -> RunResult:
+def run_experiment(cfg: RunConfig, dataset: Dataset | None = None, autoencoder=None) -> RunResult:
     """runner.hpp:232-420 in one process (k trainers on cfg.devices).
-    Without a dataset, ensure_dataset(cfg) provides the bundles."""
+    Without a dataset, ensure_dataset(cfg) provides the bundles;
+    `autoencoder` replaces AE pre-training (see _base_model)."""
     validate_run_config(cfg)
     if dataset is None:
         dataset = ensure_dataset(cfg)
@@ -253,7 +264,7 @@ def run_experiment(cfg: RunConfig, dataset: Dataset | None = None) -> RunResult:
     rounds_enabled = cfg.mode == "ltfb" and k >= 2
     split = split_dataset(dataset.total, k, cfg.validation_fraction, cfg.tournament_fraction, cfg.seed, k >= 2)
     history = RunHistory(mode=cfg.mode.replace("_", "-"), n_trainers=k)
-    base, history.pretrain = _base_model(cfg, dataset, split[1])
+    base, history.pretrain = _base_model(cfg, dataset, split[1], autoencoder)
     trainers = [_trainer_for(cfg, dataset, base, split, t) for t in range(k)]
     have_val = split[0].size > 0
     if have_val:

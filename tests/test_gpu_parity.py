@@ -19,6 +19,14 @@ pytestmark = pytest.mark.gpu
 REL_LOSS = 1e-4
 REL_EVAL = 1e-5
 REL_W = 1e-3   # weights after up to 20 Adam steps (absolute scale of lr)
+# End-to-end runs whose AE pre-training runs on the device: the AE's Adam
+# normalises every gradient component, so where an MAE gradient component is
+# a near-zero cancellation its sign can flip with the summation order and
+# that weight moves by up to ~lr (test_autoencoder_step_matches_oracle); the
+# frozen AE then differs from the reference's at that scale and the GAN losses
+# after it by up to ~2e-4 (desk_k2: 20 AE + 30 GAN steps). The GAN phase
+# itself is held to REL_LOSS with the reference's AE injected (inject=True).
+REL_LOSS_DEVICE_AE = 5e-4
 
 TINY = L.ModalityDims(image_views=1, image_channels=1, image_h=4, image_w=4)
 DESK = L.ModalityDims()
@@ -451,10 +459,11 @@ def test_autoencoder_frozen_and_bad_rows():
         L.AutoencoderPretrainer(model, ds.y)
 
 
-@pytest.mark.parametrize("gfile,pfx", [("tournament", "tiny_k2_"), ("tournament", "tiny_k3_"),
-                                       ("tournament", "tiny_k4_"), ("tournament", "desk_k2_"),
-                                       ("tournament_paper", "paper_k2_")])
-def test_run_experiment_matches_reference(golden, gfile, pfx):
+@pytest.mark.parametrize("gfile,pfx,inject", [("tournament", "tiny_k2_", False), ("tournament", "tiny_k3_", False),
+                                              ("tournament", "tiny_k4_", False), ("tournament", "desk_k2_", False),
+                                              ("tournament", "desk_k2_", True), ("tournament", "tiny_k4_", True),
+                                              ("tournament_paper", "paper_k2_", False)])
+def test_run_experiment_matches_reference(golden, gfile, pfx, inject):
     """runner.run_experiment end to end on the device -- AE pre-training,
     per-trainer reinit, chunks, validation evals, rounds, best-of-k --
     against the reference's run_experiment (tests/golden/tournament.npz).
@@ -469,10 +478,17 @@ def test_run_experiment_matches_reference(golden, gfile, pfx):
     ds = L.synthetic_dataset(dims, gen_n, sampling_seed=sampling_seed, spec_seed=spec_seed, samples_per_file=spf)
     cfg = L.RunConfig(dims=dims, arch=arch, mode="ltfb", trainers=k, shards=shards, batch_size=batch,
                       interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed)
-    res = L.run_experiment(cfg, ds)
+    ae = None
+    if inject:  # the reference's pre-trained AE: the GAN phase alone against the reference
+        ae = L.make_cyclegan(dims, arch, 0)
+        ae.blobs["enc"][:] = g[pfx + "ae_enc"]
+        ae.blobs["dec"][:] = g[pfx + "ae_dec"]
+        assert ae.enc_hash() == int(g[pfx + "ae_hashes"][0]) and ae.dec_hash() == int(g[pfx + "ae_hashes"][1])
+    res = L.run_experiment(cfg, ds, autoencoder=ae)
     h = res.history
-    assert len(h.pretrain) == ae_steps
-    if ae_steps:
+    tol = REL_LOSS if (inject or ae_steps == 0 or dims.output_dim() < 64) else REL_LOSS_DEVICE_AE
+    assert len(h.pretrain) == (0 if inject else ae_steps)
+    if ae_steps and not inject:
         assert rel([p[1] for p in h.pretrain], g[pfx + "pretrain_loss"]) < REL_LOSS
     assert [s.trainer for s in h.steps] == list(g[pfx + "steps_trainer"])
     assert [s.step for s in h.steps] == list(g[pfx + "steps_step"])
@@ -481,16 +497,17 @@ def test_run_experiment_matches_reference(golden, gfile, pfx):
     e_local = rel([r.local_metric for r in h.trainer_rounds], g[pfx + "tr_local"])
     e_evals = rel([e.combined for e in h.evals], g[pfx + "evals_combined"])
     loc, inc = np.asarray(g[pfx + "tr_local"]), np.asarray(g[pfx + "tr_incoming"])
-    report("run_experiment", case=pfx, loss_rel=errs, round_metric_rel=e_local, eval_rel=e_evals,
+    report("run_experiment", case=pfx, inject_reference_ae=inject, tolerance=tol, loss_rel=errs,
+           round_metric_rel=e_local, eval_rel=e_evals,
            min_decision_margin=float(np.min(np.abs(loc - inc) / np.abs(loc))) if loc.size else None)
-    assert max(errs.values()) < REL_LOSS, errs
+    assert max(errs.values()) < tol, errs
     assert [(r.round, tuple(p)) for r in h.rounds for p in r.pairs] == \
         [(int(r), (int(a), int(b))) for r, a, b in
          zip(g[pfx + "round_pair_round"], g[pfx + "round_pair_a"], g[pfx + "round_pair_b"])]
     assert [int(r.kept_incoming) for r in h.trainer_rounds] == [int(v) for v in g[pfx + "tr_kept"]]
-    assert e_local < REL_LOSS
+    assert e_local < tol
     assert [x.bytes for x in h.transfers] == [int(v) for v in g[pfx + "xf_bytes"]]
-    assert e_evals < REL_LOSS
+    assert e_evals < tol
     assert res.best_trainer == int(g[pfx + "best_trainer"][0])
 
 

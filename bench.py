@@ -414,6 +414,7 @@ def main():
             tj = json.load(open(tpath))
             for kname in ("step", "wide", "post"):
                 traffic[kname] = tj.get(f"{kname}_kind{kind}_{args.dims}_{KERNEL_VERSION}")
+                traffic[kname + "_warm"] = tj.get(f"{kname}_kind{kind}_{args.dims}_{KERNEL_VERSION}_warm")
         except Exception:
             traffic = {}
     step_s = ms_max / args.steps / 1e3
@@ -429,6 +430,7 @@ def main():
         a = wide_bytes / (wide_ms / 1e3) / 1e9
         wide_rl = {"kernel": "wide (k_wide_tc)" if kind == 2 else "wide", "bound": "hbm", "achieved": a,
                    "peak": hbm, "unit": "GB/s", "frac": a / hbm, "traffic": traffic.get("wide"),
+                   "traffic_warm_l2": traffic.get("wide_warm"),
                    "algorithmic_bytes_per_launch": wide_bytes, "ms_per_launch": wide_ms,
                    "share_of_kernel_time": kt["wide"][0] / ktot if ktot else None}
     step_ach = step_bytes / step_s / 1e9
@@ -464,7 +466,8 @@ def main():
         "kernels_ms_per_launch": {n: (v[0] / v[1] if v[1] else None) for n, v in kt.items()},
         "roofline": {"kernel": "step (k_wide_tc + k_post_small, one CUDA-graph step)", "bound": "hbm",
                      "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
-                     "traffic": traffic.get("step"), "peak_source": peak_src,
+                     "traffic": traffic.get("step"), "traffic_warm_l2": traffic.get("step_warm"),
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": step_bytes, "units": "one training step of B rows",
                      "traffic_version": KERNEL_VERSION},
         "kernel_rooflines": {

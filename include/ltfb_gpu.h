@@ -219,6 +219,9 @@ int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* l
 int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
 /* which kernel evaluates slice `which` (0 tournament, 1 validation): 2 tcgen05 k_eval_tc, 1 SIMT */
 int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind);
+/* 1: store-path steps run as the streamed step (a persistent two-phase wide
+   pass beside a persistent post cluster per run of steps), 0: launched steps */
+int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on);
 /* Number of kernels this trainer has launched so far (all of them ours). */
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches);
 

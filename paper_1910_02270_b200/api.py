@@ -724,6 +724,13 @@ class Trainer:
         check(lib.ltfb_trainer_wide_info(self._h, C.byref(k), C.byref(c)))
         return k.value, c.value
 
+    def stream_mode(self) -> bool:
+        """True when store-path steps run as the streamed step (persistent
+        two-phase wide pass beside a persistent post cluster per run)."""
+        k = C.c_int32(0)
+        check(lib.ltfb_trainer_stream_info(self._h, C.byref(k)))
+        return bool(k.value)
+
     def eval_info(self, which: int = 0) -> int:
         """2 when slice `which` (0 tournament, 1 validation) is evaluated by
         the tcgen05 k_eval_tc, 1 for the SIMT k_eval_wide."""

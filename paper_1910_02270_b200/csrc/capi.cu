@@ -462,6 +462,10 @@ int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind) {
   });
 }
 
+int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on) {
+  return guarded([&] { *on = T(const_cast<ltfb_trainer*>(t)).stream_mode() ? 1 : 0; });
+}
+
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches) {
   return guarded([&] { *launches = T(const_cast<ltfb_trainer*>(t)).launch_count(); });
 }

@@ -41,6 +41,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "stream_sync.cuh"
 #include "tc_ptx.cuh"
 
 namespace cg = cooperative_groups;
@@ -72,10 +73,11 @@ struct NetS {
 
 struct Layout {
   NetS net[5];  // kF, kI, kCd, kET, kDH
-  int xs, e1, be, gh, stacked, gl_dec, gl_inv, gl, gc, gi;
+  int xs, e1, be, gh, stacked, gl_dec, gl_inv, gl, gd, gc, gi;
   int xn;  // x rows of the next step (next_h), prefetched in the prologue
   int pg[3];                // partial gradients disc, fwd, inv (blob layout)
-  int mo[3], vo[3], gr[3];  // owner-slice moments / reduced gradients
+  int mo[3], vo[3], gr[3];  // owner-slice moments / reduced gradients (then new parameters)
+  int mt[3], vt[3];         // new moments of the owner slice (committed into mo / vo if applied)
   int total;
 };
 enum { kF = 0, kI = 1, kCd = 2, kET = 3, kDH = 4 };
@@ -443,14 +445,14 @@ __device__ __noinline__ int reduce_owned(int pg, int lo, int hi, int gr, int bas
 /// m, v and the new parameter of each owned element are computed in place
 /// of the slice's moment and gradient images. Nothing global changes here.
 __device__ __noinline__ void adam_compute(const StepArgs& a, int net, const NetS& n, int lo, int hi, double c1,
-                                          double c2, int gr, int mo, int vo) {
+                                          double c2, int gr, int mo, int vo, int mt, int vt) {
   float* s = S();
   const double lr = a.lr[net], b1 = a.b1, b2 = a.b2, eps = a.eps;
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
     float m = s[mo + e - lo], v = s[vo + e - lo];
     s[gr + e - lo] = adam_elem(s[n.blob + e], m, v, s[gr + e - lo], lr, b1, b2, eps, c1, c2);
-    s[mo + e - lo] = m;
-    s[vo + e - lo] = v;
+    s[mt + e - lo] = m;
+    s[vt + e - lo] = v;
   }
 }
 
@@ -460,7 +462,8 @@ __device__ __noinline__ void adam_compute(const StepArgs& a, int net, const NetS
 /// half (DSMEM stores; visible after the next cluster barrier), so no CTA
 /// has to pull or re-transpose the updated network.
 __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS& n, int lo, int hi, int gr, int mo,
-                                         int vo, int push /* 1 blob, 2 blob + W^T */) {
+                                         int vo, int mt, int vt, int push /* 1 blob, 2 blob + W^T */,
+                                         int rbase = 0, int rcount = kC) {
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   float* p = a.p[net];
@@ -469,8 +472,11 @@ __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS&
   float* m2 = a.mom2[net];
   for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
     const float pn = s[gr + e - lo];
-    m1[e] = s[mo + e - lo];
-    m2[e] = s[vo + e - lo];
+    const float mn = s[mt + e - lo], vn = s[vt + e - lo];
+    s[mo + e - lo] = mn;  // the owner slice's moments stay resident (streamed step)
+    s[vo + e - lo] = vn;
+    m1[e] = mn;
+    m2[e] = vn;
     p[e] = pn;
     int t = -1;  // W^T position of a weight element (biases have none)
     for (int l = 0; l < n.L; ++l) {
@@ -482,8 +488,7 @@ __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS&
     }
     if (t >= 0) pT[t - n.Tall] = pn;
     if (push) {
-#pragma unroll
-      for (int r = 0; r < kC; ++r) {
+      for (int r = rbase; r < rbase + rcount; ++r) {
         float* peer = cl.map_shared_rank(s, r);
         peer[n.blob + e] = pn;
         if (push == 2 && t >= 0) peer[t] = pn;
@@ -566,6 +571,8 @@ inline Layout make_layout(const ModelArgs& m) {
     y.mo[i] = take(sl);
     y.vo[i] = take(sl);
     y.gr[i] = take(sl);
+    y.mt[i] = take(sl);
+    y.vt[i] = take(sl);
   }
   y.be = take(m.E1);
   y.xs = take(kR * m.in);
@@ -576,6 +583,7 @@ inline Layout make_layout(const ModelArgs& m) {
   y.gl_dec = take(kR * m.lat);
   y.gl_inv = take(kR * m.lat);
   y.gl = take(kR * m.lat);
+  y.gd = take(kR * m.lat);
   y.gc = take(2 * kR);
   y.gi = take(kR * m.in);
   y.total = at;
@@ -590,6 +598,9 @@ inline Layout make_layout(const ModelArgs& m) {
 // debug: fine-grained stamps inside the update phases (LTFB_PHASE_PROF)
 __shared__ long long g_st[16];
 __shared__ int g_nst;
+// 1 in the streamed step's persistent cluster (k_post_loop): parameters and
+// the owners' Adam moments stay resident in shared memory across steps
+__shared__ int g_persist;
 #define ST()                                                   \
   do {                                                         \
     if (threadIdx.x == 0 && g_nst < 16) g_st[g_nst++] = clock64(); \
@@ -662,7 +673,8 @@ __device__ __noinline__ Job make_job(int q, const StepArgs& a, const Layout& Y, 
 /// bytes to the mbarrier's transaction count, issues one bulk copy (TMA
 /// engine) for the 16 B-aligned body and loads the <= 6 unaligned edge
 /// floats itself. Then the row transforms.
-__device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const Rows& R, uint64_t* bar) {
+__device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const Rows& R, uint64_t* bar,
+                                      int persist = 0) {
   float* s = S();
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x;
@@ -676,7 +688,8 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
   constexpr unsigned kSkipDG = (1u << 1) | (1u << 6) | (1u << 8) | (1u << 13) | (1u << 14) | (1u << 18);
   constexpr unsigned kSkipCyc = (1u << 2) | (1u << 3) | (1u << 5) | (1u << 7) | (1u << 9) | (1u << 10) |
                                 (1u << 11) | (1u << 12) | (1u << 15) | (1u << 17);
-  const unsigned skip = half == 0 ? kSkipDG : (half == 1 ? kSkipCyc : 0u);
+  // streamed step: the reduced wide-pass rows arrive per step (stage_enc_rows / stage_dec_rows)
+  const unsigned skip = (half == 0 ? kSkipDG : (half == 1 ? kSkipCyc : 0u)) | (persist ? (1u << 17) | (1u << 18) : 0u);
   if (q < kJobs && !((skip >> q) & 1u)) {
     const Job j = make_job(q, a, Y, R);
     if (j.n > 0 && j.src != nullptr) {
@@ -701,7 +714,9 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
   // Loads needed only much later go out as cp.async (no stall here): the
   // Adam bias corrections and the MAE total (awaited in d_update), the next
   // step's x rows (awaited in next_h). Only the index loads block.
-  if (tid < 3) {
+  if (persist) {
+    // per-step constants, next rows and row transforms: the streamed loop
+  } else if (tid < 3) {
     const int net = tid == 0 ? kDisc : (tid == 1 ? kFwd : kInv);
     const unsigned long long t = a.ctr->t[net] + 1;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(&g_pre[2 * tid])),
@@ -711,7 +726,7 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(tc::smem_u32(&g_pre[6])), "l"(a.mae_total)
                  : "memory");
   }
-  if (a.post_next_h) {  // x rows of the next step of this epoch (used by next_h)
+  if (a.post_next_h && !persist) {  // x rows of the next step of this epoch (used by next_h)
     const int nxt = (int)a.ctr->step_in_epoch + 1;
     if ((long long)nxt * a.B < (long long)a.n_part) {
       const int rows = min(a.B, a.n_part - nxt * a.B);
@@ -736,6 +751,7 @@ __device__ __noinline__ void prologue(const StepArgs& a, const Layout& Y, const 
   if (tid == 0) tc::mbar_arrive(bar);
   tc::mbar_wait(bar, 0);
   __syncthreads();
+  if (persist) return;
   {
     // enc layer-0 activation of this CTA's rows (pad rows: act(0 + b))
     const int e1 = Y.net[kET].L > 0 ? Y.e1 : Y.stacked;
@@ -817,7 +833,7 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   ST();
   if (tid == 0) s_ok[0] = dok;
   const NetS& C = Y.net[kCd];
-  adam_compute(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0]);
+  adam_compute(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0]);
   double d_sum = 0.0;
   for (int r = 0; r < kC; ++r) d_sum += cl.map_shared_rank(s_loss, r)[0];
   const double n2 = 2.0 * (double)R.rows;
@@ -827,7 +843,7 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   int all_ok = 1;
   for (int r = 0; r < kC; ++r) all_ok &= cl.map_shared_rank(s_ok, r)[0];
   const bool d_ok = isfinite(*d_loss) && all_ok;
-  if (d_ok) adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], 2);
+  if (d_ok) adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0], 2);
   ST();
   cluster_sync();  // S3: every owner's updated disc slice (blob + W^T) pushed into every CTA
   return d_ok;
@@ -848,8 +864,11 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   const int cb = R.split ? kC : 0;
   const int fok = reduce_owned(Y.pg[1], R.lo[1], R.hi[1], Y.gr[1]);
   const int iok = R.split ? 1 : reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
-  adam_compute(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1], Y.vo[1]);
-  if (!R.split) adam_compute(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2]);
+  adam_compute(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1],
+               Y.vt[1]);
+  if (!R.split)
+    adam_compute(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2],
+                 Y.vt[2]);
   ST();
   if (tid == 0) {
     s_ok[1] = fok;
@@ -882,12 +901,16 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
-    adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1],
-                a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
+    if (g_persist)  // streamed step: every CTA of both halves keeps fwd (blob + W^T) resident
+      adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 2, 0,
+                  R.split ? 2 * kC : kC);
+    else
+      adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1],
+                  a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
     out[4] = 1.0;
     ST();
     if (all_i) {
-      if (!R.split) adam_commit(a, kInv, Y.net[kI], R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], 0);
+      if (!R.split) adam_commit(a, kInv, Y.net[kI], R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2], 0);
       out[5] = 1.0;
     }
   }
@@ -976,8 +999,15 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
 /// the inv partials over its own ranks, and applies Adam(inv) on its owner
 /// slices once the step's decision (computed identically from the shared
 /// flags and loss sums) says so.
+__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec);
+
+/// Streamed step (rs != nullptr): the cycle path runs first, then the wait
+/// for the wide pass's dec half of step k (red_dec, the MAE total) and the
+/// dec-head backward; *out gets d_ok, fwd_applied, inv_applied (the same
+/// decision every CTA of the cluster computes).
 __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const Rows& R, double* s_loss, int* s_ok,
-                                      double* s_wl) {
+                                      double* s_wl, const StreamArgs* rs = nullptr, int k = 0,
+                                      int* out = nullptr) {
   cg::cluster_group cl = cg::this_cluster();
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -987,8 +1017,8 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   const int latent = Y.stacked + kR * m.lat;
   const int nr = R.nr, rows = R.rows;
   wnet_fwd(F, Y.xs, 2, latent);
-  if (DH.L > 0) {
-    wnet_fwd(DH, latent, 2, -1);
+  if (DH.L > 0) wnet_fwd(DH, latent, 2, -1);  // dec-head tape
+  if (DH.L > 0 && !rs) {
     dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
     wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
   }
@@ -1008,7 +1038,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   cp_wait_all();  // g_pre (prologue cp.async); reduce_owned's barrier publishes it
   const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2], kC);
   if (tid == 0) s_ok[2] = iok;
-  adam_compute(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2]);
+  adam_compute(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2]);
   cluster_sync();  // S2 (d_update's flags)
   double d_sum = 0.0;
   int all_ok = 1;
@@ -1019,6 +1049,27 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   const double d_loss = ((double)rows * (d_sum / (2.0 * (double)rows))) / (double)rows;
   const bool d_ok = isfinite(d_loss) && all_ok;
   cluster_sync();  // S3
+  if (rs) {
+    // streamed step: the discriminator update above ran while the wide pass
+    // streamed its dec half; now wait for it (red_dec, the MAE total), run
+    // the dec-head backward and hand dL/dlatent (dec, cycle) to the partner
+    // CTA at S3b
+    __shared__ int s_w;
+    if (tid == 0) {
+      s_w = wait_counter(&rs->sync->dec_done, (unsigned long long)rs->S_wide * (k + 1), rs->sync, 3) ? 1 : 0;
+      if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[32 * k + 7] = gtimer();
+      g_pre[6] = __ldcg(rs->mae_total[k & 1]);
+    }
+    __syncthreads();
+    stage_dec_rows(a, Y, R, rs->red_dec[k & 1]);
+    if (DH.L > 0) {
+      dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
+      wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
+    }
+    __syncthreads();
+    cluster_sync();  // S3b
+  }
+  bool f_app = false, i_app = false;
   if (d_ok) {
     cluster_sync();  // S4
     cluster_sync();  // S5
@@ -1035,10 +1086,17 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     const double fm = g_pre[6] / (double)((long long)rows * m.out);
     const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
     const double total = ((double)rows * total_raw) / (double)rows;
+    f_app = isfinite(total) && all_f;
+    i_app = f_app && all_i;
     if (isfinite(total) && all_f && all_i)  // trainer.hpp:256-264: inv after fwd
-      adam_commit(a, kInv, I, R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], 0);
+      adam_commit(a, kInv, I, R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2], g_persist ? 2 : 0, kC,
+                  kC);  // streamed step: the cyc half keeps inv (blob + W^T) resident
   }
-  cluster_sync();  // S6
+  if (out) {
+    out[0] = d_ok;
+    out[1] = f_app;
+    out[2] = i_app;
+  }
 }
 
 __device__ __noinline__ void print_phases(const long long* ph, int n) {
@@ -1102,6 +1160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (tid == 0) {
     g_nst = 0;
+    g_persist = 0;
     tc::mbar_init(&s_bar, 1);
     tc::fence_barrier_init();
   }
@@ -1110,6 +1169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   PH();
   if (half == 1) {
     cyc_half(a, Y, R, s_loss, s_ok, s_wl);
+    cluster_sync();  // S6
     return;
   }
   const NetS& F = Y.net[kF];
@@ -1210,6 +1270,293 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef PH
 }
 
+// ============================================================ streamed step ==
+// k_post_loop: the post half of the streamed step. One persistent 16-CTA
+// cluster per run of steps inside an epoch, beside the persistent wide pass
+// (k_wide_ps) on the other SMs. The blob images, W^T images and the owners'
+// Adam moments stay resident in shared memory (the owners push every update
+// into the CTAs that read it), so a step stages only its rows of the
+// wide-pass sums. Per step k (DeviceTrainer::launch_stream_run):
+//   D/G half: wait enc_done(k) -> enc rows -> D-step chain -> S1 -> disc
+//             update -> adversarial + fwd backward -> fwd update -> S6 ->
+//             next_h (h / x rows of step k+1) -> h_done += 1 -> record
+//   cyc half: fwd / inv forward, cycle path, inv gradients -> wait
+//             dec_done(k) -> dec rows -> dec-head backward -> S1 -> inv
+//             update -> S6 -> next step's x rows
+// Skip / abort decisions are the launched kernel's, computed by every CTA
+// from the same cluster-shared flags; the counters they need (Adam t, the
+// skip count) are tracked locally from the values at launch.
+
+/// This CTA's rows of the reduced enc layer-0 sums (D/G half), enc layer-0
+/// bias + activation applied as the launched prologue does (pad rows act(b)).
+__device__ __noinline__ void stage_enc_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_enc) {
+  float* s = S();
+  const ModelArgs& m = a.m;
+  const int E1 = m.E1;
+  const int e1 = Y.net[kET].L > 0 ? Y.e1 : Y.stacked;
+  for (int i = threadIdx.x; i < kR * E1; i += kThreads) {
+    const int r = i / E1, c = i - r * E1;
+    const float v = r < R.nr ? __ldcg(red_enc + (long long)(R.r0 + r) * E1 + c) : 0.0f;
+    s[e1 + i] = act_f(m.enc_act0, m.enc_slope0, v + s[Y.be + c]);
+  }
+  __syncthreads();
+}
+
+/// This CTA's rows of dL/dh = (1/n) S Wd^T (cyc half), as the launched prologue.
+__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec) {
+  float* s = S();
+  const ModelArgs& m = a.m;
+  const int D = m.D;
+  const float gscale = (float)(1.0 / ((double)R.rows * (double)m.out));
+  const int gh = Y.net[kDH].L > 0 ? Y.gh : Y.gl_dec;
+  for (int i = threadIdx.x; i < kR * D; i += kThreads) {
+    const int r = i / D;
+    const float v = r < R.nr ? __ldcg(red_dec + (long long)R.r0 * D + i) : 0.0f;
+    s[gh + i] = v * gscale;
+  }
+  __syncthreads();
+}
+
+/// x rows of step `nxt` of the epoch (this CTA's row block) into xn, async.
+__device__ __noinline__ void prefetch_next_x(const StepArgs& a, const Layout& Y, const Rows& R, int nxt,
+                                             unsigned epoch) {
+  float* s = S();
+  const int in = a.m.in;
+  if ((long long)nxt * a.B >= (long long)a.n_part) return;
+  const int rows = min(a.B, a.n_part - nxt * a.B);
+  const int per = (rows + kC - 1) / kC;
+  const int r0 = min(R.rank * per, rows), nr = max(0, min(per, rows - r0));
+  const unsigned* perm = a.perm[epoch & 1u] + (long long)nxt * a.B + r0;
+  for (int i = threadIdx.x; i < kR * in; i += kThreads) {
+    const int r = i / in, c = i - r * in;
+    if (r < nr)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(s + Y.xn + i)),
+                   "l"(a.sx + (long long)perm[r] * in + c)
+                   : "memory");
+    else
+      s[Y.xn + i] = 0.0f;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_post_loop(const __grid_constant__ StepArgs ap, const __grid_constant__ Layout Lp,
+                const __grid_constant__ StreamArgs rp) {
+  __shared__ Layout Y;
+  __shared__ __align__(16) StepArgs a_s;
+  __shared__ __align__(16) StreamArgs r_s;
+  {
+    const int* src = reinterpret_cast<const int*>(&ap);
+    int* dst = reinterpret_cast<int*>(&a_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(StepArgs) / sizeof(int)); i += kThreads) dst[i] = src[i];
+    const int* src2 = reinterpret_cast<const int*>(&Lp);
+    int* dst2 = reinterpret_cast<int*>(&Y);
+    for (int i = threadIdx.x; i < (int)(sizeof(Layout) / sizeof(int)); i += kThreads) dst2[i] = src2[i];
+    const int* src3 = reinterpret_cast<const int*>(&rp);
+    int* dst3 = reinterpret_cast<int*>(&r_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(StreamArgs) / sizeof(int)); i += kThreads) dst3[i] = src3[i];
+    __syncthreads();
+  }
+  const StepArgs& a = a_s;
+  const StreamArgs& r = r_s;
+  __shared__ double s_loss[4];
+  __shared__ double s_wl[kWarps];
+  __shared__ int s_ok[4];
+  __shared__ double s_g[6];
+  __shared__ int s_res[3];    // d_ok, fwd applied, inv applied of the step
+  __shared__ int s_err[2];    // StepSync::error seen before S6 (step parity; read from rank 0)
+  __shared__ int s_w;
+  __shared__ __align__(8) uint64_t s_bar;
+  const ModelArgs& m = a.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  cg::cluster_group cl = cg::this_cluster();
+  StepSync* sy = r.sync;
+  Rows R;
+  const int crank = (int)cl.block_rank();
+  R.split = 1;  // launched only as the 16-CTA split cluster
+  const int half = crank / kC;
+  R.rank = crank % kC;
+  for (int q = 0; q < 3; ++q) {
+    const int c = q == 0 ? Y.net[kCd].count : (q == 1 ? Y.net[kF].count : Y.net[kI].count);
+    R.lo[q] = owner_lo(c, R.rank);
+    R.hi[q] = owner_lo(c, R.rank + 1);
+  }
+  auto set_rows = [&](int sie) {
+    R.rows = min(a.B, a.n_part - sie * a.B);
+    const int per = (R.rows + kC - 1) / kC;
+    R.r0 = min(R.rank * per, R.rows);
+    R.nr = max(0, min(per, R.rows - R.r0));
+  };
+  // counters this run advances (trainer.hpp:274-289), tracked locally
+  unsigned long long t_disc = a.ctr->t[kDisc], t_fwd = a.ctr->t[kFwd], t_inv = a.ctr->t[kInv];
+  unsigned long long skipped = a.ctr->skipped;
+  if (tid == 0) {
+    g_nst = 0;
+    g_persist = 1;
+    tc::mbar_init(&s_bar, 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  if (crank == 0 && tid == 0) {  // resident: the host may launch the wide pass now
+    sy->t_post0 = gtimer();
+    *reinterpret_cast<volatile int*>(r.resident_host) = r.run_id;
+    __threadfence_system();
+  }
+  if (a.ctr->aborted) {  // trainer.hpp:282-288: a run after the abort is all no-ops
+    if (crank == 0 && tid == 0) atomicExch(&sy->abort, 1);
+    return;
+  }
+  set_rows(r.sie0);
+  prologue(a, Y, R, &s_bar, 1);
+  const NetS& F = Y.net[kF];
+  const NetS& C = Y.net[kCd];
+  const NetS& ET = Y.net[kET];
+  const int latent = Y.stacked + kR * m.lat;
+  const bool pstamp = r.prof != nullptr && tid == 0 && (crank == 0 || crank == kC);
+#define PSTAMP(slot) do { if (pstamp) r.prof[32 * k + (slot)] = gtimer(); } while (0)
+  for (int k = 0; k < r.n; ++k) {
+    const int sie = r.sie0 + k;
+    if (crank == 0) PSTAMP(8);
+    set_rows(sie);
+    const int nr = R.nr, rows = R.rows;
+    prefetch_next_x(a, Y, R, sie + 1, r.epoch);
+    if (tid < 3) {  // Adam bias corrections 1 - b^t of this step's t (host std::pow table)
+      const unsigned long long t = (tid == 0 ? t_disc : (tid == 1 ? t_fwd : t_inv)) + 1;
+      g_pre[2 * tid] = a.adam_c[2 * t];
+      g_pre[2 * tid + 1] = a.adam_c[2 * t + 1];
+    }
+    if (half == 1) {
+      int res[3];
+      cyc_half(a, Y, R, s_loss, s_ok, s_wl, &r, k, res);
+      PSTAMP(15);
+      if (tid == 0) {
+        s_res[0] = res[0];
+        s_res[1] = res[1];
+        s_res[2] = res[2];
+        s_err[k & 1] = ld_acquire_i(&sy->error);
+      }
+      cluster_sync();  // S6
+      cp_wait_all();   // the next step's x rows
+      __syncthreads();
+      for (int i = tid; i < kR * m.in; i += kThreads) S()[Y.xs + i] = S()[Y.xn + i];
+    } else {
+      // ---- D-step: wait for the enc half of the wide pass of step k ----
+      if (tid == 0)
+        s_w = wait_counter(&sy->enc_done, (unsigned long long)r.S_wide * (k + 1), sy, 2) ? 1 : 0;
+      PSTAMP(9);
+      __syncthreads();
+      stage_enc_rows(a, Y, R, r.red_enc[k & 1]);
+      if (ET.L > 0) wnet_fwd(ET, Y.e1, 2, Y.stacked);  // real latents -> stacked[0, R)
+      wnet_fwd(F, Y.xs, 2, latent);                    // fake latents -> stacked[R, 2R)
+      wnet_fwd(C, Y.stacked, 4, -1);                   // disc on [real; fake]
+      {
+        const double lv = bce_warp(C.a[C.L - 1], C.dz[C.L - 1], 4, kR, nr, 2.0 * (double)rows, 1.0f);
+        if (lane == 0) s_wl[warp] = lv;
+        __syncwarp();
+      }
+      wnet_bwd(C, 4, -1, -1, -1);
+      __syncthreads();
+      pg_net(C, Y.stacked, 2 * kR, Y.pg[0]);
+      if (tid == 0) s_loss[0] = sum_warps(s_wl);
+      __syncthreads();
+      cluster_arrive();  // S1
+      cluster_wait();
+      PSTAMP(10);
+      double d_loss = 0.0;
+      const bool d_ok = d_update(a, Y, R, s_loss, s_ok, &d_loss);
+      PSTAMP(11);
+      if (tid == 0)
+        for (int i = 0; i < 6; ++i) s_g[i] = 0.0;
+      if (d_ok) {
+        // adversarial path through the updated disc (train_ops.hpp:106-117):
+        // its input gradient waits in gd for the dec / cycle terms
+        wnet_fwd(C, latent, 2, -1);
+        {
+          const double lv = bce_warp(C.a[C.L - 1], C.dz[C.L - 1], 2, kR, nr, (double)rows, m.lambda_adv);
+          if (lane == 0) s_wl[warp] = lv;
+          __syncwarp();
+        }
+        wnet_bwd(C, 2, Y.gd, -1, -1);
+      }
+      __syncthreads();
+      cluster_sync();  // S3b: the partner's dec-head backward (after the wide pass's dec half) is done
+      {
+        float* s = S();
+        const float* pdec = cl.map_shared_rank(s + Y.gl_dec, kC + R.rank);
+        const float* pinv = cl.map_shared_rank(s + Y.gl_inv, kC + R.rank);
+        for (int i = tid; i < kR * m.lat; i += kThreads) {
+          s[Y.gl_dec + i] = pdec[i];
+          s[Y.gl_inv + i] = pinv[i];
+        }
+        if (tid == 0) {  // the partner saw dec_done(k) before S3b; the MAE total of step k
+          wait_counter(&sy->dec_done, (unsigned long long)r.S_wide * (k + 1), sy, 5);
+          g_pre[6] = __ldcg(r.mae_total[k & 1]);
+        }
+        __syncthreads();
+      }
+      if (d_ok) {
+        {  // grad_latent = (dec + disc) + inv (train_ops.hpp:104, 116-117, 126-127), the warp's rows
+          float* s = S();
+          for (int i = 0; i < 2; ++i)
+            for (int c = lane; c < m.lat; c += 32) {
+              const int o = (warp + 8 * i) * m.lat + c;
+              s[Y.gl + o] = (s[Y.gl_dec + o] + s[Y.gd + o]) + s[Y.gl_inv + o];
+            }
+          __syncwarp();
+        }
+        dz_warp(Y.gl, F, F.L - 1, F.dz[F.L - 1]);
+        wnet_bwd(F, 2, -1, -1, -1);
+        __syncthreads();
+        pg_net(F, Y.xs, kR, Y.pg[1]);
+        if (tid == 0) s_loss[1] = sum_warps(s_wl);
+        double g[6];
+        g_update(a, Y, R, s_loss, s_ok, g);
+        if (tid == 0)
+          for (int i = 0; i < 6; ++i) s_g[i] = g[i];
+      }
+      if (tid == 0) {
+        s_res[0] = d_ok;
+        s_res[1] = s_g[4] != 0.0;
+        s_res[2] = s_g[5] != 0.0;
+        s_err[k & 1] = ld_acquire_i(&sy->error);
+      }
+      PSTAMP(12);
+      cluster_sync();  // S6: the updated generator in every CTA
+      PSTAMP(13);
+      if ((long long)(sie + 1) * a.B < (long long)a.n_part) {
+        next_h(a, Y, sie, r.epoch);  // h / x rows of step k+1 (also into this CTA's xs)
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          atomicAdd(&sy->h_done, 1ull);
+        }
+      }
+      PSTAMP(14);
+      if (R.rank == 0 && tid == 0) finish(a, d_ok, d_loss, s_g);
+    }
+    // ---- the step's decision, identical in every CTA ----
+    __syncthreads();
+    const bool d_ok = s_res[0] != 0, f_app = s_res[1] != 0, i_app = s_res[2] != 0;
+    if (d_ok) ++t_disc;
+    if (f_app) ++t_fwd;
+    if (i_app) ++t_inv;
+    bool stop = false;
+    if (!(d_ok && i_app)) {
+      ++skipped;
+      stop = (long long)skipped > (long long)a.abort_threshold;  // finish() set ctr->aborted
+    }
+    if (stop && crank == 0 && tid == 0) {
+      __threadfence();
+      atomicExch(&sy->abort, 1);
+    }
+    // a timed-out hand-off anywhere: every CTA reads rank 0's view from before S6
+    if (cl.map_shared_rank(s_err, 0)[k & 1]) stop = true;
+    if (stop) break;
+  }
+#undef PSTAMP
+  cp_wait_all();
+  cluster_sync();  // no CTA leaves while peers may still read its shared memory
+}
+
 }  // namespace ps
 
 namespace ps {
@@ -1259,6 +1606,59 @@ int post_tpl_kind(const StepArgs& a) {
   const ps::Layout y = ps::make_layout(m);
   if ((std::size_t)y.total * sizeof(float) > kSmemCap) return 0;
   return 1;
+}
+
+int post_loop_supported(const StepArgs& a) {
+  if (!post_tpl_kind(a) || std::getenv("LTFB_POST_NO_SPLIT")) return 0;
+  static PerDevice probe;
+  return probe.value([] {
+    if (cudaFuncSetAttribute(ps::k_post_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(ps::k_post_loop, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(2 * ps::kC);
+    q.blockDim = dim3(ps::kThreads);
+    q.dynamicSmemBytes = kSmemCap;
+    cudaLaunchAttribute qa;
+    qa.id = cudaLaunchAttributeClusterDimension;
+    qa.val.clusterDim.x = 2 * ps::kC;
+    qa.val.clusterDim.y = 1;
+    qa.val.clusterDim.z = 1;
+    q.attrs = &qa;
+    q.numAttrs = 1;
+    int nclusters = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, ps::k_post_loop, &q) == cudaSuccess && nclusters >= 1;
+    cudaGetLastError();
+    return ok ? 1 : 0;
+  });
+}
+
+void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s) {
+  static thread_local ps::Layout cache;
+  static thread_local ModelArgs cache_m{};
+  static thread_local bool have = false;
+  if (!have || std::memcmp(&cache_m, &a.m, sizeof(ModelArgs)) != 0) {
+    cache = ps::make_layout(a.m);
+    cache_m = a.m;
+    have = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * ps::kC);
+  cfg.blockDim = dim3(ps::kThreads);
+  cfg.dynamicSmemBytes = (std::size_t)cache.total * sizeof(float);
+  cfg.stream = s;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = 2 * ps::kC;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, ps::k_post_loop, a, cache, r);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("streamed post cluster launch: ") + cudaGetErrorString(e));
 }
 
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {

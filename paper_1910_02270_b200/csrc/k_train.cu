@@ -232,6 +232,18 @@ __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
   ctr->step_in_epoch = 0;
 }
 
+/// Start of a streamed run: the hand-off counters restart, the first step's
+/// h counts as ready (the row kernel or the previous run produced it).
+__global__ void k_stream_init(StepSync* sy, int run_id) {
+  sy->enc_done = 0;
+  sy->dec_done = 0;
+  sy->h_done = kStreamSignalers;
+  sy->abort = 0;
+  sy->resident = -run_id;  // error stays sticky: the host reads it after the chunk
+  sy->t_post0 = sy->t_wide0 = 0;
+  __threadfence();
+}
+
 /// Timer gate (bench timed regions): holds the stream until the host has
 /// enqueued the work behind it (*flag != 0), so the device-timed region
 /// starts with a full queue; gives up after ~0.5 s so a missed release can
@@ -285,5 +297,15 @@ void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s) {
 }
 
 void launch_gate(const volatile int* flag, cudaStream_t s) { k_gate<<<1, 1, 0, s>>>(flag); }
+
+void launch_stream_init(StepSync* sy, int run_id, cudaStream_t s) { k_stream_init<<<1, 1, 0, s>>>(sy, run_id); }
+
+void prepare_stream_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_stream_init);
+  cudaFuncGetAttributes(&fa, k_gate);
+  cudaFuncGetAttributes(&fa, k_begin_epoch);
+  prepare_wide_ps();
+}
 
 }  // namespace ltfb_dev

@@ -86,6 +86,19 @@ void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, i
 void encode_y_map(WideTcParamsHost& p, int which, const float* yb, const StepArgs& a, int yb_rows);
 void launch_prep_wide(const StepArgs& a, const WideTcParamsHost& p, cudaStream_t s);
 void launch_wide_tc_params(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s);
+/// Streamed step (k_wide_ps.cu / k_post_tpl.cu k_post_loop): the persistent
+/// two-phase wide pass over S CTAs and the persistent post cluster of a run.
+bool wide_ps_supported(const StepArgs& a, int S);
+/// Loads every kernel a streamed run launches (lazy module loading must not
+/// happen while the persistent post cluster spins).
+void prepare_wide_ps();
+void prepare_stream_kernels();
+void launch_wide_ps(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r, int S, cudaStream_t s);
+/// 1 if the streamed post cluster (16 CTAs, split mode) can run this model here.
+int post_loop_supported(const StepArgs& a);
+void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s);
+/// Resets the run's StepSync (h of the first step counted as ready).
+void launch_stream_init(StepSync* sy, int run_id, cudaStream_t s);
 void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
 bool post_fast_supported(const StepArgs& a);

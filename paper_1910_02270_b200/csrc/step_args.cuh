@@ -90,6 +90,38 @@ struct StepArgs {
   const double* adam_c;  // [cap x 2]: 1-b1^t, 1-b2^t (host std::pow)
 };
 
+/// Hand-offs of the streamed step (DeviceTrainer stream mode) between the
+/// persistent wide kernel (k_wide_ps) and the persistent post cluster
+/// (k_post_loop). Reset by k_stream_init at the start of every run; the
+/// counters only grow inside a run.
+struct StepSync {
+  unsigned long long enc_done;  // wide CTAs done reducing P_enc (+S per step)
+  unsigned long long dec_done;  // wide CTAs done reducing P_dec and the MAE (+S per step)
+  unsigned long long h_done;    // post D/G CTAs that wrote the next step's h / x rows (+kStreamSignalers per step)
+  int abort;                    // post: numeric abort, the run stops
+  int error;                    // a wait timed out (never expected): the run stops, the host raises
+  int resident;                 // post: the cluster of run `run_id` is resident
+  int err_site;                 // which wait timed out first (diagnostics)
+  unsigned long long t_post0, t_wide0;  // %globaltimer at the start of each kernel of the run (diagnostics)
+};
+/// CTAs of the post cluster that signal h_done (the D/G half, one row block each).
+constexpr int kStreamSignalers = 8;
+
+/// One run of the streamed step: n steps inside one epoch.
+struct StreamArgs {
+  int n;         // steps in the run
+  int sie0;      // step_in_epoch of the run's first step
+  unsigned epoch;
+  int run_id;
+  int S_wide;    // CTAs of the persistent wide kernel (split count of the partials)
+  StepSync* sync;
+  int* resident_host;  // mapped pinned int: the host waits for the post cluster before launching the wide pass
+  float* red_enc[2];   // reduced wide-pass sums per step parity [B x E1] / [B x D]
+  float* red_dec[2];
+  double* mae_total[2];
+  unsigned long long* prof;  // LTFB_STREAM_PROF: [n x 16] %globaltimer stamps per step, else null
+};
+
 /// Candidate evaluation (train_ops.hpp:191-205) over a resident slice.
 struct EvalArgs {
   ModelArgs m;

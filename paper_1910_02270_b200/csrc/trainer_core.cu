@@ -1,3 +1,5 @@
+#include <chrono>
+#include <thread>
 // DeviceTrainer implementation (see trainer_core.hpp).
 #include "trainer_core.hpp"
 
@@ -237,6 +239,36 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   {
     wide_dirty_ = true;
   }
+  // streamed step: the post cluster takes 2 x kPostCluster SMs for a whole
+  // run, the persistent wide pass the others (and, for one split-K order on
+  // every path, so do the launched wide passes)
+  {
+    const int Ss = sm_count_ - 2 * ltfb_dev::kPostCluster;
+    const bool tool = std::getenv("CUDA_INJECTION64_PATH") != nullptr;  // ncu / compute-sanitizer serialise kernels
+    // LTFB_NO_STREAM=1: launched steps; =2: launched steps with the streamed
+    // step's wide CTA count (the two paths then sum in the same order)
+    const char* ns = std::getenv("LTFB_NO_STREAM");
+    const bool able = wide_kind_ >= 2 && post_tpl_ && a.h_in_gather && spec_.n_shards == 1 && !a.phase_prof &&
+                      static_cast<std::size_t>(Ss) <= (ma.out + 31) / 32 && ltfb_dev::wide_ps_supported(a, Ss) &&
+                      ltfb_dev::post_loop_supported(a);
+    stream_on_ = able && !ns && !tool;
+    if (able && (stream_on_ || tool || (ns && ns[0] == '2'))) {
+      S_ = static_cast<std::size_t>(Ss);
+      a.S = Ss;
+    }
+    if (stream_on_) {
+      S_stream_ = Ss;
+      LTFB_CUDA(cudaMalloc(reinterpret_cast<void**>(&sync_), sizeof(ltfb_dev::StepSync)));
+      LTFB_CUDA(cudaMemsetAsync(sync_, 0, sizeof(ltfb_dev::StepSync), stream_));
+      LTFB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&resident_), sizeof(int), cudaHostAllocMapped));
+      *reinterpret_cast<volatile int*>(resident_) = 0;
+      red2_.alloc(static_cast<std::size_t>(B) * (ma.E1 + ma.D));
+      mae2_.alloc(1);
+      LTFB_CUDA(cudaStreamCreateWithFlags(&post_stream_, cudaStreamNonBlocking));
+      for (auto& e : st_ev_) LTFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ltfb_dev::prepare_stream_kernels();
+    }
+  }
   sync_stream();
 }
 
@@ -244,6 +276,14 @@ DeviceTrainer::~DeviceTrainer() {
   DeviceGuard g(spec_.device);
   release_gate();
   if (stream_) cudaStreamSynchronize(stream_);
+  if (post_stream_) {
+    cudaStreamSynchronize(post_stream_);
+    cudaStreamDestroy(post_stream_);
+  }
+  for (auto e : st_ev_)
+    if (e) cudaEventDestroy(e);
+  if (sync_) cudaFree(sync_);
+  if (resident_) cudaFreeHost(resident_);
   if (gate_) cudaFreeHost(gate_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (int i = 0; i < 2; ++i) {
@@ -742,6 +782,15 @@ void DeviceTrainer::enqueue_steps(std::size_t n) {
         for (std::size_t r = ranges[s].first; r < ranges[s].second; ++r)
           if (owner_[slots[begin + r]] >= 0 && owner_[slots[begin + r]] != s) ++epoch_shuffled_;
     }
+    if (stream_on_ && !ktime_on_) {  // streamed step: the rest of this epoch (or of n) as one run
+      const std::size_t srun = std::min<std::size_t>(n - i, steps_per_epoch_ - step_in_epoch_);
+      launch_stream_run(srun);
+      step_in_epoch_ += srun;
+      epoch_steps_ += srun;
+      host_step_ += srun;
+      i += srun - 1;
+      continue;
+    }
     // a run of steps inside this epoch goes out as one CUDA graph launch
     // runs are powers of two (<= kMaxGraphRun) so a handful of cached
     // graphs covers every position in every epoch
@@ -817,6 +866,97 @@ bool DeviceTrainer::launch_graph(std::size_t steps) {
   return true;
 }
 
+void DeviceTrainer::launch_stream_run(std::size_t steps) {
+  prepare_params();  // weight re-layouts / W^T images before the run
+  if (!h_ready_) {   // h / x rows of the run's first step
+    ltfb_dev::launch_row_h(args_, true, stream_);
+    ++launches_;
+  }
+  ++run_id_;
+  ltfb_dev::launch_stream_init(sync_, run_id_, stream_);
+  ltfb_dev::StreamArgs r{};
+  r.n = static_cast<int>(steps);
+  r.sie0 = static_cast<int>(step_in_epoch_);
+  r.epoch = epoch_;
+  r.run_id = run_id_;
+  r.S_wide = S_stream_;
+  r.sync = sync_;
+  LTFB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&r.resident_host), resident_, 0));
+  const int B = args_.B;
+  r.red_enc[0] = args_.scratch + args_.L.red_enc;
+  r.red_dec[0] = args_.scratch + args_.L.red_dec;
+  r.red_enc[1] = red2_.p;
+  r.red_dec[1] = red2_.p + static_cast<std::size_t>(B) * margs_.E1;
+  r.mae_total[0] = args_.mae_total;
+  r.mae_total[1] = mae2_.p;
+  const bool prof = std::getenv("LTFB_STREAM_PROF") != nullptr;
+  if (prof) {
+    if (prof_.n < 32 * steps) prof_.alloc(32 * steps);
+    LTFB_CUDA(cudaMemsetAsync(prof_.p, 0, prof_.bytes(), stream_));
+    r.prof = prof_.p;
+  }
+  // the post cluster first (it starts behind everything queued on stream_),
+  // then -- once it is resident, so the cooperative wide pass finds exactly
+  // its SMs free -- the wide pass on stream_; stream_ then joins post_stream_
+  LTFB_CUDA(cudaEventRecord(st_ev_[0], stream_));
+  LTFB_CUDA(cudaStreamWaitEvent(post_stream_, st_ev_[0], 0));
+  ltfb_dev::launch_post_loop(args_, r, post_stream_);
+  release_gate();
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*reinterpret_cast<volatile int*>(resident_) != run_id_) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+      stream_on_ = false;
+      throw ltfb::Error("CUDA error: streamed step: the post cluster did not become resident");
+    }
+    std::this_thread::yield();
+  }
+  ltfb_dev::launch_wide_ps(wtp_, args_, r, S_stream_, stream_);
+  LTFB_CUDA(cudaEventRecord(st_ev_[1], post_stream_));
+  LTFB_CUDA(cudaStreamWaitEvent(stream_, st_ev_[1], 0));
+  launches_ += 3;
+  h_ready_ = next_h_on() && step_in_epoch_ + steps < steps_per_epoch_;
+  if (std::getenv("LTFB_STREAM_DEBUG") || prof) {
+    sync_stream();
+    check_stream_error();
+  }
+  if (prof) {  // per-step stage times (us) relative to the wide pass's phase-1 start of each step
+    std::vector<unsigned long long> h(32 * steps);
+    LTFB_CUDA(cudaMemcpy(h.data(), prof_.p, h.size() * 8, cudaMemcpyDeviceToHost));
+    static const char* names[32] = {"w.p1", "w.p1red", "w.p2", "w.p2prod", "w.p2red", "w.hwait", "-", "c.decwait",
+                                    "d.start", "d.encwait", "d.S1", "d.dupd", "d.gupd", "d.S6", "d.nexth", "c.end",
+                                    "m.p1last", "m.p2first", "m.p2last", "e.p1part", "e.p2part", "w.gs1", "w.gs2",
+                                    "e.p2t0", "e.p2t5", "s.p2t0", "s.p2t5", "-", "-", "-", "-", "-"};
+    double acc[32] = {}, per_step = 0;
+    int cnt = 0;
+    for (std::size_t k = 2; k + 1 < steps; ++k, ++cnt) {
+      for (int s = 0; s < 32; ++s)
+        if (h[32 * k + s]) acc[s] += ((double)h[32 * k + s] - (double)h[32 * k + 0]) * 1e-3;
+      per_step += ((double)h[32 * (k + 1)] - (double)h[32 * k]) * 1e-3;
+    }
+    if (cnt) {
+      std::fprintf(stderr, "stream prof (%d steps, us from w.p1 of the step; step %.2f us):", cnt, per_step / cnt);
+      for (int s = 0; s < 32; ++s)
+        if (names[s][0] != '-') std::fprintf(stderr, " %s %.1f", names[s], acc[s] / cnt);
+      std::fprintf(stderr, "\n");
+    }
+  }
+}
+
+void DeviceTrainer::check_stream_error() {
+  if (!stream_on_) return;
+  ltfb_dev::StepSync sy{};
+  LTFB_CUDA(cudaMemcpy(&sy, sync_, sizeof sy, cudaMemcpyDeviceToHost));
+  if (std::getenv("LTFB_STREAM_DEBUG"))
+    std::fprintf(stderr, "stream run %d: enc %llu dec %llu h %llu abort %d error %d site %d wide-post start %.1f us\n",
+                 run_id_, sy.enc_done, sy.dec_done, sy.h_done, sy.abort, sy.error, sy.err_site,
+                 (double)((long long)sy.t_wide0 - (long long)sy.t_post0) * 1e-3);
+  if (sy.error) {
+    stream_on_ = false;
+    throw ltfb::Error("CUDA error: streamed step: a hand-off between the wide pass and the post cluster timed out "
+                      "(code " + std::to_string(sy.error) + ", site " + std::to_string(sy.err_site) + ")");
+  }
+}
+
 bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepRecord>& out) {
   DeviceGuard g(spec_.device);
   // trainer.hpp:282-288: the skip threshold was exceeded; the device trainer
@@ -830,6 +970,7 @@ bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepReco
     enqueue_steps(chunk);
     close_epoch_segment(false, false);
     sync_stream();
+    check_stream_error();
     if (ktime_on_) resolve_kernel_times();
     std::vector<ltfb_dev::StepRec> recs(chunk);
     const std::size_t at = first % rec_.n;

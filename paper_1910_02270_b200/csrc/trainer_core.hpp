@@ -180,6 +180,9 @@ class DeviceTrainer {
   int wide_kernel_kind() const { return wide_kind_; }
   /// Wide part of evaluate() on slice `which`: 2 = k_eval_tc (tcgen05), 1 = SIMT k_eval_wide.
   int eval_kind(int which) const { return eval_tc_[which & 1].ready ? 2 : 1; }
+  /// 1 when store-path steps run as the streamed step (persistent two-phase
+  /// wide pass + persistent post cluster per run, launch_stream_run).
+  bool stream_mode() const { return stream_on_; }
   std::uint64_t launch_count() const { return launches_; }
 
  private:
@@ -199,6 +202,21 @@ class DeviceTrainer {
   /// kernel already produced them (h_ready_).
   cudaGraphExec_t graph_for(std::size_t steps, bool row_head = true);
   static constexpr std::size_t kMaxGraphRun = 32;
+  /// Streamed step: `steps` steps of the current epoch as one run of the
+  /// persistent post cluster (post_stream_) beside the persistent wide pass
+  /// (stream_), which overlap across steps through StepSync hand-offs.
+  void launch_stream_run(std::size_t steps);
+  void check_stream_error();
+  bool stream_on_ = false;
+  int S_stream_ = 0;
+  int run_id_ = 0;
+  cudaStream_t post_stream_ = nullptr;
+  cudaEvent_t st_ev_[2] = {nullptr, nullptr};
+  ltfb_dev::StepSync* sync_ = nullptr;
+  int* resident_ = nullptr;  // pinned, mapped
+  DevBuf<float> red2_;       // red_enc / red_dec of the odd steps of a run
+  DevBuf<double> mae2_;
+  DevBuf<unsigned long long> prof_;  // LTFB_STREAM_PROF stamps
 
  public:
   /// Captures (without running) the step graphs of every run length the

@@ -601,6 +601,9 @@ __shared__ int g_nst;
 // 1 in the streamed step's persistent cluster (k_post_loop): parameters and
 // the owners' Adam moments stay resident in shared memory across steps
 __shared__ int g_persist;
+// LTFB_STREAM_PROF: this step's stamp row (cluster rank 0 only), else null
+__shared__ unsigned long long* g_pb;
+#define GSTAMP(slot) do { if (g_persist && g_pb && threadIdx.x == 0) g_pb[slot] = gtimer(); } while (0)
 #define ST()                                                   \
   do {                                                         \
     if (threadIdx.x == 0 && g_nst < 16) g_st[g_nst++] = clock64(); \
@@ -857,7 +860,9 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x;
   ST();
+  GSTAMP(29);
   cluster_sync();  // S4: fwd / inv partials + adv / cyc sums
+  GSTAMP(30);
   ST();
   // split mode: the inv partials, their reduction and the cycle losses live
   // in the cyc half (ranks kC .. 2kC-1), which also applies Adam(inv)
@@ -870,6 +875,7 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
     adam_compute(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2],
                  Y.vt[2]);
   ST();
+  GSTAMP(31);
   if (tid == 0) {
     s_ok[1] = fok;
     if (!R.split) s_ok[2] = iok;
@@ -880,6 +886,7 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
     cyc_sum += cl.map_shared_rank(s_loss, cb + r)[2];
   }
   cluster_sync();  // S5: flags
+  GSTAMP(27);
   ST();
   int all_f = 1, all_i = 1;
   for (int r = 0; r < kC; ++r) {
@@ -1057,7 +1064,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     __shared__ int s_w;
     if (tid == 0) {
       s_w = wait_counter(&rs->sync->dec_done, (unsigned long long)rs->S_wide * (k + 1), rs->sync, 3) ? 1 : 0;
-      if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[32 * k + 7] = gtimer();
+      if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[128 * k + 7] = gtimer();
       g_pre[6] = __ldcg(rs->mae_total[k & 1]);
     }
     __syncthreads();
@@ -1412,10 +1419,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const NetS& ET = Y.net[kET];
   const int latent = Y.stacked + kR * m.lat;
   const bool pstamp = r.prof != nullptr && tid == 0 && (crank == 0 || crank == kC);
-#define PSTAMP(slot) do { if (pstamp) r.prof[32 * k + (slot)] = gtimer(); } while (0)
+#define PSTAMP(slot) do { if (pstamp) r.prof[128 * k + (slot)] = gtimer(); } while (0)
   for (int k = 0; k < r.n; ++k) {
     const int sie = r.sie0 + k;
     if (crank == 0) PSTAMP(8);
+    if (tid == 0) g_pb = (r.prof && crank == 0) ? r.prof + 128 * k : nullptr;
     set_rows(sie);
     const int nr = R.nr, rows = R.rows;
     prefetch_next_x(a, Y, R, sie + 1, r.epoch);
@@ -1478,7 +1486,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         wnet_bwd(C, 2, Y.gd, -1, -1);
       }
       __syncthreads();
+      GSTAMP(94);
       cluster_sync();  // S3b: the partner's dec-head backward (after the wide pass's dec half) is done
+      GSTAMP(95);
       {
         float* s = S();
         const float* pdec = cl.map_shared_rank(s + Y.gl_dec, kC + R.rank);
@@ -1503,9 +1513,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           __syncwarp();
         }
+        GSTAMP(92);
         dz_warp(Y.gl, F, F.L - 1, F.dz[F.L - 1]);
         wnet_bwd(F, 2, -1, -1, -1);
         __syncthreads();
+        GSTAMP(93);
         pg_net(F, Y.xs, kR, Y.pg[1]);
         if (tid == 0) s_loss[1] = sum_warps(s_wl);
         double g[6];

@@ -177,6 +177,8 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
   tc::tc_fence_after();
   const uint32_t T = tmem_base;
 
+  // per-tile stamps of phase 2 (CTA 0): slot 32 + 5 j + e
+#define TSTAMP(kk, j, e) do { if (r.prof && blockIdx.x == 0 && (j) < 12) r.prof[128 * (kk) + 32 + 5 * (j) + (e)] = gtimer(); } while (0)
   // ---- per-role state that runs on across phases ----
   int prod_next = 0;   // w0: next running tile index whose weights are issued
   int gath_next = 0;   // w6-9: next running tile index whose y rows are gathered
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
           tc::mbar_expect_tx(&full[s], kWt);
           tc::tma_load_2d(WeH(s), &tp.tm_wet, &full[s], c0, 0);
         } else {             // phase 2: Wd (MMA3) and WdT (MMA2, two K-blocks)
+          TSTAMP(q >> 1, j, 0);
           tc::mbar_expect_tx(&full[s], 2 * kWt);
           tc::tma_load_2d(WdH(s), &tp.tm_wd, &full[s], c0, 0);
           tc::tma_load_2d(WtH(s), &tp.tm_wdt, &full[s], 0, c0);
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
   double mae_e[4] = {0.0, 0.0, 0.0, 0.0};
   int q_done = 0;  // phases executed
   const bool stamp = r.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-#define WSTAMP(slot) do { if (stamp) r.prof[32 * k + (slot)] = gtimer(); } while (0)
+#define WSTAMP(slot) do { if (stamp) r.prof[128 * k + (slot)] = gtimer(); } while (0)
   for (int q = 0; q < nphase; ++q) {
     q_done = q + 1;
     const int k = q >> 1;
@@ -273,10 +276,10 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             }
             tc::tc_commit(&empty[s]);
           }
-          if (r.prof && blockIdx.x == 0) r.prof[32 * k + 16] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 16] = gtimer();
         } else {
           mbar_wait_to(&h_ready, hr_par);
-          if (r.prof && blockIdx.x == 0) r.prof[32 * k + 17] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 17] = gtimer();
           tc::tc_fence_after();
           auto mma3 = [&](int i) {
             const int s = i % kStages;
@@ -316,6 +319,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
               // sready is arrived once per phase-2 tile: indexed by the phase-2 tile count
               const int o3 = o_run + (n3 - i0);
               if (tc::mbar_test(&sready[o3 % kStages], (uint32_t)(o3 / kStages) & 1u)) {
+                TSTAMP(k, n3 - i0, 4);
                 mma3(n3++);
                 issued = true;
               }
@@ -327,13 +331,14 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
               const bool obuf = oi < 2 || tc::mbar_test(&oempty[oi & 1], ((uint32_t)(oi >> 1) & 1u) ^ 1u);
               if (staged && obuf) {
                 mma2(n2, oi & 1);
+                TSTAMP(k, n2 - i0, 2);
                 ++n2;
                 issued = true;
               }
             }
             if (!issued) __nanosleep(20);
           }
-          if (r.prof && blockIdx.x == 0) r.prof[32 * k + 18] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 18] = gtimer();
         }
         tc::tc_commit(&done);
       }
@@ -406,7 +411,8 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&oempty[ob]);
           tc::mbar_arrive(&sready[oi % kStages]);
-          if (r.prof && blockIdx.x == 0 && rr == 0 && (j == 0 || j == 5)) r.prof[32 * k + (j == 0 ? 23 : 24)] = gtimer();
+          if (r.prof && blockIdx.x == 0 && rr == 0 && (j == 0 || j == 5)) r.prof[128 * k + (j == 0 ? 23 : 24)] = gtimer();
+          if (rr == 0) TSTAMP(k, j, 3);
 #pragma unroll
           for (int e = 0; e < 4; ++e) mae_e[e] += (double)tsum[e];
         }
@@ -427,7 +433,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             *reinterpret_cast<float4*>(P + 32 * half + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
       }
       tc::tc_fence_before();
-      if (r.prof && blockIdx.x == 0 && rr == 0) r.prof[32 * k + (ph2 ? 20 : 19)] = gtimer();
+      if (r.prof && blockIdx.x == 0 && rr == 0) r.prof[128 * k + (ph2 ? 20 : 19)] = gtimer();
       if (ph2) {
         red[rr] = (mae_e[0] + mae_e[1]) + (mae_e[2] + mae_e[3]);
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -490,7 +496,8 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
         tc::tc_fence_before();
         tc::mbar_arrive(&split_done[s]);
         if (ph2 && r.prof && blockIdx.x == 0 && tg == 0 && (i - i0 == 0 || i - i0 == 5))
-          r.prof[32 * k + (i - i0 == 0 ? 25 : 26)] = gtimer();
+          r.prof[128 * k + (i - i0 == 0 ? 25 : 26)] = gtimer();
+        if (ph2 && tg == 0) TSTAMP(k, i - i0, 1);
       }
     }
     if (my_tiles > 0) done_par ^= 1u;
@@ -576,7 +583,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
     if (!ph2 && warp >= 2 && warp < 6) {
       if (threadIdx.x == 64) {
         s_go = wait_counter(&sy->h_done, (unsigned long long)kStreamSignalers * (k + 1), sy, 4) ? 1 : 0;
-        if (r.prof && blockIdx.x == 0) r.prof[32 * k + 5] = gtimer();
+        if (r.prof && blockIdx.x == 0) r.prof[128 * k + 5] = gtimer();
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
@@ -599,6 +606,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
       for (int i = consumed; i < gath_next; ++i) mbar_wait_to(&yfull[i % kYStages], (uint32_t)(i / kYStages) & 1u);
   }
 #undef WSTAMP
+#undef TSTAMP
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<512>(T);

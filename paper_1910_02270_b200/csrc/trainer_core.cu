@@ -891,7 +891,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
   r.mae_total[1] = mae2_.p;
   const bool prof = std::getenv("LTFB_STREAM_PROF") != nullptr;
   if (prof) {
-    if (prof_.n < 32 * steps) prof_.alloc(32 * steps);
+    if (prof_.n < 128 * steps) prof_.alloc(128 * steps);
     LTFB_CUDA(cudaMemsetAsync(prof_.p, 0, prof_.bytes(), stream_));
     r.prof = prof_.p;
   }
@@ -920,7 +920,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     check_stream_error();
   }
   if (prof) {  // per-step stage times (us) relative to the wide pass's phase-1 start of each step
-    std::vector<unsigned long long> h(32 * steps);
+    std::vector<unsigned long long> h(128 * steps);
     LTFB_CUDA(cudaMemcpy(h.data(), prof_.p, h.size() * 8, cudaMemcpyDeviceToHost));
     static const char* names[32] = {"w.p1", "w.p1red", "w.p2", "w.p2prod", "w.p2red", "w.hwait", "-", "c.decwait",
                                     "d.start", "d.encwait", "d.S1", "d.dupd", "d.gupd", "d.S6", "d.nexth", "c.end",
@@ -930,13 +930,38 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     int cnt = 0;
     for (std::size_t k = 2; k + 1 < steps; ++k, ++cnt) {
       for (int s = 0; s < 32; ++s)
-        if (h[32 * k + s]) acc[s] += ((double)h[32 * k + s] - (double)h[32 * k + 0]) * 1e-3;
-      per_step += ((double)h[32 * (k + 1)] - (double)h[32 * k]) * 1e-3;
+        if (h[128 * k + s]) acc[s] += ((double)h[128 * k + s] - (double)h[128 * k + 0]) * 1e-3;
+      per_step += ((double)h[128 * (k + 1)] - (double)h[128 * k]) * 1e-3;
     }
     if (cnt) {
       std::fprintf(stderr, "stream prof (%d steps, us from w.p1 of the step; step %.2f us):", cnt, per_step / cnt);
       for (int s = 0; s < 32; ++s)
         if (names[s][0] != '-') std::fprintf(stderr, " %s %.1f", names[s], acc[s] / cnt);
+      // phase-2 tiles of CTA 0 in step 3: producer issue, staged, MMA2 issued, epilogue done, MMA3 issued
+      if (steps > 4) {
+        const std::size_t k = 3;
+        std::fprintf(stderr, "\n  post (us from c.decwait): S3b-arrive %.2f S3b %.2f fwd-bwd-start %.2f pg-start %.2f S4-arr %.2f S4 %.2f adam %.2f S5 %.2f gupd %.2f S6 %.2f nexth %.2f",
+                     ((double)h[128 * k + 94] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 95] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 92] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 93] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 29] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 30] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 31] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 27] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 12] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 13] - (double)h[128 * k + 7]) * 1e-3,
+                     ((double)h[128 * k + 14] - (double)h[128 * k + 7]) * 1e-3);
+        std::fprintf(stderr, "\n  tiles of step 3 (us from w.p2): prod / staged / mma2 / epi / mma3\n");
+        for (int j = 0; j < 12; ++j) {
+          std::fprintf(stderr, "   t%2d", j);
+          for (int e = 0; e < 5; ++e) {
+            const unsigned long long v = h[128 * k + 32 + 5 * j + e];
+            std::fprintf(stderr, " %7.2f", v ? ((double)v - (double)h[128 * k + 2]) * 1e-3 : -1.0);
+          }
+          std::fprintf(stderr, "\n");
+        }
+      }
       std::fprintf(stderr, "\n");
     }
   }

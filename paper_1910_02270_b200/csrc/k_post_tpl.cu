@@ -1064,7 +1064,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     __shared__ int s_w;
     if (tid == 0) {
       s_w = wait_counter(&rs->sync->dec_done, (unsigned long long)rs->S_wide * (k + 1), rs->sync, 3) ? 1 : 0;
-      if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[128 * k + 7] = gtimer();
+      if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[512 * k + 7] = gtimer();
       g_pre[6] = __ldcg(rs->mae_total[k & 1]);
     }
     __syncthreads();
@@ -1419,11 +1419,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const NetS& ET = Y.net[kET];
   const int latent = Y.stacked + kR * m.lat;
   const bool pstamp = r.prof != nullptr && tid == 0 && (crank == 0 || crank == kC);
-#define PSTAMP(slot) do { if (pstamp) r.prof[128 * k + (slot)] = gtimer(); } while (0)
+#define PSTAMP(slot) do { if (pstamp) r.prof[512 * k + (slot)] = gtimer(); } while (0)
   for (int k = 0; k < r.n; ++k) {
     const int sie = r.sie0 + k;
     if (crank == 0) PSTAMP(8);
-    if (tid == 0) g_pb = (r.prof && crank == 0) ? r.prof + 128 * k : nullptr;
+    if (tid == 0) g_pb = (r.prof && crank == 0) ? r.prof + 512 * k : nullptr;
     set_rows(sie);
     const int nr = R.nr, rows = R.rows;
     prefetch_next_x(a, Y, R, sie + 1, r.epoch);

@@ -234,7 +234,10 @@ __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
 
 /// Start of a streamed run: the hand-off counters restart, the first step's
 /// h counts as ready (the row kernel or the previous run produced it).
-__global__ void k_stream_init(StepSync* sy, int run_id) {
+__global__ void k_stream_init(StepSync* sy, int run_id, unsigned* grid_bar) {
+  // the streamed wide pass's barrier: arrival count and per-CTA flags restart
+  for (int i = threadIdx.x; i < 32 + 32 * 160; i += blockDim.x) grid_bar[64 + i] = 0;
+  if (threadIdx.x != 0) return;
   sy->enc_done = 0;
   sy->dec_done = 0;
   sy->h_done = kStreamSignalers;
@@ -298,7 +301,9 @@ void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s) {
 
 void launch_gate(const volatile int* flag, cudaStream_t s) { k_gate<<<1, 1, 0, s>>>(flag); }
 
-void launch_stream_init(StepSync* sy, int run_id, cudaStream_t s) { k_stream_init<<<1, 1, 0, s>>>(sy, run_id); }
+void launch_stream_init(StepSync* sy, int run_id, unsigned* grid_bar, cudaStream_t s) {
+  k_stream_init<<<1, 256, 0, s>>>(sy, run_id, grid_bar);
+}
 
 void prepare_stream_kernels() {
   cudaFuncAttributes fa;

@@ -53,8 +53,8 @@ constexpr int kW = 64;
 constexpr uint32_t kY = 16384;       // [128 x 32] f32
 constexpr uint32_t kWt = 8192;       // [64 x 32] f32
 constexpr uint32_t kStage = 4 * kWt; // phase 1: WeT hi/lo; phase 2: Wd hi/lo, WdT hi/lo
-constexpr int kStages = 3;           // == TMEM y slots
-constexpr int kYStages = 4;
+constexpr int kStages = 4;           // == TMEM y slots
+constexpr int kYStages = 3;
 constexpr int kMaxQ = 16;            // float4 outputs reduced per CTA (one of P_enc / P_dec)
 constexpr int kThreads = 320;
 // partial groups of the reduction: k_wide_tc's grouping (10 groups of 32
@@ -64,7 +64,10 @@ constexpr int kG = 10;
 constexpr uint32_t kRedOff = kYStages * kY + kStages * kStage;  // reduction scratch
 constexpr uint32_t kMaxS = 148;
 constexpr uint32_t kSmem = kRedOff + (kMaxS + kG) * kMaxQ * 16 + 1024;
-constexpr uint32_t kPenc = 0, kPdec = 64, kO0 = 128, kHhi = 192, kHlo = 256, kYbase = 320;
+// TMEM columns: one split-K accumulator shared by the phases (P_enc in
+// phase 1, P_dec in phase 2: each is read out before the other phase's
+// first MMA), the O double buffer, h hi / lo, and a y slot per stage
+constexpr uint32_t kPacc = 0, kO0 = 64, kHhi = 128, kHlo = 192, kYbase = 256;
 static_assert(kYbase + 64 * kStages <= 512, "TMEM columns");
 static_assert(kSmem <= 227 * 1024, "shared memory");
 }  // namespace wp
@@ -75,27 +78,39 @@ struct WidePsParams {
 
 /// Sense-reversing grid barrier of the cooperative launch, with a timeout
 /// (a missing CTA raises sync->error instead of hanging the GPU).
-__device__ __forceinline__ void grid_sync_t(unsigned* bar, unsigned n, StepSync* sy) {
+/// Grid barrier of the persistent wide pass. Arrival: one release atomic on
+/// a counter. Release: the last CTA to arrive bumps every CTA's own flag
+/// (one 128-B line per CTA), so the waiting CTAs poll disjoint lines instead
+/// of all polling one (measured: ~4 us of release latency with one shared
+/// generation word under 131 pollers). `epoch` counts this kernel's barriers
+/// (identical in every CTA); flags only grow, so no reset is needed.
+__device__ __forceinline__ void grid_sync_t(unsigned* bar, unsigned n, StepSync* sy, unsigned epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g0 = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == n - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    unsigned* cnt = bar + 64;
+    unsigned* flags = bar + 96;  // flag of CTA c at flags[32 c]
+    unsigned old;
+    // acq_rel: the last arriver acquires every CTA's writes before it releases the flags
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    if (old + 1 == n * epoch) {
+      // one release fence, then plain (relaxed) flag stores: a release store
+      // per flag would fence 132 times
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (unsigned c = 0; c < n; ++c)
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + 32 * c), "r"(epoch) : "memory");
     } else {
       const unsigned long long t0 = gtimer();
-      while (*gen == g0) {
+      unsigned cur;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(flags + 32 * blockIdx.x) : "memory");
+        if (cur >= epoch) break;
         if (gtimer() - t0 > kStreamTimeoutNs) {
           if (atomicCAS(&sy->error, 0, 2) == 0) sy->err_site = 6;
           break;
         }
-        __nanosleep(64);
+        __nanosleep(32);
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -115,6 +130,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
               const __grid_constant__ StreamArgs r, const float* __restrict__ bias_pad) {
   using namespace wp;
   if (a.ctr->aborted) return;  // the post cluster leaves at once too
+  unsigned bar_epoch = 0;      // grid barriers passed in this launch (k_stream_init zeroes the counter and flags)
   if (blockIdx.x == 0 && threadIdx.x == 0) r.sync->t_wide0 = gtimer();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -178,7 +194,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
   const uint32_t T = tmem_base;
 
   // per-tile stamps of phase 2 (CTA 0): slot 32 + 5 j + e
-#define TSTAMP(kk, j, e) do { if (r.prof && blockIdx.x == 0 && (j) < 12) r.prof[128 * (kk) + 32 + 5 * (j) + (e)] = gtimer(); } while (0)
+#define TSTAMP(kk, j, e) do { if (r.prof && blockIdx.x == 0 && (j) < 12) r.prof[512 * (kk) + 32 + 5 * (j) + (e)] = gtimer(); } while (0)
   // ---- per-role state that runs on across phases ----
   int prod_next = 0;   // w0: next running tile index whose weights are issued
   int gath_next = 0;   // w6-9: next running tile index whose y rows are gathered
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
   double mae_e[4] = {0.0, 0.0, 0.0, 0.0};
   int q_done = 0;  // phases executed
   const bool stamp = r.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-#define WSTAMP(slot) do { if (stamp) r.prof[128 * k + (slot)] = gtimer(); } while (0)
+#define WSTAMP(slot) do { if (stamp) r.prof[512 * k + (slot)] = gtimer(); } while (0)
   for (int q = 0; q < nphase; ++q) {
     q_done = q + 1;
     const int k = q >> 1;
@@ -267,29 +283,29 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             const uint32_t weh = tc::smem_u32(WeH(s)), wel = tc::smem_u32(WeL(s));
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t bh = tc::sdesc_sw128(weh + 32 * kk, 16, 1024);
-              tc::mma_tf32_ts(T + kPenc, T + tYh(s) + 8 * kk, bh, i_enc, (i > i0 || kk > 0) ? 1u : 0u);
+              tc::mma_tf32_ts(T + kPacc, T + tYh(s) + 8 * kk, bh, i_enc, (i > i0 || kk > 0) ? 1u : 0u);
               if (kPrecise) {
-                tc::mma_tf32_ts(T + kPenc, T + tYl(s) + 8 * kk, bh, i_enc, 1u);
-                tc::mma_tf32_ts(T + kPenc, T + tYh(s) + 8 * kk, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc,
+                tc::mma_tf32_ts(T + kPacc, T + tYl(s) + 8 * kk, bh, i_enc, 1u);
+                tc::mma_tf32_ts(T + kPacc, T + tYh(s) + 8 * kk, tc::sdesc_sw128(wel + 32 * kk, 16, 1024), i_enc,
                                 1u);
               }
             }
             tc::tc_commit(&empty[s]);
           }
-          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 16] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[512 * k + 16] = gtimer();
         } else {
           mbar_wait_to(&h_ready, hr_par);
-          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 17] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[512 * k + 17] = gtimer();
           tc::tc_fence_after();
           auto mma3 = [&](int i) {
             const int s = i % kStages;
             tc::tc_fence_after();
             const uint32_t wdh = tc::smem_u32(WdH(s)), wdl = tc::smem_u32(WdL(s));
             for (int kk = 0; kk < 4; ++kk) {
-              tc::mma_tf32_ts(T + kPdec, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdh + 32 * kk, 16, 1024), i_enc,
+              tc::mma_tf32_ts(T + kPacc, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdh + 32 * kk, 16, 1024), i_enc,
                               (i > i0 || kk > 0) ? 1u : 0u);
               if (kPrecise)
-                tc::mma_tf32_ts(T + kPdec, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdl + 32 * kk, 16, 1024), i_enc,
+                tc::mma_tf32_ts(T + kPacc, T + tYl(s) + 8 * kk, tc::sdesc_sw128(wdl + 32 * kk, 16, 1024), i_enc,
                                 1u);
             }
             tc::tc_commit(&empty[s]);
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             }
             if (!issued) __nanosleep(20);
           }
-          if (r.prof && blockIdx.x == 0) r.prof[128 * k + 18] = gtimer();
+          if (r.prof && blockIdx.x == 0) r.prof[512 * k + 18] = gtimer();
         }
         tc::tc_commit(&done);
       }
@@ -411,7 +427,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&oempty[ob]);
           tc::mbar_arrive(&sready[oi % kStages]);
-          if (r.prof && blockIdx.x == 0 && rr == 0 && (j == 0 || j == 5)) r.prof[128 * k + (j == 0 ? 23 : 24)] = gtimer();
+          if (r.prof && blockIdx.x == 0 && rr == 0 && (j == 0 || j == 5)) r.prof[512 * k + (j == 0 ? 23 : 24)] = gtimer();
           if (rr == 0) TSTAMP(k, j, 3);
 #pragma unroll
           for (int e = 0; e < 4; ++e) mae_e[e] += (double)tsum[e];
@@ -425,7 +441,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
       }
       for (int half = 0; half < 2; ++half) {
         float v[32];
-        if (my_tiles > 0) tc::tmem_ld32(T + lane_addr + (ph2 ? kPdec : kPenc) + 32 * half, v);
+        if (my_tiles > 0) tc::tmem_ld32(T + lane_addr + kPacc + 32 * half, v);
         else
           for (int u = 0; u < 32; ++u) v[u] = 0.0f;
         if (rr < rows)
@@ -433,7 +449,8 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             *reinterpret_cast<float4*>(P + 32 * half + u) = make_float4(v[u], v[u + 1], v[u + 2], v[u + 3]);
       }
       tc::tc_fence_before();
-      if (r.prof && blockIdx.x == 0 && rr == 0) r.prof[128 * k + (ph2 ? 20 : 19)] = gtimer();
+      if (r.prof && blockIdx.x == 0 && rr == 0) r.prof[512 * k + (ph2 ? 20 : 19)] = gtimer();
+      if (r.prof && ph2 && rr == 0) r.prof[512 * k + 128 + blockIdx.x] = gtimer();
       if (ph2) {
         red[rr] = (mae_e[0] + mae_e[1]) + (mae_e[2] + mae_e[3]);
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -496,7 +513,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
         tc::tc_fence_before();
         tc::mbar_arrive(&split_done[s]);
         if (ph2 && r.prof && blockIdx.x == 0 && tg == 0 && (i - i0 == 0 || i - i0 == 5))
-          r.prof[128 * k + (i - i0 == 0 ? 25 : 26)] = gtimer();
+          r.prof[512 * k + (i - i0 == 0 ? 25 : 26)] = gtimer();
         if (ph2 && tg == 0) TSTAMP(k, i - i0, 1);
       }
     }
@@ -508,18 +525,25 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
 
     // ---- phase end: grid-wide fixed-order reduction of this phase's partials ----
     if (ph2) WSTAMP(3);
-    grid_sync_t(a.grid_bar, (unsigned)S, sy);
+    if (ph2 && r.prof && blockIdx.x == 0 && threadIdx.x == 64) r.prof[512 * k + 299] = gtimer();
+    if (ph2 && r.prof) {
+      __syncthreads();
+      if (threadIdx.x == 0) r.prof[512 * k + 300 + blockIdx.x] = gtimer();
+    }
+    grid_sync_t(a.grid_bar, (unsigned)S, sy, ++bar_epoch);
     WSTAMP(ph2 ? 22 : 21);
     {
       const int q_all = rows * (kW / 4);  // float4 outputs of P_enc or P_dec
       const int lo = (int)((long long)q_all * blockIdx.x / S);
       const int hi = (int)((long long)q_all * (blockIdx.x + 1) / S);
       const int nq = hi - lo;
-      float4* stage = reinterpret_cast<float4*>(sm + kRedOff);            // [S][kMaxQ]
+      float4* stage = reinterpret_cast<float4*>(sm + kRedOff);                  // [S][kMaxQ]
       float4* part = reinterpret_cast<float4*>(sm + kRedOff) + kMaxS * kMaxQ;  // [kG][kMaxQ]
       const int g = threadIdx.x / 32, o = threadIdx.x % 32;  // o < nq <= kMaxQ active
       const long long pstride4 = (long long)a.B * kW / 4;
       const float4* P4 = reinterpret_cast<const float4*>(ph2 ? a.P_dec : a.P_enc);
+      // every partial's slice [lo, hi) by one bulk copy (TMA engine) per
+      // source CTA, then summed in ascending partial order per group
       if (threadIdx.x == 0 && nq > 0) tc::mbar_expect_tx(&rbar, (uint32_t)(S * nq * 16));
       __syncthreads();
       if ((int)threadIdx.x < S && nq > 0) {
@@ -530,9 +554,7 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
             "l"(P4 + threadIdx.x * pstride4 + lo), "r"(nq * 16), "r"(tc::smem_u32(&rbar))
             : "memory");
       }
-      if (nq > 0) {
-        mbar_wait_to(&rbar, rbar_par);
-      }
+      if (nq > 0) mbar_wait_to(&rbar, rbar_par);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (o < nq)
         for (int sidx = g; sidx < S; sidx += kG) {
@@ -583,14 +605,14 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
     if (!ph2 && warp >= 2 && warp < 6) {
       if (threadIdx.x == 64) {
         s_go = wait_counter(&sy->h_done, (unsigned long long)kStreamSignalers * (k + 1), sy, 4) ? 1 : 0;
-        if (r.prof && blockIdx.x == 0) r.prof[128 * k + 5] = gtimer();
+        if (r.prof && blockIdx.x == 0) r.prof[512 * k + 5] = gtimer();
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     // a failed wait (abort / timeout): every CTA sees the flags at the same
     // grid barrier, so all leave together after the next one
     if (ph2) {
-      grid_sync_t(a.grid_bar, (unsigned)S, sy);
+      grid_sync_t(a.grid_bar, (unsigned)S, sy, ++bar_epoch);
       if (threadIdx.x == 0) s_go = (ld_acquire_i(&sy->abort) | ld_acquire_i(&sy->error)) ? 0 : 1;
       __syncthreads();
       if (!s_go) break;

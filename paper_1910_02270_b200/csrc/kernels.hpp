@@ -98,7 +98,7 @@ void launch_wide_ps(const WideTcParamsHost& p, const StepArgs& a, const StreamAr
 int post_loop_supported(const StepArgs& a);
 void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s);
 /// Resets the run's StepSync (h of the first step counted as ready).
-void launch_stream_init(StepSync* sy, int run_id, cudaStream_t s);
+void launch_stream_init(StepSync* sy, int run_id, unsigned* grid_bar, cudaStream_t s);
 void launch_reduce(const StepArgs& a, cudaStream_t s);
 void launch_post(const StepArgs& a, cudaStream_t s);
 bool post_fast_supported(const StepArgs& a);

@@ -147,7 +147,9 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   scratch_.alloc(static_cast<std::size_t>(lay.total));
   ctr_.alloc(1);
   LTFB_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(ltfb_dev::Counters), stream_));
-  grid_bar_.alloc(2);
+  // [0..1]: the launched wide pass's barrier; from 64 on: the streamed wide
+  // pass's per-CTA release flags (one 128-B line each) and its arrival count
+  grid_bar_.alloc(64 + 32 * 160);
   LTFB_CUDA(cudaMemsetAsync(grid_bar_.p, 0, grid_bar_.bytes(), stream_));
   rec_.alloc(4096);
   for (int i = 0; i < 2; ++i) {
@@ -873,7 +875,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     ++launches_;
   }
   ++run_id_;
-  ltfb_dev::launch_stream_init(sync_, run_id_, stream_);
+  ltfb_dev::launch_stream_init(sync_, run_id_, grid_bar_.p, stream_);
   ltfb_dev::StreamArgs r{};
   r.n = static_cast<int>(steps);
   r.sie0 = static_cast<int>(step_in_epoch_);
@@ -891,7 +893,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
   r.mae_total[1] = mae2_.p;
   const bool prof = std::getenv("LTFB_STREAM_PROF") != nullptr;
   if (prof) {
-    if (prof_.n < 128 * steps) prof_.alloc(128 * steps);
+    if (prof_.n < 512 * steps) prof_.alloc(512 * steps);
     LTFB_CUDA(cudaMemsetAsync(prof_.p, 0, prof_.bytes(), stream_));
     r.prof = prof_.p;
   }
@@ -920,7 +922,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     check_stream_error();
   }
   if (prof) {  // per-step stage times (us) relative to the wide pass's phase-1 start of each step
-    std::vector<unsigned long long> h(128 * steps);
+    std::vector<unsigned long long> h(512 * steps);
     LTFB_CUDA(cudaMemcpy(h.data(), prof_.p, h.size() * 8, cudaMemcpyDeviceToHost));
     static const char* names[32] = {"w.p1", "w.p1red", "w.p2", "w.p2prod", "w.p2red", "w.hwait", "-", "c.decwait",
                                     "d.start", "d.encwait", "d.S1", "d.dupd", "d.gupd", "d.S6", "d.nexth", "c.end",
@@ -930,8 +932,8 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     int cnt = 0;
     for (std::size_t k = 2; k + 1 < steps; ++k, ++cnt) {
       for (int s = 0; s < 32; ++s)
-        if (h[128 * k + s]) acc[s] += ((double)h[128 * k + s] - (double)h[128 * k + 0]) * 1e-3;
-      per_step += ((double)h[128 * (k + 1)] - (double)h[128 * k]) * 1e-3;
+        if (h[512 * k + s]) acc[s] += ((double)h[512 * k + s] - (double)h[512 * k + 0]) * 1e-3;
+      per_step += ((double)h[512 * (k + 1)] - (double)h[512 * k]) * 1e-3;
     }
     if (cnt) {
       std::fprintf(stderr, "stream prof (%d steps, us from w.p1 of the step; step %.2f us):", cnt, per_step / cnt);
@@ -941,23 +943,40 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
       if (steps > 4) {
         const std::size_t k = 3;
         std::fprintf(stderr, "\n  post (us from c.decwait): S3b-arrive %.2f S3b %.2f fwd-bwd-start %.2f pg-start %.2f S4-arr %.2f S4 %.2f adam %.2f S5 %.2f gupd %.2f S6 %.2f nexth %.2f",
-                     ((double)h[128 * k + 94] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 95] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 92] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 93] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 29] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 30] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 31] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 27] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 12] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 13] - (double)h[128 * k + 7]) * 1e-3,
-                     ((double)h[128 * k + 14] - (double)h[128 * k + 7]) * 1e-3);
+                     ((double)h[512 * k + 94] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 95] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 92] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 93] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 29] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 30] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 31] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 27] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 12] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 13] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 14] - (double)h[512 * k + 7]) * 1e-3);
+        {  // phase-2 partials written, per CTA, relative to CTA 0
+          std::vector<double> d;
+          for (int c = 0; c < S_stream_; ++c)
+            if (h[512 * k + 128 + c]) d.push_back(((double)h[512 * k + 128 + c] - (double)h[512 * k + 128]) * 1e-3);
+          std::sort(d.begin(), d.end());
+          if (!d.empty())
+            std::fprintf(stderr, "\n  phase-2 partials per CTA vs CTA 0 (us): min %.2f p10 %.2f median %.2f p90 %.2f max %.2f",
+                         d.front(), d[d.size() / 10], d[d.size() / 2], d[d.size() * 9 / 10], d.back());
+          std::vector<double> b;
+          for (int c = 0; c < S_stream_; ++c)
+            if (h[512 * k + 300 + c]) b.push_back(((double)h[512 * k + 300 + c] - (double)h[512 * k + 128]) * 1e-3);
+          std::sort(b.begin(), b.end());
+          if (!b.empty())
+            std::fprintf(stderr, "\n  phase-2 barrier arrival per CTA vs CTA 0 partials (us): min %.2f median %.2f max %.2f; CTA0 pre-sync %.2f",
+                         b.front(), b[b.size() / 2], b.back(),
+                         ((double)h[512 * k + 299] - (double)h[512 * k + 128]) * 1e-3);
+        }
         std::fprintf(stderr, "\n  tiles of step 3 (us from w.p2): prod / staged / mma2 / epi / mma3\n");
         for (int j = 0; j < 12; ++j) {
           std::fprintf(stderr, "   t%2d", j);
           for (int e = 0; e < 5; ++e) {
-            const unsigned long long v = h[128 * k + 32 + 5 * j + e];
-            std::fprintf(stderr, " %7.2f", v ? ((double)v - (double)h[128 * k + 2]) * 1e-3 : -1.0);
+            const unsigned long long v = h[512 * k + 32 + 5 * j + e];
+            std::fprintf(stderr, " %7.2f", v ? ((double)v - (double)h[512 * k + 2]) * 1e-3 : -1.0);
           }
           std::fprintf(stderr, "\n");
         }

@@ -236,7 +236,7 @@ __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
 /// h counts as ready (the row kernel or the previous run produced it).
 __global__ void k_stream_init(StepSync* sy, int run_id, unsigned* grid_bar) {
   // the streamed wide pass's barrier: arrival count and per-CTA flags restart
-  for (int i = threadIdx.x; i < 32 + 32 * 160; i += blockDim.x) grid_bar[64 + i] = 0;
+  for (int i = threadIdx.x; i < 32 + 32 * 160; i += blockDim.x) grid_bar[64 + i] = 0;  // [64, 96 + 32 * 160)
   if (threadIdx.x != 0) return;
   sy->enc_done = 0;
   sy->dec_done = 0;

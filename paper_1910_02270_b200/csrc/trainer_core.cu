@@ -149,7 +149,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   LTFB_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(ltfb_dev::Counters), stream_));
   // [0..1]: the launched wide pass's barrier; from 64 on: the streamed wide
   // pass's per-CTA release flags (one 128-B line each) and its arrival count
-  grid_bar_.alloc(64 + 32 * 160);
+  grid_bar_.alloc(96 + 32 * 160);
   LTFB_CUDA(cudaMemsetAsync(grid_bar_.p, 0, grid_bar_.bytes(), stream_));
   rec_.alloc(4096);
   for (int i = 0; i < 2; ++i) {

@@ -623,7 +623,9 @@ def test_split_and_sequential_post_kernels_agree():
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for no_split in ("", "1"):
-        env = dict(os.environ, PYTHONPATH=repo)
+        # launched steps in both (the streamed step needs the split cluster),
+        # so both runs use the same wide-pass CTA count / split-K order
+        env = dict(os.environ, PYTHONPATH=repo, LTFB_NO_STREAM="1")
         if no_split:
             env["LTFB_POST_NO_SPLIT"] = "1"
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
@@ -766,3 +768,31 @@ def test_run_outputs_match_reference_run_directory(run, tmp_path, monkeypatch):
         # Adam moves each weight by <= ~lr per step: 2 lr steps bounds any
         # drift from sign flips of near-zero gradients
         assert float(np.max(np.abs(ma.blobs[n] - mb.blobs[n]))) <= 2 * cfg.arch.lr * cfg.step_budget, n
+
+
+def test_streamed_step_matches_launched_step():
+    """The streamed step (persistent two-phase wide pass beside a persistent
+    post cluster, DeviceTrainer stream mode) computes exactly what the
+    launched step computes (LTFB_NO_STREAM=2: launched kernels at the same
+    wide-pass CTA count): identical step records over several epochs and
+    runs, identical final generator / discriminator hashes and evaluation."""
+    import json
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("", "2"):
+        env = dict(os.environ, PYTHONPATH=repo)
+        env.pop("LTFB_NO_STREAM", None)
+        if mode:
+            env["LTFB_NO_STREAM"] = mode
+        r = subprocess.run([sys.executable, os.path.join(repo, "tools", "stream_check.py"), "--steps", "70",
+                            "--n", "2000"], capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    a, b = outs
+    assert a["stream"] and not b["stream"] and a["wide_ctas"] == b["wide_ctas"]
+    assert a["records"] == b["records"]
+    for key in ("fwd_hash", "inv_hash", "disc_hash", "eval"):
+        assert a[key] == b[key], key

@@ -627,6 +627,45 @@ __host__ __device__ __forceinline__ int owner_lo(int count, int r) {
   return r <= 0 ? 0 : (r >= kC ? count : ((count * r / kC) & ~3));
 }
 
+/// Streamed step: the new parameters of net n (adam_compute left them in
+/// every owner's gr slice) into this CTA's blob image and, if wT, its W^T
+/// image: DSMEM loads from the kC owners at cluster ranks rbase .. rbase+kC-1.
+/// Valid from the owners' flag barrier (S5 / S2) until their next
+/// adam_compute, which the cluster reaches only after the next S1.
+__device__ __noinline__ void pull_net(const NetS& n, int gr, int rbase, bool wT) {
+  cg::cluster_group cl = cg::this_cluster();
+  float* s = S();
+  const int count = n.count;
+  // one element of every owner slice per thread and round: the kC remote
+  // loads of a round are independent and go out back to back
+  int slice = 0;
+  for (int r = 0; r < kC; ++r) slice = max(slice, owner_lo(count, r + 1) - owner_lo(count, r));
+  for (int base = 0; base < slice; base += kThreads) {
+    const int i = base + (int)threadIdx.x;
+    float v[kC];
+    int e[kC];
+#pragma unroll
+    for (int r = 0; r < kC; ++r) {
+      const int lo = owner_lo(count, r), hi = owner_lo(count, r + 1);
+      e[r] = lo + i < hi ? lo + i : -1;
+      v[r] = e[r] >= 0 ? cl.map_shared_rank(s + gr, rbase + r)[i] : 0.0f;
+    }
+#pragma unroll
+    for (int r = 0; r < kC; ++r) {
+      if (e[r] < 0) continue;
+      s[n.blob + e[r]] = v[r];
+      if (wT)
+        for (int l = 0; l < n.L; ++l) {
+          const int in = n.w[l], out = n.w[l + 1], q = e[r] - n.woff[l];
+          if (q >= 0 && q < in * out) {
+            const int k = q / out, j = q - k * out;
+            s[n.T[l] + j * (in + 1) + k] = v[r];
+          }
+        }
+    }
+  }
+}
+
 /// A host->smem staging job: n floats from src to smem offset dst.
 struct Job {
   int dst, n;
@@ -908,9 +947,8 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
-    if (g_persist)  // streamed step: every CTA of both halves keeps fwd (blob + W^T) resident
-      adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 2, 0,
-                  R.split ? 2 * kC : kC);
+    if (g_persist)  // streamed step: every CTA pulls the new fwd from the owners (pull_net)
+      adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 0);
     else
       adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1],
                   a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
@@ -1096,8 +1134,8 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     f_app = isfinite(total) && all_f;
     i_app = f_app && all_i;
     if (isfinite(total) && all_f && all_i)  // trainer.hpp:256-264: inv after fwd
-      adam_commit(a, kInv, I, R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2], g_persist ? 2 : 0, kC,
-                  kC);  // streamed step: the cyc half keeps inv (blob + W^T) resident
+      adam_commit(a, kInv, I, R.lo[2], R.hi[2], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2],
+                  0);  // streamed step: the cyc half pulls the new inv (pull_net)
   }
   if (out) {
     out[0] = d_ok;
@@ -1440,9 +1478,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_res[0] = res[0];
         s_res[1] = res[1];
         s_res[2] = res[2];
-        s_err[k & 1] = ld_acquire_i(&sy->error);
       }
-      cluster_sync();  // S6
+      // the generator's new parameters straight from the owners' slices
+      // (no push, no closing barrier): fwd (blob) and inv (blob + W^T)
+      if (res[1]) pull_net(F, Y.gr[1], 0, false);
+      if (res[2]) pull_net(Y.net[kI], Y.gr[2], kC, true);
       cp_wait_all();   // the next step's x rows
       __syncthreads();
       for (int i = tid; i < kR * m.in; i += kThreads) S()[Y.xs + i] = S()[Y.xn + i];
@@ -1485,6 +1525,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         wnet_bwd(C, 2, Y.gd, -1, -1);
       }
+      if (tid == 0) s_err[k & 1] = ld_acquire_i(&sy->error);  // read by every CTA after S3b
+      if (k > 0) transpose_net(F);  // W^T of the fwd pulled last step (input gradients below)
       __syncthreads();
       GSTAMP(94);
       cluster_sync();  // S3b: the partner's dec-head backward (after the wide pass's dec half) is done
@@ -1524,16 +1566,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         g_update(a, Y, R, s_loss, s_ok, g);
         if (tid == 0)
           for (int i = 0; i < 6; ++i) s_g[i] = g[i];
+        PSTAMP(12);
+        // the new fwd blob straight from the owners' slices (its W^T image is
+        // rebuilt next step while this half waits for the dec half)
+        if (g[4] != 0.0) pull_net(F, Y.gr[1], 0, false);
+        __syncthreads();
+        PSTAMP(13);
       }
       if (tid == 0) {
         s_res[0] = d_ok;
         s_res[1] = s_g[4] != 0.0;
         s_res[2] = s_g[5] != 0.0;
-        s_err[k & 1] = ld_acquire_i(&sy->error);
       }
-      PSTAMP(12);
-      cluster_sync();  // S6: the updated generator in every CTA
-      PSTAMP(13);
       if ((long long)(sie + 1) * a.B < (long long)a.n_part) {
         next_h(a, Y, sie, r.epoch);  // h / x rows of step k+1 (also into this CTA's xs)
         __syncthreads();

@@ -11,6 +11,7 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
 #include <memory>
 #include <span>
 #include <string>
@@ -99,57 +100,76 @@ struct DatasetView {
   const float* y = nullptr;
 };
 
+/// data/store.hpp:45-57: file-access accounting of the store.
+struct AccessCounters {
+  std::uint64_t files_opened = 0;
+  std::uint64_t bytes_read = 0;
+  std::uint64_t samples_shuffled = 0;
+};
+
+/// Host view of the trainer's HBM-resident preload store
+/// (data/store.hpp:62-99 accessors): the partition, the loader shard that
+/// owns each slot (files dealt round-robin to shards, store.hpp:100-135)
+/// and the access counters (the preload phase reads every partition record
+/// once; training reads no file).
+class StoreView {
+ public:
+  int n_shards() const { return n_shards_; }
+  const std::vector<std::uint32_t>& partition() const { return partition_; }
+  const std::vector<std::int32_t>& owners() const { return owner_; }
+  const AccessCounters& counters() const { return counters_; }
+  const std::vector<std::uint32_t>& file_open_counts() const { return file_open_counts_; }
+  std::size_t size() const { return partition_.size(); }
+
+ private:
+  friend class Trainer;
+  int n_shards_ = 1;
+  std::vector<std::uint32_t> partition_;
+  std::vector<std::int32_t> owner_;
+  std::vector<std::uint32_t> file_open_counts_;
+  AccessCounters counters_;
+};
+
 class Trainer {
  public:
   /// train::Trainer(TrainerConfig, const DatasetIndex&, CycleGan<float>)
-  /// (trainer.hpp:43-79): the partition is preloaded into HBM.
-  Trainer(TrainerConfig cfg, const DatasetView& ds, CycleGan<float> model)
+  /// (trainer.hpp:43-79) over an in-memory dataset: the partition is
+  /// preloaded into HBM; the view's rows count as bundles of
+  /// `samples_per_file` records for the store's accounting.
+  Trainer(TrainerConfig cfg, const DatasetView& ds, CycleGan<float> model, std::size_t samples_per_file = 500)
       : cfg_(std::move(cfg)), mirror_(std::move(model)) {
-    if (!mirror_.autoencoder_frozen) throw ltfb::ContractError("Trainer: model autoencoder must be frozen");
-    if (cfg_.train_ids.empty()) throw ltfb::ContractError("plan_epoch: empty partition");
-    const ltfb_dims d = to_c(mirror_.dims);
-    const ltfb_arch a = arch_of(mirror_);
-    ltfb_trainer_config c{};
-    c.trainer_id = cfg_.trainer_id;
-    c.device = cfg_.device;
-    c.n_shards = cfg_.n_shards;
-    c.numeric_abort_threshold = cfg_.numeric_abort_threshold;
-    c.batch_size = cfg_.batch_size;
-    c.seed = cfg_.seed;
-    c.w_f = cfg_.w_f;
-    c.w_i = cfg_.w_i;
-    c.wide_kernel = cfg_.wide_kernel;
-    ltfb_trainer* h = nullptr;
-    check(ltfb_trainer_create(&d, &a, &c, &h));
-    h_.reset(h);
-    push_model();
     const std::size_t in = mirror_.dims.input_dim, out = mirror_.dims.output_dim();
-    auto rows = [&](const std::vector<std::uint32_t>& ids, std::vector<float>& x, std::vector<float>& y) {
-      x.resize(ids.size() * in);
-      y.resize(ids.size() * out);
+    const std::size_t files = (ds.total + samples_per_file - 1) / std::max<std::size_t>(1, samples_per_file);
+    init([&](const std::vector<std::uint32_t>& ids, float* x, float* y) {
       for (std::size_t i = 0; i < ids.size(); ++i) {
         if (ids[i] >= ds.total) throw ltfb::ContractError("DataStore: partition id outside dataset");
-        std::copy_n(ds.x + static_cast<std::size_t>(ids[i]) * in, in, x.data() + i * in);
-        std::copy_n(ds.y + static_cast<std::size_t>(ids[i]) * out, out, y.data() + i * out);
+        std::copy_n(ds.x + static_cast<std::size_t>(ids[i]) * in, in, x + i * in);
+        std::copy_n(ds.y + static_cast<std::size_t>(ids[i]) * out, out, y + i * out);
       }
-    };
-    std::vector<float> x, y;
-    rows(cfg_.train_ids, x, y);
-    check(ltfb_trainer_load_store(h_.get(), cfg_.train_ids.data(), cfg_.train_ids.size(), x.data(), y.data(),
-                                  nullptr));
-    if (!cfg_.tournament_ids.empty()) {
-      rows(cfg_.tournament_ids, x, y);
-      check(ltfb_trainer_set_slice(h_.get(), LTFB_SLICE_TOURNAMENT, x.data(), y.data(),
-                                   cfg_.tournament_ids.size()));
-    }
+    }, [&](std::uint32_t id) { return static_cast<std::size_t>(id) / std::max<std::size_t>(1, samples_per_file); },
+         files, static_cast<std::uint64_t>(mirror_.dims.record_floats()) * 4);
   }
 
   /// train::Trainer(TrainerConfig, const DatasetIndex&, CycleGan<float>)
-  /// over LBDS bundle files on disk (data/bundle.hpp:134-224): the
-  /// partition and the tournament slice are read once (the preload of
-  /// store.hpp:100-135) and made resident in HBM.
+  /// over LBDS bundle files on disk (data/bundle.hpp:134-224): only the
+  /// partition's and the tournament slice's records are read (the preload
+  /// of store.hpp:100-135, one pass per file) and made resident in HBM.
   Trainer(TrainerConfig cfg, const ltfb::data::DatasetIndex& index, CycleGan<float> model)
-      : Trainer(cfg, read_view(index, cfg), std::move(model)) {}  // cfg copied: read_view reads it
+      : cfg_(std::move(cfg)), mirror_(std::move(model)) {
+    if (!(index.dims == mirror_.dims)) throw ltfb::DimensionError("Trainer: dataset dims differ from the model's");
+    init([&](const std::vector<std::uint32_t>& ids, float* x, float* y) {
+      ltfb::data::read_records(index, std::span<const std::uint32_t>(ids), x, y, index.dims.output_dim());
+    }, [&](std::uint32_t id) { return index.locate(id).file_idx; }, index.paths.size(), index.stride_bytes());
+  }
+
+  /// trainer.hpp:90-97: one model hash per replica (the device trainer
+  /// keeps one replica per shard in lockstep: all equal by construction).
+  std::vector<std::uint64_t> replica_hashes() {
+    return std::vector<std::uint64_t>(static_cast<std::size_t>(cfg_.n_shards), model().model_hash());
+  }
+
+  /// trainer.hpp:88-89: the trainer's data store (host view).
+  const StoreView& store() const { return store_; }
 
   int id() const { return cfg_.trainer_id; }
   const TrainerConfig& config() const { return cfg_; }
@@ -206,6 +226,17 @@ class Trainer {
     return {m.forward_mae, m.inverse_mae, m.combined};
   }
 
+  /// The shared validation slice (runner.hpp:319-337 evaluate_all), resident in HBM.
+  void set_validation(const float* x, const float* y, std::size_t rows) {
+    check(ltfb_trainer_set_slice(h_.get(), LTFB_SLICE_VALIDATION, x, y, rows));
+  }
+  /// surrogate::evaluate of the trainer's own generator on the validation slice.
+  EvalMetric evaluate_validation(double w_f, double w_i) {
+    ltfb_eval_metric m{};
+    check(ltfb_trainer_evaluate(h_.get(), LTFB_SLICE_VALIDATION, nullptr, nullptr, w_f, w_i, &m));
+    return {m.forward_mae, m.inverse_mae, m.combined};
+  }
+
   /// trainer.hpp:117-127: copy fwd / inv, zero their moments, keep t.
   void adopt_generators(const ltfb::nn::MlpParams<float>& fwd, const ltfb::nn::MlpParams<float>& inv) {
     if (!fwd.same_shape(mirror_.fwd) || !inv.same_shape(mirror_.inv))
@@ -253,27 +284,83 @@ class Trainer {
     std::vector<ltfb_epoch_record> buf(1024);
     std::uint64_t n = 0;
     check(ltfb_trainer_take_epochs(h_.get(), buf.data(), buf.size(), &n));
-    for (std::uint64_t i = 0; i < n; ++i)
+    // training epochs of the preload store read no file (store.hpp:140-181)
+    for (std::uint64_t i = 0; i < n; ++i) {
       history_.epochs.push_back({cfg_.trainer_id, buf[i].epoch, buf[i].steps, 0, 0, buf[i].samples_shuffled,
                                  buf[i].seconds, buf[i].partial != 0});
+      store_.counters_.samples_shuffled += buf[i].samples_shuffled;
+    }
   }
 
-  // Rows of the partition and the tournament slice read from the bundles
-  // into a dense host view indexed by global id (only those rows filled).
-  static DatasetView read_view(const ltfb::data::DatasetIndex& index, const TrainerConfig& cfg) {
-    static thread_local std::vector<float> x, y;
-    const std::size_t in = index.dims.input_dim, out = index.dims.output_dim();
-    x.assign(index.total * in, 0.0f);
-    y.assign(index.total * out, 0.0f);
-    for (const auto* ids : {&cfg.train_ids, &cfg.tournament_ids}) {
-      std::vector<float> bx(ids->size() * in), by(ids->size() * out);
-      ltfb::data::read_records(index, std::span<const std::uint32_t>(*ids), bx.data(), by.data(), out);
-      for (std::size_t i = 0; i < ids->size(); ++i) {
-        std::copy_n(bx.data() + i * in, in, x.data() + static_cast<std::size_t>((*ids)[i]) * in);
-        std::copy_n(by.data() + i * out, out, y.data() + static_cast<std::size_t>((*ids)[i]) * out);
-      }
+  /// Creates the device trainer, preloads the partition (rows(ids, x, y)
+  /// fills host rows of the given ids) and the tournament slice, and writes
+  /// the preload phase's epoch-0 record (trainer.hpp:56-73).
+  template <class Rows, class FileOf>
+  void init(Rows&& rows, FileOf&& file_of, std::size_t n_files, std::uint64_t stride_bytes) {
+    if (!mirror_.autoencoder_frozen) throw ltfb::ContractError("Trainer: model autoencoder must be frozen");
+    if (cfg_.train_ids.empty()) throw ltfb::ContractError("plan_epoch: empty partition");
+    const auto t0 = std::chrono::steady_clock::now();
+    const ltfb_dims d = to_c(mirror_.dims);
+    const ltfb_arch a = arch_of(mirror_);
+    ltfb_trainer_config c{};
+    c.trainer_id = cfg_.trainer_id;
+    c.device = cfg_.device;
+    c.n_shards = cfg_.n_shards;
+    c.numeric_abort_threshold = cfg_.numeric_abort_threshold;
+    c.batch_size = cfg_.batch_size;
+    c.seed = cfg_.seed;
+    c.w_f = cfg_.w_f;
+    c.w_i = cfg_.w_i;
+    c.wide_kernel = cfg_.wide_kernel;
+    ltfb_trainer* h = nullptr;
+    check(ltfb_trainer_create(&d, &a, &c, &h));
+    h_.reset(h);
+    push_model();
+    // store.hpp:100-135: files covering the partition dealt round-robin to
+    // shards in file order; the loader shard owns every record it loads
+    store_.n_shards_ = cfg_.n_shards;
+    store_.partition_ = cfg_.train_ids;
+    store_.file_open_counts_.assign(n_files, 0);
+    std::vector<std::size_t> file(cfg_.train_ids.size());
+    std::vector<int> loader(n_files, -1);
+    std::vector<char> used(n_files, 0);
+    for (std::size_t i = 0; i < file.size(); ++i) {
+      file[i] = file_of(cfg_.train_ids[i]);
+      if (file[i] >= n_files) throw ltfb::ContractError("DataStore: partition id outside dataset");
+      used[file[i]] = 1;
     }
-    return DatasetView{index.dims, index.total, x.data(), y.data()};
+    int next = 0;
+    for (std::size_t f = 0; f < n_files; ++f)
+      if (used[f]) {
+        loader[f] = next;
+        next = (next + 1) % std::max(1, cfg_.n_shards);
+        ++store_.file_open_counts_[f];
+        ++store_.counters_.files_opened;
+      }
+    store_.owner_.resize(file.size());
+    for (std::size_t i = 0; i < file.size(); ++i) store_.owner_[i] = loader[file[i]];
+    store_.counters_.bytes_read = static_cast<std::uint64_t>(cfg_.train_ids.size()) * stride_bytes;
+    // only the partition's rows and the tournament slice's rows on the host
+    const std::size_t in = mirror_.dims.input_dim, out = mirror_.dims.output_dim();
+    {
+      std::vector<float> x(cfg_.train_ids.size() * in), y(cfg_.train_ids.size() * out);
+      rows(cfg_.train_ids, x.data(), y.data());
+      check(ltfb_trainer_load_store(h_.get(), cfg_.train_ids.data(), cfg_.train_ids.size(), x.data(), y.data(),
+                                    store_.owner_.data()));
+    }
+    if (!cfg_.tournament_ids.empty()) {
+      std::vector<float> x(cfg_.tournament_ids.size() * in), y(cfg_.tournament_ids.size() * out);
+      rows(cfg_.tournament_ids, x.data(), y.data());
+      check(ltfb_trainer_set_slice(h_.get(), LTFB_SLICE_TOURNAMENT, x.data(), y.data(),
+                                   cfg_.tournament_ids.size()));
+    }
+    ltfb::train::EpochRecord rec;
+    rec.trainer = cfg_.trainer_id;
+    rec.epoch = 0;
+    rec.files_opened = store_.counters_.files_opened;
+    rec.bytes_read = store_.counters_.bytes_read;
+    rec.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    history_.epochs.push_back(rec);
   }
 
   TrainerConfig cfg_;
@@ -281,6 +368,7 @@ class Trainer {
   CycleGan<float> mirror_;
   bool dirty_ = false;
   ltfb::train::HistorySegment history_;
+  StoreView store_;
 };
 
 struct RoundResult {

@@ -82,21 +82,26 @@ def build(verbose: bool = False) -> str:
 
 FACADE_SRC = os.path.join(REPO, "tests", "cpp", "facade_test.cpp")
 FACADE_BIN = os.path.join(OUT, "facade_test")
+CPP_TESTS = ("facade_test", "run_experiment_test")
 
 
 def build_facade_test() -> str | None:
-    """The C++ façade (include/ltfb_b200/trainer.hpp) test program, linked
-    against the in-tree library (g++; runs on the GPU box)."""
-    if not os.path.exists(FACADE_SRC):
-        return None
-    deps = [FACADE_SRC, LIB] + _headers()
-    if os.path.exists(FACADE_BIN) and os.path.getmtime(FACADE_BIN) >= max(os.path.getmtime(d) for d in deps):
-        return FACADE_BIN
-    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(REPO, "include"), FACADE_SRC, "-L" + OUT, "-lltfb_gpu",
-           "-Wl,-rpath,$ORIGIN", "-o", FACADE_BIN]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("g++ failed for the C++ facade test:\n" + r.stderr[-4000:])
+    """The C++ façade programs (include/ltfb_b200/trainer.hpp, runner.hpp:
+    tests/cpp/*.cpp), linked against the in-tree library (g++; run on the
+    GPU box)."""
+    for name in CPP_TESTS:
+        src = os.path.join(REPO, "tests", "cpp", name + ".cpp")
+        out = os.path.join(OUT, name)
+        if not os.path.exists(src):
+            continue
+        deps = [src, LIB] + _headers()
+        if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+            continue
+        cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(REPO, "include"), src, "-L" + OUT, "-lltfb_gpu",
+               "-Wl,-rpath,$ORIGIN", "-o", out]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for the C++ test program {name}:\n" + r.stderr[-4000:])
     return FACADE_BIN
 
 

@@ -72,6 +72,17 @@ int main() {
     ltfb_b200::Trainer tb(c, index, m);
     tb.train_steps(10);
     if (tb.history().steps.back().g_total != ts[0]->history().steps[9].g_total) return 3;
+    // store() / replica_hashes() (trainer.hpp:88-97): the preload read each
+    // partition record once from the 2 files covering ids 20..199
+    const auto& st = tb.store();
+    if (st.size() != 180 || st.counters().files_opened != 2 ||
+        st.counters().bytes_read != 180 * dims.record_floats() * 4)
+      return 4;
+    if (tb.history().epochs.empty() || tb.history().epochs.front().epoch != 0 ||
+        tb.history().epochs.front().files_opened != 2)
+      return 5;
+    const auto hs = tb.replica_hashes();
+    if (hs.size() != 1 || hs[0] != tb.model().model_hash()) return 6;
     std::filesystem::remove_all(dir);
   }
   try {  // the reference's error behaviour through the façade

@@ -796,3 +796,35 @@ def test_streamed_step_matches_launched_step():
     assert a["records"] == b["records"]
     for key in ("fwd_hash", "inv_hash", "disc_hash", "eval"):
         assert a[key] == b[key], key
+
+
+def test_cpp_run_experiment_matches_reference(golden):
+    """The C++ run_experiment (include/ltfb_b200/runner.hpp, runner.hpp:232-437
+    over the façade Trainer / tournament_round) on the reference's tiny_k2
+    run: AE pre-training losses, step losses, round decisions, validation
+    metrics and the best trainer as the reference's run; the store's
+    accounting (the preload epoch-0 record's files_opened / bytes_read,
+    trainer summaries) exactly."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(L.LIB_PATH), "run_experiment_test")
+    if not os.path.exists(exe):
+        pytest.skip("run_experiment_test not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    g = golden("tournament")
+    p = "tiny_k2_"
+    assert rel(got["pretrain_loss"], g[p + "pretrain_loss"]) < REL_LOSS
+    assert got["steps_trainer"] == [int(v) for v in g[p + "steps_trainer"]]
+    assert got["steps_step"] == [int(v) for v in g[p + "steps_step"]]
+    assert rel(got["steps_d_loss"], g[p + "steps_d_loss"]) < REL_LOSS
+    assert rel(got["steps_g_total"], g[p + "steps_g_total"]) < REL_LOSS
+    assert got["tr_kept"] == [int(v) for v in g[p + "tr_kept"]]
+    assert rel(got["tr_local"], g[p + "tr_local"]) < REL_LOSS
+    assert rel(got["evals_combined"], g[p + "evals_combined"]) < REL_LOSS
+    assert got["epochs_epoch"] == [int(v) for v in g[p + "epochs_epoch"]]
+    assert got["epochs_files_opened"] == [int(v) for v in g[p + "epochs_files_opened"]]
+    assert got["epochs_bytes_read"] == [int(v) for v in g[p + "epochs_bytes_read"]]
+    assert got["best_trainer"] == int(g[p + "best_trainer"][0])

@@ -191,6 +191,14 @@ int ltfb_trainer_load_ae_source(ltfb_trainer* t, const float* y, uint64_t n);
  * Adam(dec). LTFB_ENUMERIC as the reference: a non-finite loss or enc
  * gradient changes nothing, a non-finite dec gradient leaves enc applied. */
 int ltfb_trainer_ae_step(ltfb_trainer* t, const uint32_t* idx, uint64_t n, double* loss);
+/* Distributed AE pre-training (runner.hpp:249-279 with the union of the
+   training partitions sharded over the ranks' HBM stores, BASELINE config C5):
+   a zeroed AE source of `rows` rows; this trainer's store rows (by slot)
+   into source rows [dst_row, dst_row + n); ltfb_trainer_ae_allgather then
+   assembles every rank's rows (in place, NCCL all-gather on the trainer's
+   stream) and ltfb_trainer_ae_step runs on the assembled batch. */
+int ltfb_trainer_ae_alloc_source(ltfb_trainer* t, uint64_t rows);
+int ltfb_trainer_ae_fill_from_store(ltfb_trainer* t, const uint32_t* slots, uint64_t n, uint64_t dst_row);
 /* The runner's AE batch draws (runner.hpp:257-266): steps x batch row
  * indices from Rng(mix_seed({seed, 0xae1})).below(rows), step-major. */
 int ltfb_ae_batch_rows(uint64_t seed, uint64_t rows, uint64_t batch, uint64_t steps, uint32_t* out);
@@ -250,6 +258,9 @@ int ltfb_comm_destroy(ltfb_comm* c);
 int ltfb_trainer_exchange(ltfb_trainer* t, ltfb_comm* c, int peer);
 /* Broadcast a network blob from `root` (AE broadcast, runner.hpp:285). */
 int ltfb_trainer_broadcast(ltfb_trainer* t, ltfb_comm* c, int net, int root);
+/* In-place all-gather of the AE source: rank r contributes rows
+   [r * rows_per_rank, (r + 1) * rows_per_rank). */
+int ltfb_trainer_ae_allgather(ltfb_trainer* t, ltfb_comm* c, uint64_t rows_per_rank);
 
 /* ---- host algorithms of the path (bit-exact, product implementations) -- */
 uint64_t ltfb_mix_seed(const uint64_t* words, int n);                        /* rng.hpp:23-30 */

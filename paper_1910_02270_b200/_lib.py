@@ -116,7 +116,8 @@ EXPORTS = (
     "ltfb_partition_dataset", "ltfb_split_dataset", "ltfb_epoch_permutation",
     "ltfb_incoming_wins", "ltfb_synth_generate", "ltfb_init_params", "ltfb_net_param_count",
     "ltfb_trainer_synchronize", "ltfb_trainer_prepare_graphs", "ltfb_trainer_load_ae_source", "ltfb_trainer_ae_step", "ltfb_ae_batch_rows",
-    "ltfb_adam_step",
+    "ltfb_adam_step", "ltfb_trainer_ae_alloc_source", "ltfb_trainer_ae_fill_from_store",
+    "ltfb_trainer_ae_allgather",
 )
 
 
@@ -187,6 +188,9 @@ _sig("ltfb_synth_generate_ids", C.c_int, C.POINTER(Dims), C.c_uint64, C.c_double
      C.c_uint64, C.c_uint64, f32p, f32p, C.c_int)
 _sig("ltfb_nccl_available", C.c_int)
 _sig("ltfb_selftest_tcgen05", C.c_int, f32p, f32p, f32p, f32p, f32p, f32p, f32p, f32p)
+_sig("ltfb_trainer_ae_alloc_source", C.c_int, P, C.c_uint64)
+_sig("ltfb_trainer_ae_fill_from_store", C.c_int, P, u32p, C.c_uint64, C.c_uint64)
+_sig("ltfb_trainer_ae_allgather", C.c_int, P, P, C.c_uint64)
 _sig("ltfb_adam_step", C.c_int, f32p, f32p, f32p, f32p, C.c_uint64, C.POINTER(C.c_uint64), C.c_double,
      C.c_double, C.c_double, C.c_double, C.c_int)
 _sig("ltfb_nccl_unique_id", C.c_int, C.c_char_p)

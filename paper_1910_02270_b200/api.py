@@ -756,6 +756,24 @@ class Trainer:
         """Length of the fwd part of the generator payload fwd||inv."""
         return param_count(self._dims, self._arch, 2)
 
+    # -- distributed AE pre-training (runner.pretrain_autoencoder_sharded)
+    def ae_alloc_source(self, rows: int):
+        check(lib.ltfb_trainer_ae_alloc_source(self._h, rows))
+
+    def ae_fill_from_store(self, slots: np.ndarray, dst_row: int):
+        s = np.ascontiguousarray(slots, np.uint32)
+        check(lib.ltfb_trainer_ae_fill_from_store(self._h, s, s.size, dst_row))
+
+    def ae_allgather(self, comm: "Comm", rows_per_rank: int):
+        check(lib.ltfb_trainer_ae_allgather(self._h, comm._h, rows_per_rank))
+
+    def ae_step(self, idx: np.ndarray) -> float:
+        i = np.ascontiguousarray(idx, np.uint32)
+        loss = C.c_double(0.0)
+        check(lib.ltfb_trainer_ae_step(self._h, i, i.size, C.byref(loss)))
+        self._dirty = True
+        return loss.value
+
     def exchange(self, comm: "Comm", peer: int):
         check(lib.ltfb_trainer_exchange(self._h, comm._h, peer))
 

@@ -126,6 +126,7 @@ struct NcclApi {
   nccl_result (*Send)(const void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
   nccl_result (*Recv)(void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
   nccl_result (*Bcast)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  nccl_result (*AllGather)(const void*, void*, size_t, int, nccl_comm, cudaStream_t) = nullptr;
   nccl_result (*GroupStart)() = nullptr;
   nccl_result (*GroupEnd)() = nullptr;
   const char* (*ErrStr)(nccl_result) = nullptr;
@@ -147,11 +148,12 @@ NcclApi& nccl() {
     api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.Bcast = reinterpret_cast<decltype(api.Bcast)>(sym("ncclBroadcast"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.ErrStr = reinterpret_cast<decltype(api.ErrStr)>(sym("ncclGetErrorString"));
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
-             api.Bcast && api.GroupStart && api.GroupEnd && api.ErrStr;
+             api.Bcast && api.AllGather && api.GroupStart && api.GroupEnd && api.ErrStr;
   });
   return api;
 }
@@ -392,6 +394,17 @@ int ltfb_trainer_load_ae_source(ltfb_trainer* t, const float* y, uint64_t n) {
   });
 }
 
+int ltfb_trainer_ae_alloc_source(ltfb_trainer* t, uint64_t rows) {
+  return guarded([&] { T(t).ae_alloc_source(rows); });
+}
+
+int ltfb_trainer_ae_fill_from_store(ltfb_trainer* t, const uint32_t* slots, uint64_t n, uint64_t dst_row) {
+  return guarded([&] {
+    if (!slots && n) throw ltfb::ContractError("ae_fill_from_store: null slots");
+    T(t).ae_fill_from_store(slots, n, dst_row);
+  });
+}
+
 int ltfb_trainer_ae_step(ltfb_trainer* t, const uint32_t* idx, uint64_t n, double* loss) {
   return guarded([&] {
     if (!idx || n == 0) throw ltfb::ContractError("ae_step: empty batch");
@@ -572,6 +585,22 @@ int ltfb_trainer_exchange(ltfb_trainer* t, ltfb_comm* c, int peer) {
     nccl_check(api.Send(tr.generator_dev(), n, kNcclFloat, peer, c->comm, tr.stream()), "ncclSend");
     nccl_check(api.Recv(tr.incoming_dev(), n, kNcclFloat, peer, c->comm, tr.stream()), "ncclRecv");
     nccl_check(api.GroupEnd(), "ncclGroupEnd");
+  });
+}
+
+int ltfb_trainer_ae_allgather(ltfb_trainer* t, ltfb_comm* c, uint64_t rows_per_rank) {
+  return guarded([&] {
+    auto& tr = T(t);
+    if (!c) throw ltfb::ContractError("null communicator");
+    if (rows_per_rank * static_cast<uint64_t>(c->nranks) > tr.ae_source_rows())
+      throw ltfb::ContractError("ae_allgather: AE source smaller than rows_per_rank x ranks");
+    DeviceGuard g(tr.device());
+    const std::size_t count = rows_per_rank * static_cast<std::size_t>(tr.out_pad());
+    float* buf = tr.ae_source_dev();
+    // in place: rank r's rows sit at [r * rows_per_rank, (r + 1) * rows_per_rank)
+    nccl_check(nccl().AllGather(buf + count * static_cast<std::size_t>(c->rank), buf, count, kNcclFloat, c->comm,
+                                tr.stream()),
+               "ncclAllGather");
   });
 }
 

@@ -232,6 +232,18 @@ __global__ void k_begin_epoch(Counters* ctr, unsigned epoch) {
   ctr->step_in_epoch = 0;
 }
 
+/// Store rows by slot into a row-major destination slab (the distributed AE
+/// batch, runner.hpp:255-277 with the union sharded over the ranks' stores):
+/// one CTA per row, float4 copies of the padded row.
+__global__ void k_gather_rows(const float* __restrict__ src, const unsigned* __restrict__ slots, int n,
+                              float* __restrict__ dst, int out_pad) {
+  const int r = blockIdx.x;
+  if (r >= n) return;
+  const float4* s = reinterpret_cast<const float4*>(src + (long long)slots[r] * out_pad);
+  float4* d = reinterpret_cast<float4*>(dst + (long long)r * out_pad);
+  for (int i = threadIdx.x; i < out_pad / 4; i += blockDim.x) d[i] = __ldg(s + i);
+}
+
 /// Start of a streamed run: the hand-off counters restart, the first step's
 /// h counts as ready (the row kernel or the previous run produced it).
 __global__ void k_stream_init(StepSync* sy, int run_id, unsigned* grid_bar) {
@@ -303,6 +315,10 @@ void launch_gate(const volatile int* flag, cudaStream_t s) { k_gate<<<1, 1, 0, s
 
 void launch_stream_init(StepSync* sy, int run_id, unsigned* grid_bar, cudaStream_t s) {
   k_stream_init<<<1, 256, 0, s>>>(sy, run_id, grid_bar);
+}
+
+void launch_gather_rows(const float* src, const unsigned* slots, int n, float* dst, int out_pad, cudaStream_t s) {
+  if (n > 0) k_gather_rows<<<n, 256, 0, s>>>(src, slots, n, dst, out_pad);
 }
 
 void prepare_stream_kernels() {

@@ -113,6 +113,8 @@ int post_tpl_kind(const StepArgs& a);
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s);
 void launch_begin_epoch(Counters* ctr, unsigned epoch, cudaStream_t s);
 void launch_gate(const volatile int* flag, cudaStream_t s);
+/// dst[r] = src[slots[r]] for n rows of out_pad floats (device pointers).
+void launch_gather_rows(const float* src, const unsigned* slots, int n, float* dst, int out_pad, cudaStream_t s);
 
 /// Autoencoder pre-training step (k_ae.cu): one batch of n rows of the AE
 /// source slab selected by idx; every pointer device memory.

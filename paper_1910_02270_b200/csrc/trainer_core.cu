@@ -1326,6 +1326,29 @@ void DeviceTrainer::load_ae_source(const float* y, std::size_t n) {
   ae_rows_ = n;
 }
 
+void DeviceTrainer::ae_alloc_source(std::size_t rows) {
+  DeviceGuard g(spec_.device);
+  if (rows == 0) throw ContractError("ae_alloc_source: empty source");
+  const std::size_t op = static_cast<std::size_t>(margs_.out_pad);
+  ae_y_.alloc(rows * op);
+  LTFB_CUDA(cudaMemsetAsync(ae_y_.p, 0, ae_y_.bytes(), stream_));
+  ae_rows_ = rows;
+  sync_stream();
+}
+
+void DeviceTrainer::ae_fill_from_store(const std::uint32_t* slots, std::size_t n, std::size_t dst_row) {
+  DeviceGuard g(spec_.device);
+  if (dst_row + n > ae_rows_) throw ContractError("ae_fill_from_store: rows outside the AE source");
+  for (std::size_t i = 0; i < n; ++i)
+    if (slots[i] >= n_part_) throw ContractError("ae_fill_from_store: slot outside the store");
+  if (n == 0) return;
+  if (ae_fill_slots_.n < n) ae_fill_slots_.alloc(std::max<std::size_t>(n, 128));
+  LTFB_CUDA(cudaMemcpyAsync(ae_fill_slots_.p, slots, n * 4, cudaMemcpyHostToDevice, stream_));
+  ltfb_dev::launch_gather_rows(sy_.p, ae_fill_slots_.p, static_cast<int>(n),
+                               ae_y_.p + dst_row * static_cast<std::size_t>(margs_.out_pad), margs_.out_pad, stream_);
+  ++launches_;
+}
+
 /// surrogate/train_ops.hpp:71-81 on the device: loss, gradients, then
 /// Adam(enc) and Adam(dec) with the reference's NumericError semantics
 /// (a non-finite loss or enc gradient changes nothing; a non-finite dec

@@ -150,6 +150,14 @@ class DeviceTrainer {
   /// One AE step on rows `rows_idx` (slots of the AE source store).
   double ae_step(const std::uint32_t* rows_idx, std::size_t n);
   void load_ae_source(const float* y, std::size_t n);
+  /// Distributed AE (C5: the union of the partitions sharded over the ranks'
+  /// stores): a zeroed AE source slab of `rows` rows, filled per step from
+  /// the stores (ae_fill_from_store, then an all-gather across ranks).
+  void ae_alloc_source(std::size_t rows);
+  void ae_fill_from_store(const std::uint32_t* slots, std::size_t n, std::size_t dst_row);
+  float* ae_source_dev() { return ae_y_.p; }
+  std::size_t ae_source_rows() const { return ae_rows_; }
+  int out_pad() const { return margs_.out_pad; }
 
   // exposed for benchmarks: launches one step without reading back
   void enqueue_steps(std::size_t n);
@@ -329,6 +337,7 @@ class DeviceTrainer {
 
   // AE pre-training (k_ae.cu)
   DevBuf<float> ae_y_;
+  DevBuf<unsigned> ae_fill_slots_;
   std::size_t ae_rows_ = 0;
   DevBuf<unsigned> ae_idx_;
   DevBuf<double> ae_loss_;

@@ -30,7 +30,7 @@ import numpy as np
 from .api import (BundleDataset, IoError, write_synth_bundles, CycleGan, Dataset, EvalRecord, HistorySegment, RoundRecord, Trainer, TrainerConfig,
                   TrainerRoundRecord, TransferRecord, ConfigError, ContractError, hex64, fnv1a64,
                   make_cyclegan, mix_seed, pair_trainers, param_count, pretrain_autoencoder,
-                  reinit_gan_nets, split_dataset, tournament_round, EvalMetric)
+                  reinit_gan_nets, split_dataset, tournament_round, EvalMetric, ae_batch_rows)
 
 
 @dataclass
@@ -74,6 +74,55 @@ class RunConfig:
     # slice) or "shard" (rank r holds 1/k of it; all k models are evaluated on
     # every shard and the metrics combined)
     validation_sharding: str = "replicate"
+    # run_experiment_rank: "replicate" (every rank pre-trains the AE on a host
+    # copy of the whole union of the training partitions) or "shard" (each
+    # AE batch is assembled from the ranks' HBM stores by an NCCL all-gather:
+    # no rank holds the union; BASELINE config C5). Same draws, same result.
+    ae_sharding: str = "replicate"
+
+
+def sharded_ae_plan(parts, batch_size: int, steps: int, seed: int):
+    """runner.hpp:251-277 with the union of the training partitions sharded
+    over the ranks' stores: for the draws the replicated pre-training makes
+    (Rng(mix_seed({seed, 0xae1})).below over the sorted union), each batch
+    row's owning rank and its slot in that rank's store (the position in the
+    rank's partition). Returns (owner [steps x b], slot [steps x b], b)."""
+    ids = np.concatenate([np.asarray(p, np.uint32) for p in parts])
+    rk = np.concatenate([np.full(len(p), r, np.int32) for r, p in enumerate(parts)])
+    sl = np.concatenate([np.arange(len(p), dtype=np.uint32) for p in parts])
+    order = np.argsort(ids, kind="stable")  # the sorted union
+    b = min(batch_size, ids.size)
+    draws = ae_batch_rows(seed, ids.size, b, steps) if steps else np.zeros((0, b), np.uint32)
+    return rk[order][draws], sl[order][draws], b
+
+
+def sharded_ae_indices(owner_row: np.ndarray, k: int, b: int) -> np.ndarray:
+    """Source row of every batch row after the all-gather: rank r's rows sit
+    at [r b, r b + count_r) in batch order."""
+    idx = np.empty(owner_row.size, np.uint32)
+    for r in range(k):
+        pos = np.nonzero(owner_row == r)[0]
+        idx[pos] = r * b + np.arange(pos.size, dtype=np.uint32)
+    return idx
+
+
+def pretrain_autoencoder_sharded(trainer, comm, parts, rank: int, steps: int, batch_size: int, seed: int) -> list:
+    """AE pre-training (train_ops.hpp:71-81, runner.hpp:249-279) on this
+    rank's Trainer: per step every rank gathers the batch rows its store
+    holds into its block of the AE source, an in-place NCCL all-gather
+    assembles the batch on every rank, and every rank runs the same AE step
+    (replicated, deterministic: identical enc / dec everywhere)."""
+    k = len(parts)
+    owner, slot, b = sharded_ae_plan(parts, batch_size, steps, seed)
+    trainer.ae_alloc_source(k * b)
+    out = []
+    for s in range(steps):
+        mine = np.nonzero(owner[s] == rank)[0]
+        trainer.ae_fill_from_store(slot[s][mine], rank * b)
+        if k > 1:
+            comm.ae_allgather(trainer, b)
+        out.append((s + 1, trainer.ae_step(sharded_ae_indices(owner[s], k, b))))
+    return out
 
 
 @dataclass
@@ -325,6 +374,9 @@ class NcclRoundComm:
     def exchange(self, trainer, peer: int):
         trainer.exchange(self.comm, peer)
 
+    def ae_allgather(self, trainer, rows_per_rank: int):
+        trainer.ae_allgather(self.comm, rows_per_rank)
+
     def all_gather(self, obj):
         out = [None] * self.world
         self.dist.all_gather_object(out, obj)
@@ -460,8 +512,20 @@ def run_experiment_rank(cfg: RunConfig, dataset: Dataset | None, comm, device: i
     split = split_dataset(dataset.total, k, cfg.validation_fraction, cfg.tournament_fraction, cfg.seed, k >= 2)
     history = RunHistory(mode=cfg.mode.replace("_", "-"), n_trainers=k)
     rcfg = RunConfig(**{**cfg.__dict__, "devices": (device,)})
-    base, history.pretrain = _base_model(rcfg, dataset, split[1])  # replicated, deterministic
-    t = _trainer_for(rcfg, dataset, base, split, comm.rank)
+    if cfg.ae_sharding not in ("replicate", "shard"):
+        raise ConfigError("ae_sharding must be 'replicate' or 'shard'")
+    if cfg.ae_sharding == "shard":
+        # the trainer's store first (its rows are the AE's source), then the
+        # AE pre-training on the trainer itself: reinit_gan_nets touches only
+        # fwd / inv / disc and the AE only enc / dec, so the order is free
+        base = make_cyclegan(cfg.dims, cfg.arch, mix_seed(cfg.seed, 0xAE0))
+        base.autoencoder_frozen = True
+        t = _trainer_for(rcfg, dataset, base, split, comm.rank)
+        history.pretrain = pretrain_autoencoder_sharded(t, comm, split[1], comm.rank, cfg.ae_steps,
+                                                        cfg.batch_size, cfg.seed) if cfg.ae_steps else []
+    else:
+        base, history.pretrain = _base_model(rcfg, dataset, split[1])  # replicated, deterministic
+        t = _trainer_for(rcfg, dataset, base, split, comm.rank)
     if rounds_enabled:
         warm_peer_links(t, comm)
     have_val = split[0].size > 0

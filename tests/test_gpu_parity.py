@@ -520,6 +520,7 @@ def test_multi_gpu_run_matches_reference(tmp_path):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
+    import json
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr", "127.0.0.1", "--master-port", "29533",
@@ -535,6 +536,19 @@ def test_multi_gpu_run_matches_reference(tmp_path):
     rb = [x.split(",") for x in open(os.path.join(gold, "summary.csv")).read().splitlines()]
     ints = [i for i, c in enumerate(rb[0]) if not c.startswith("final_")]
     assert [[row[i] for i in ints] for row in ra] == [[row[i] for i in ints] for row in rb]
+    # the desk_k2 run with the AE pre-training's batches gathered from the two
+    # ranks' HBM stores (NCCL all-gather, no rank holds the union: BASELINE
+    # C5) computes exactly what the replicated pre-training computes
+    outs = []
+    for ae, port in (("replicate", "29535"), ("shard", "29536")):
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                            "--master-addr", "127.0.0.1", "--master-port", port,
+                            os.path.join(repo, "tools", "dist_run.py"), "--golden", "desk_k2_", "--ae-sharding", ae],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        outs.append(json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]))
+    for key in ("pretrain", "g_total", "local", "best_hash"):
+        assert outs[0][key] == outs[1][key], key
     # the same run with the validation slice sharded over the two GPUs
     # (runner.sharded_validation): same checks against the reference
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",

@@ -127,3 +127,28 @@ def test_run_config_refuses_unsupported_store_modes():
     for kw in ({"data_store": "dynamic"}, {"data_store": "none"}, {"store_budget_mb": 64}):
         with pytest.raises(L.ConfigError):
             validate_run_config(L.RunConfig(**kw))
+
+
+def test_sharded_ae_plan_assembles_the_replicated_batch():
+    """runner.sharded_ae_plan / sharded_ae_indices: with the union of the
+    training partitions sharded over k ranks' stores, every rank's rows packed
+    into its block and an all-gather of the blocks, the AE step's source rows
+    are exactly the rows the replicated pre-training draws from the sorted
+    union (runner.hpp:255-277)."""
+    from paper_1910_02270_b200.runner import sharded_ae_indices, sharded_ae_plan
+    rng = np.random.default_rng(4)
+    total, k, b, steps, seed = 500, 3, 32, 6, 42
+    ids = rng.permutation(total).astype(np.uint32)
+    parts = [ids[:170], ids[170:330], ids[330:480]]  # ids[480:] is nobody's (validation)
+    y = rng.standard_normal((total, 7)).astype(np.float32)  # a row per global id
+    union = np.sort(np.concatenate(parts))
+    draws = L.ae_batch_rows(seed, union.size, b, steps)
+    owner, slot, bb = sharded_ae_plan(parts, b, steps, seed)
+    assert bb == b
+    for s in range(steps):
+        src = np.zeros((k * b, 7), np.float32)
+        for r in range(k):  # each rank fills its block from its own store
+            mine = np.nonzero(owner[s] == r)[0]
+            src[r * b:r * b + mine.size] = y[parts[r][slot[s][mine]]]
+        got = src[sharded_ae_indices(owner[s], k, b)]
+        assert np.array_equal(got, y[union[draws[s]]])

@@ -23,6 +23,7 @@ def main():
     p.add_argument("--golden", default="tiny_k2_")
     p.add_argument("--out", default=None, help="rank 0 writes the run directory here (outputs.py)")
     p.add_argument("--validation-sharding", default="replicate", choices=["replicate", "shard"])
+    p.add_argument("--ae-sharding", default="replicate", choices=["replicate", "shard"])
     a = p.parse_args()
     import torch
     import torch.distributed as dist
@@ -49,7 +50,7 @@ def main():
                       interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed, gen_n=gen_n,
                       samples_per_file=spf, spec_seed=spec_seed, sampling_seed=sampling_seed,
                       data_dir="data_" + pfx.rstrip("_"),  # = tests/golden/run_<pfx>/config.json
-                      validation_sharding=a.validation_sharding)
+                      validation_sharding=a.validation_sharding, ae_sharding=a.ae_sharding)
     res = L.run_experiment_rank(cfg, ds, comm, device=local)
     ok = True
     if rank == 0:
@@ -69,12 +70,19 @@ def main():
             "best_trainer": res.best_trainer == int(g[pfx + "best_trainer"][0]),
             "evals_rel": rel([e.combined for e in h.evals], g[pfx + "evals_combined"]),
         }
+        checks["pretrain_rel"] = rel([pp[1] for pp in h.pretrain], g[pfx + "pretrain_loss"]) if ae_steps else 0.0
+        # end to end with the device AE (tests/test_gpu_parity.py REL_LOSS_DEVICE_AE)
         ok = (checks["steps_order"] and checks["kept"] and checks["xf_bytes"] and checks["best_trainer"]
-              and checks["g_total_rel"] < 1e-3 and checks["local_rel"] < 1e-3 and checks["evals_rel"] < 1e-3)
+              and checks["g_total_rel"] < 5e-4 and checks["local_rel"] < 5e-4 and checks["evals_rel"] < 5e-4
+              and checks["pretrain_rel"] < 1e-4)
         if a.out:
             L.write_run_outputs(a.out, cfg, h, res.best_model)
-        print(json.dumps({"golden": pfx, "ranks": world, "validation": a.validation_sharding, "ok": bool(ok), "checks": checks,
-                          "rounds": len(h.rounds), "exchange": "nccl device-to-device"}))
+        print(json.dumps({"golden": pfx, "ranks": world, "validation": a.validation_sharding,
+                          "ae": a.ae_sharding, "ok": bool(ok), "checks": checks,
+                          "rounds": len(h.rounds), "exchange": "nccl device-to-device",
+                          "pretrain": [pp[1] for pp in h.pretrain], "g_total": [s.g_total for s in h.steps],
+                          "local": [r.local_metric for r in h.trainer_rounds],
+                          "best_hash": L.hex64(res.best_model.model_hash())}))
     okt = [ok]
     dist.broadcast_object_list(okt, src=0)
     comm.comm.close()

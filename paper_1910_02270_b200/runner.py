@@ -106,14 +106,15 @@ def sharded_ae_indices(owner_row: np.ndarray, k: int, b: int) -> np.ndarray:
     return idx
 
 
-def pretrain_autoencoder_sharded(trainer, comm, parts, rank: int, steps: int, batch_size: int, seed: int) -> list:
+def pretrain_autoencoder_sharded(trainer, comm, parts, rank: int, steps: int, batch_size: int, seed: int,
+                                 plan=None) -> list:
     """AE pre-training (train_ops.hpp:71-81, runner.hpp:249-279) on this
     rank's Trainer: per step every rank gathers the batch rows its store
     holds into its block of the AE source, an in-place NCCL all-gather
     assembles the batch on every rank, and every rank runs the same AE step
     (replicated, deterministic: identical enc / dec everywhere)."""
     k = len(parts)
-    owner, slot, b = sharded_ae_plan(parts, batch_size, steps, seed)
+    owner, slot, b = plan if plan is not None else sharded_ae_plan(parts, batch_size, steps, seed)
     trainer.ae_alloc_source(k * b)
     out = []
     for s in range(steps):

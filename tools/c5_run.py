@@ -34,7 +34,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1910_02270_b200 as L
-    from paper_1910_02270_b200.runner import pretrain_autoencoder_sharded
+    from paper_1910_02270_b200.runner import pretrain_autoencoder_sharded, sharded_ae_plan
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -69,9 +69,17 @@ def main():
     render_s = max_all(time.perf_counter() - t0)
     out_pad = (dims.output_dim() + 3) // 4 * 4
     store_bytes = int(train_parts[rank].size) * (dims.input_dim + out_pad) * 4
-    # AE pre-training over the sharded union (first step untimed: allocation)
+    # AE pre-training over the sharded union: the host plan (which rank holds
+    # each draw: a sort of the union ids), then the device steps
     t0 = time.perf_counter()
-    pre = pretrain_autoencoder_sharded(tr, comm, train_parts, rank, a.ae_steps, a.batch, seed)
+    plan = sharded_ae_plan(train_parts, a.batch, a.ae_steps + 1, seed)
+    plan_s = max_all(time.perf_counter() - t0)
+    pretrain_autoencoder_sharded(tr, comm, train_parts, rank, 1, a.batch, seed,
+                                 plan=(plan[0][:1], plan[1][:1], plan[2]))  # allocation, first launch
+    tr.synchronize()
+    t0 = time.perf_counter()
+    pre = pretrain_autoencoder_sharded(tr, comm, train_parts, rank, a.ae_steps, a.batch, seed,
+                                       plan=(plan[0][1:], plan[1][1:], plan[2]))
     tr.synchronize()
     ae_ms = max_all((time.perf_counter() - t0) * 1e3 / max(1, a.ae_steps))
     # epoch plan of this rank's partition (the host shuffle the trainer runs
@@ -107,7 +115,7 @@ def main():
                           a.total, dims.output_dim(), world, a.batch, a.interval),
             "n_gpus": world, "samples_total": a.total, "partition_rows_per_gpu": int(train_parts[rank].size),
             "store_bytes_per_gpu": store_bytes, "store_gb_per_gpu": store_bytes / 1e9,
-            "render_s": render_s, "ae_steps": a.ae_steps, "ae_ms_per_step": ae_ms,
+            "render_s": render_s, "ae_plan_s": plan_s, "ae_steps": a.ae_steps, "ae_ms_per_step": ae_ms,
             "ae_source": "batches gathered from every rank's store (NCCL all-gather), union never replicated",
             "ae_first_losses": [x[1] for x in pre[:3]],
             "epoch_plan_ms": plan_ms, "steps": a.steps, "rounds": rounds[0],

@@ -354,53 +354,48 @@ __device__ __forceinline__ void pg_layer4(const NetS& n, int l, int below, int R
 
 __device__ __noinline__ void pg_net(const NetS& n, int x, int R, int pg) {
   float* s = S();
-  {
-    bool all4 = true;
-    for (int l = 0; l < n.L; ++l) all4 = all4 && (n.w[l] % 4 == 0);
-    if (all4) {  // one pass per layer, float4 operands (no barrier needed: disjoint outputs)
-      for (int l = 0; l < n.L; ++l) pg_layer4(n, l, l == 0 ? x : n.a[l - 1], R, pg);
-      return;
-    }
-  }
-  int base = 0;
-  int start[kMaxL + 1];
-  for (int l = 0; l < n.L; ++l) {
-    start[l] = base;
-    base += ((n.w[l] + 2) >> 1) * n.w[l + 1];
-  }
-  start[n.L] = base;
-  for (int t = threadIdx.x; t < base; t += kThreads) {
-    int l = 0;
-    while (t >= start[l + 1]) ++l;
-    const int IN = n.w[l], OUT = n.w[l + 1], q = t - start[l];
-    const int kp = q / OUT, j = q - kp * OUT;
-    const int k0 = 2 * kp, k1 = k0 + 1;
+  // per layer: the float4 path where the input width is a multiple of 4,
+  // else the pairwise path (same per-element row order either way: outputs
+  // are disjoint, so no barrier between layers)
+  const int L = n.L;
+  for (int l = 0; l < L; ++l) {
+    const int IN = n.w[l], OUT = n.w[l + 1];
     const int below = l == 0 ? x : n.a[l - 1];
-    const float* d = s + n.dz[l] + j;
-    float a0 = 0.0f, a1 = 0.0f;
-    if (k1 < IN) {
-      const float* b0 = s + below + k0;
-#pragma unroll 4
-      for (int r = 0; r < R; ++r) {
-        const float dv = d[r * OUT];
-        a0 = fmaf(b0[r * IN], dv, a0);
-        a1 = fmaf(b0[r * IN + 1], dv, a1);
-      }
-    } else if (k0 < IN) {  // k1 == IN: bias
-      const float* b0 = s + below + k0;
-#pragma unroll 4
-      for (int r = 0; r < R; ++r) {
-        const float dv = d[r * OUT];
-        a0 = fmaf(b0[r * IN], dv, a0);
-        a1 += dv;
-      }
-    } else {  // k0 == IN: bias only
-#pragma unroll 4
-      for (int r = 0; r < R; ++r) a0 += d[r * OUT];
+    if (IN % 4 == 0) {
+      pg_layer4(n, l, below, R, pg);
+      continue;
     }
+    const int items = ((IN + 2) >> 1) * OUT;
+    const float* dz = s + n.dz[l];
     const int pgW = pg + n.woff[l], pgb = pg + n.boff[l];
-    s[k0 < IN ? pgW + k0 * OUT + j : pgb + j] = a0;
-    if (k1 <= IN && k0 < IN) s[k1 < IN ? pgW + k1 * OUT + j : pgb + j] = a1;
+    for (int t = threadIdx.x; t < items; t += kThreads) {
+      const int kp = t / OUT, j = t - kp * OUT;
+      const int k0 = 2 * kp, k1 = k0 + 1;
+      const float* d = dz + j;
+      float a0 = 0.0f, a1 = 0.0f;
+      if (k1 < IN) {
+        const float* b0 = s + below + k0;
+#pragma unroll 4
+        for (int r = 0; r < R; ++r) {
+          const float dv = d[r * OUT];
+          a0 = fmaf(b0[r * IN], dv, a0);
+          a1 = fmaf(b0[r * IN + 1], dv, a1);
+        }
+      } else if (k0 < IN) {  // k1 == IN: bias
+        const float* b0 = s + below + k0;
+#pragma unroll 4
+        for (int r = 0; r < R; ++r) {
+          const float dv = d[r * OUT];
+          a0 = fmaf(b0[r * IN], dv, a0);
+          a1 += dv;
+        }
+      } else {  // k0 == IN: bias only
+#pragma unroll 4
+        for (int r = 0; r < R; ++r) a0 += d[r * OUT];
+      }
+      s[k0 < IN ? pgW + k0 * OUT + j : pgb + j] = a0;
+      if (k1 <= IN && k0 < IN) s[k1 < IN ? pgW + k1 * OUT + j : pgb + j] = a1;
+    }
   }
 }
 
@@ -861,6 +856,16 @@ __device__ __noinline__ void dz_warp(int g, const NetS& n, int l, int out) {
   __syncwarp();
 }
 
+/// Field f of a per-CTA shared array from cluster ranks base .. base+kC-1:
+/// every remote load issued before any is used (one DSMEM round trip, not
+/// kC dependent ones); callers then combine v[0..kC) in rank order.
+template <typename T>
+__device__ __forceinline__ void from_ranks(T* arr, int f, int base, T (&v)[kC]) {
+  cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+  for (int r = 0; r < kC; ++r) v[r] = cl.map_shared_rank(arr, base + r)[f];
+}
+
 /// Disc update: owner reduction, finite check (adam.hpp:95-102), Adam, and
 /// the DSMEM pull of the peers' updated slices + W^T rebuild. Returns d_ok;
 /// *d_loss gets the D-step loss (weighted mean of one shard).
@@ -877,13 +882,21 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
   const NetS& C = Y.net[kCd];
   adam_compute(a, kDisc, C, R.lo[0], R.hi[0], g_pre[0], g_pre[1], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0]);
   double d_sum = 0.0;
-  for (int r = 0; r < kC; ++r) d_sum += cl.map_shared_rank(s_loss, r)[0];
+  {
+    double v[kC];
+    from_ranks(s_loss, 0, 0, v);
+    for (int r = 0; r < kC; ++r) d_sum += v[r];
+  }
   const double n2 = 2.0 * (double)R.rows;
   *d_loss = ((double)R.rows * (d_sum / n2)) / (double)R.rows;
   cluster_sync();  // S2: flags
   ST();
   int all_ok = 1;
-  for (int r = 0; r < kC; ++r) all_ok &= cl.map_shared_rank(s_ok, r)[0];
+  {
+    int v[kC];
+    from_ranks(s_ok, 0, 0, v);
+    for (int r = 0; r < kC; ++r) all_ok &= v[r];
+  }
   const bool d_ok = isfinite(*d_loss) && all_ok;
   if (d_ok) adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0], 2);
   ST();
@@ -920,17 +933,27 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
     if (!R.split) s_ok[2] = iok;
   }
   double adv_sum = 0.0, cyc_sum = 0.0;
-  for (int r = 0; r < kC; ++r) {
-    adv_sum += cl.map_shared_rank(s_loss, r)[1];
-    cyc_sum += cl.map_shared_rank(s_loss, cb + r)[2];
+  {
+    double va[kC], vc[kC];
+    from_ranks(s_loss, 1, 0, va);
+    from_ranks(s_loss, 2, cb, vc);
+    for (int r = 0; r < kC; ++r) {
+      adv_sum += va[r];
+      cyc_sum += vc[r];
+    }
   }
   cluster_sync();  // S5: flags
   GSTAMP(27);
   ST();
   int all_f = 1, all_i = 1;
-  for (int r = 0; r < kC; ++r) {
-    all_f &= cl.map_shared_rank(s_ok, r)[1];
-    all_i &= cl.map_shared_rank(s_ok, cb + r)[2];
+  {
+    int vf[kC], vi[kC];
+    from_ranks(s_ok, 1, 0, vf);
+    from_ranks(s_ok, 2, cb, vi);
+    for (int r = 0; r < kC; ++r) {
+      all_f &= vf[r];
+      all_i &= vi[r];
+    }
   }
   const int rows = R.rows;
   const long long n_fwd = (long long)rows * m.out;
@@ -1087,9 +1110,15 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   cluster_sync();  // S2 (d_update's flags)
   double d_sum = 0.0;
   int all_ok = 1;
-  for (int r = 0; r < kC; ++r) {
-    d_sum += cl.map_shared_rank(s_loss, r)[0];
-    all_ok &= cl.map_shared_rank(s_ok, r)[0];
+  {
+    double vd[kC];
+    int vo[kC];
+    from_ranks(s_loss, 0, 0, vd);
+    from_ranks(s_ok, 0, 0, vo);
+    for (int r = 0; r < kC; ++r) {
+      d_sum += vd[r];
+      all_ok &= vo[r];
+    }
   }
   const double d_loss = ((double)rows * (d_sum / (2.0 * (double)rows))) / (double)rows;
   const bool d_ok = isfinite(d_loss) && all_ok;
@@ -1120,11 +1149,19 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     cluster_sync();  // S5
     double adv_sum = 0.0, cyc_sum = 0.0;
     int all_f = 1, all_i = 1;
-    for (int r = 0; r < kC; ++r) {
-      adv_sum += cl.map_shared_rank(s_loss, r)[1];
-      cyc_sum += cl.map_shared_rank(s_loss, kC + r)[2];
-      all_f &= cl.map_shared_rank(s_ok, r)[1];
-      all_i &= cl.map_shared_rank(s_ok, kC + r)[2];
+    {
+      double va[kC], vc[kC];
+      int vf[kC], vi[kC];
+      from_ranks(s_loss, 1, 0, va);
+      from_ranks(s_loss, 2, kC, vc);
+      from_ranks(s_ok, 1, 0, vf);
+      from_ranks(s_ok, 2, kC, vi);
+      for (int r = 0; r < kC; ++r) {
+        adv_sum += va[r];
+        cyc_sum += vc[r];
+        all_f &= vf[r];
+        all_i &= vi[r];
+      }
     }
     const double adv = adv_sum / (double)rows;
     const double cyc = cyc_sum / (double)((long long)rows * m.in);

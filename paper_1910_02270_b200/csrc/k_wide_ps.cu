@@ -536,48 +536,53 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
       const int q_all = rows * (kW / 4);  // float4 outputs of P_enc or P_dec
       const int lo = (int)((long long)q_all * blockIdx.x / S);
       const int hi = (int)((long long)q_all * (blockIdx.x + 1) / S);
-      const int nq = hi - lo;
       float4* stage = reinterpret_cast<float4*>(sm + kRedOff);                  // [S][kMaxQ]
       float4* part = reinterpret_cast<float4*>(sm + kRedOff) + kMaxS * kMaxQ;  // [kG][kMaxQ]
       const int g = threadIdx.x / 32, o = threadIdx.x % 32;  // o < nq <= kMaxQ active
       const long long pstride4 = (long long)a.B * kW / 4;
       const float4* P4 = reinterpret_cast<const float4*>(ph2 ? a.P_dec : a.P_enc);
-      // every partial's slice [lo, hi) by one bulk copy (TMA engine) per
+      // this CTA's slice [lo, hi) in chunks of kMaxQ outputs (one chunk when
+      // S >= 128): every partial's chunk by one bulk copy (TMA engine) per
       // source CTA, then summed in ascending partial order per group
-      if (threadIdx.x == 0 && nq > 0) tc::mbar_expect_tx(&rbar, (uint32_t)(S * nq * 16));
-      __syncthreads();
-      if ((int)threadIdx.x < S && nq > 0) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                tc::smem_u32(stage + threadIdx.x * kMaxQ)),
-            "l"(P4 + threadIdx.x * pstride4 + lo), "r"(nq * 16), "r"(tc::smem_u32(&rbar))
-            : "memory");
-      }
-      if (nq > 0) mbar_wait_to(&rbar, rbar_par);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (o < nq)
-        for (int sidx = g; sidx < S; sidx += kG) {
-          const float4 v = stage[sidx * kMaxQ + o];
-          acc.x += v.x;
-          acc.y += v.y;
-          acc.z += v.z;
-          acc.w += v.w;
+      for (int c0 = lo; c0 < hi; c0 += kMaxQ) {
+        const int nq = min(kMaxQ, hi - c0);
+        if (threadIdx.x == 0) tc::mbar_expect_tx(&rbar, (uint32_t)(S * nq * 16));
+        __syncthreads();
+        if ((int)threadIdx.x < S) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  tc::smem_u32(stage + threadIdx.x * kMaxQ)),
+              "l"(P4 + threadIdx.x * pstride4 + c0), "r"(nq * 16), "r"(tc::smem_u32(&rbar))
+              : "memory");
         }
-      if (o < kMaxQ) part[g * kMaxQ + o] = acc;
-      __syncthreads();
-      if (g == 0 && o < nq) {
-        float4 t = part[o];
-        for (int u = 1; u < kG; ++u) {
-          const float4 w = part[u * kMaxQ + o];
-          t.x += w.x;
-          t.y += w.y;
-          t.z += w.z;
-          t.w += w.w;
+        mbar_wait_to(&rbar, rbar_par);
+        rbar_par ^= 1u;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (o < nq)
+          for (int sidx = g; sidx < S; sidx += kG) {
+            const float4 v = stage[sidx * kMaxQ + o];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+          }
+        if (o < kMaxQ) part[g * kMaxQ + o] = acc;
+        __syncthreads();
+        if (g == 0 && o < nq) {
+          float4 t = part[o];
+          for (int u = 1; u < kG; ++u) {
+            const float4 w = part[u * kMaxQ + o];
+            t.x += w.x;
+            t.y += w.y;
+            t.z += w.z;
+            t.w += w.w;
+          }
+          float4* dst = reinterpret_cast<float4*>(ph2 ? r.red_dec[k & 1] : r.red_enc[k & 1]);
+          dst[c0 + o] = t;
+          __threadfence();
         }
-        float4* dst = reinterpret_cast<float4*>(ph2 ? r.red_dec[k & 1] : r.red_enc[k & 1]);
-        dst[lo + o] = t;
-        __threadfence();
+        __syncthreads();  // stage / part are refilled by the next chunk
       }
       if (ph2 && blockIdx.x == 0 && warp == 0) {  // forward-MAE total: strided partials, fixed xor tree
         double v[5];
@@ -591,7 +596,6 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
           __threadfence();
         }
       }
-      if (nq > 0) rbar_par ^= 1u;
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
@@ -636,8 +640,10 @@ __global__ void __launch_bounds__(wp::kThreads, 1)
 
 // ----------------------------------------------------------------- host --
 bool wide_ps_supported(const StepArgs& a, int S) {
-  return a.m.E1 == wp::kW && a.m.D == wp::kW && a.B <= 128 && a.m.out >= wp::kTileN && S >= 128 &&
-         S <= (int)wp::kMaxS && (a.B * (wp::kW / 4) + S - 1) / S <= wp::kMaxQ;
+  // every CTA owns >= 1 column tile (S <= tiles); the reduction walks its
+  // output slice in chunks of kMaxQ
+  return a.m.E1 == wp::kW && a.m.D == wp::kW && a.B <= 128 && a.m.out >= wp::kTileN && S >= 1 &&
+         S <= (int)wp::kMaxS && S <= (a.m.out + wp::kTileN - 1) / wp::kTileN;
 }
 
 static PerDevice g_wide_ps_attr;

@@ -462,71 +462,77 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
     const int q_enc = rows * (kW / 4), q_all = 2 * q_enc;
     const int lo = (int)((long long)q_all * blockIdx.x / gridDim.x);
     const int hi = (int)((long long)q_all * (blockIdx.x + 1) / gridDim.x);
-    const int nq = hi - lo;  // <= kMaxQ for the shapes the kernel accepts
     float4* part = reinterpret_cast<float4*>(sm);  // [G][kMaxQ]
     const int G = kThreads / kMaxQ;                // 10 groups
     const int g = threadIdx.x / kMaxQ, o = threadIdx.x % kMaxQ;
     const long long pstride4 = (long long)a.B * kW / 4;
-    // every partial's slice [lo, hi) arrives by one or two bulk copies (TMA
-    // engine, one per source CTA, issued by 148 threads) into shared memory:
-    // far cheaper than 16 dependent-free LDG.128 per thread through L1
+    // this CTA's output slice [lo, hi) in chunks of kMaxQ float4 (one chunk
+    // unless the grid is small, e.g. 97 CTAs at desk dims with B = 128):
+    // every partial's chunk arrives by one or two bulk copies (TMA engine,
+    // one per source CTA) into shared memory
     float4* stage = reinterpret_cast<float4*>(sm + 8192);  // [S][kMaxQ]
-    const int e0 = lo, e1 = min(hi, q_enc), d0 = max(lo, q_enc), d1 = hi;
-    const int ne = max(0, e1 - e0), nd = max(0, d1 - d0);
-    if (threadIdx.x == 0 && nq > 0) tc::mbar_expect_tx(&rbar, (uint32_t)(a.S * nq * 16));
-    __syncthreads();
-    if ((int)threadIdx.x < a.S && nq > 0) {
-      const int sidx = threadIdx.x;
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      const uint32_t dst = tc::smem_u32(stage + sidx * kMaxQ);
-      const float4* pe4 = reinterpret_cast<const float4*>(a.P_enc) + sidx * pstride4;
-      const float4* pd4 = reinterpret_cast<const float4*>(a.P_dec) + sidx * pstride4;
-      if (ne > 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-            "l"(pe4 + e0), "r"(ne * 16), "r"(tc::smem_u32(&rbar))
-            : "memory");
-      if (nd > 0)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                dst + 16u * (uint32_t)ne),
-            "l"(pd4 + (d0 - q_enc)), "r"(nd * 16), "r"(tc::smem_u32(&rbar))
-            : "memory");
-    }
-    if (nq > 0) tc::mbar_wait(&rbar, 0);
-    float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    if (o < nq) {
-      constexpr int kMaxPer = 16;  // ceil(148 / 10)
+    uint32_t rpar = 0;
+    for (int c0 = lo; c0 < hi; c0 += kMaxQ) {
+      const int c1 = min(hi, c0 + kMaxQ), nq = c1 - c0;
+      const int e0 = c0, e1 = min(c1, q_enc), d0 = max(c0, q_enc), d1 = c1;
+      const int ne = max(0, e1 - e0), nd = max(0, d1 - d0);
+      if (threadIdx.x == 0) tc::mbar_expect_tx(&rbar, (uint32_t)(a.S * nq * 16));
+      __syncthreads();
+      if ((int)threadIdx.x < a.S) {
+        const int sidx = threadIdx.x;
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const uint32_t dst = tc::smem_u32(stage + sidx * kMaxQ);
+        const float4* pe4 = reinterpret_cast<const float4*>(a.P_enc) + sidx * pstride4;
+        const float4* pd4 = reinterpret_cast<const float4*>(a.P_dec) + sidx * pstride4;
+        if (ne > 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+              "l"(pe4 + e0), "r"(ne * 16), "r"(tc::smem_u32(&rbar))
+              : "memory");
+        if (nd > 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  dst + 16u * (uint32_t)ne),
+              "l"(pd4 + (d0 - q_enc)), "r"(nd * 16), "r"(tc::smem_u32(&rbar))
+              : "memory");
+      }
+      tc::mbar_wait(&rbar, rpar);
+      rpar ^= 1u;
+      float4 acc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      if (o < nq) {
+        constexpr int kMaxPer = 16;  // ceil(148 / 10)
 #pragma unroll
-      for (int u = 0; u < kMaxPer; ++u) {
-        const int sidx = g + u * G;
-        if (sidx < a.S) {
-          const float4 v = stage[sidx * kMaxQ + o];
-          acc.x += v.x;
-          acc.y += v.y;
-          acc.z += v.z;
-          acc.w += v.w;
+        for (int u = 0; u < kMaxPer; ++u) {
+          const int sidx = g + u * G;
+          if (sidx < a.S) {
+            const float4 v = stage[sidx * kMaxQ + o];
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+          }
         }
       }
-    }
-    if (prof && threadIdx.x == 0) s_ph[4] = clock64();
-    part[g * kMaxQ + o] = acc;
-    __syncthreads();
-    if (prof && threadIdx.x == 0) s_ph[5] = clock64();
-    if (g == 0 && o < nq) {
-      float4 t = part[o];
-      for (int k = 1; k < G; ++k) {
-        const float4 w = part[k * kMaxQ + o];
-        t.x += w.x;
-        t.y += w.y;
-        t.z += w.z;
-        t.w += w.w;
+      if (prof && threadIdx.x == 0) s_ph[4] = clock64();
+      part[g * kMaxQ + o] = acc;
+      __syncthreads();
+      if (prof && threadIdx.x == 0) s_ph[5] = clock64();
+      if (g == 0 && o < nq) {
+        float4 t = part[o];
+        for (int k = 1; k < G; ++k) {
+          const float4 w = part[k * kMaxQ + o];
+          t.x += w.x;
+          t.y += w.y;
+          t.z += w.z;
+          t.w += w.w;
+        }
+        const int q = c0 + o;
+        float4* red_enc = reinterpret_cast<float4*>(a.scratch + a.L.red_enc);
+        float4* red_dec = reinterpret_cast<float4*>(a.scratch + a.L.red_dec);
+        if (q < q_enc) red_enc[q] = t;
+        else red_dec[q - q_enc] = t;
       }
-      const int q = lo + o;
-      float4* red_enc = reinterpret_cast<float4*>(a.scratch + a.L.red_enc);
-      float4* red_dec = reinterpret_cast<float4*>(a.scratch + a.L.red_dec);
-      if (q < q_enc) red_enc[q] = t;
-      else red_dec[q - q_enc] = t;
+      __syncthreads();  // stage / part are refilled by the next chunk
     }
     if (prof && threadIdx.x == 0) s_ph[6] = clock64();
     if (blockIdx.x == 0 && warp == 0) {  // MAE total: lanes own strided partials, fixed xor tree
@@ -555,9 +561,9 @@ __global__ void __launch_bounds__(wt::kThreads, 1)
 
 // ----------------------------------------------------------------- host --
 bool wide_tc_supported(const StepArgs& a) {
-  // one CTA per SM (<= 160 partials for the in-kernel reduction's 10 x 16 loads)
-  return a.m.E1 == wt::kW && a.m.D == wt::kW && a.B <= wt::kRows && a.m.out >= wt::kTileN && a.S <= 160 &&
-         (2 * a.B * (wt::kW / 4) + a.S - 1) / a.S <= 32;
+  // one CTA per SM (<= 160 partials for the in-kernel reduction's 10 x 16
+  // loads); the reduction walks its output slice in chunks, any grid size
+  return a.m.E1 == wt::kW && a.m.D == wt::kW && a.B <= wt::kRows && a.m.out >= wt::kTileN && a.S <= 160;
 }
 
 void launch_wide_tc(const StepArgs&, cudaStream_t) {

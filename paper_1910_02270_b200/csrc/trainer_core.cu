@@ -245,7 +245,7 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   // run, the persistent wide pass the others (and, for one split-K order on
   // every path, so do the launched wide passes)
   {
-    const int Ss = sm_count_ - 2 * ltfb_dev::kPostCluster;
+    const int Ss = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, static_cast<int>((ma.out + 31) / 32));
     const bool tool = std::getenv("CUDA_INJECTION64_PATH") != nullptr;  // ncu / compute-sanitizer serialise kernels
     // LTFB_NO_STREAM=1: launched steps; =2: launched steps with the streamed
     // step's wide CTA count (the two paths then sum in the same order)

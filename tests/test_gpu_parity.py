@@ -842,3 +842,29 @@ def test_cpp_run_experiment_matches_reference(golden):
     assert got["epochs_files_opened"] == [int(v) for v in g[p + "epochs_files_opened"]]
     assert got["epochs_bytes_read"] == [int(v) for v in g[p + "epochs_bytes_read"]]
     assert got["best_trainer"] == int(g[p + "best_trainer"][0])
+
+
+@pytest.mark.parametrize("mode", ["", "1"])
+def test_desk_b128_matches_oracle(oracle, mode, monkeypatch):
+    """Desk dims at B = 128 (the C5 shape: 97 column tiles, so the wide pass
+    runs 97 CTAs and each CTA reduces a slice of ~43 outputs in chunks), on
+    the streamed step and on the launched step (LTFB_NO_STREAM=1): step
+    losses within REL_LOSS of the C oracle over several steps."""
+    if mode:
+        monkeypatch.setenv("LTFB_NO_STREAM", mode)
+    else:
+        monkeypatch.delenv("LTFB_NO_STREAM", raising=False)
+    n = 700
+    ds = L.synthetic_dataset(DESK, n, sampling_seed=6, spec_seed=1)
+    model = L.make_cyclegan(DESK, L.SurrogateArch(), 13)
+    model.autoencoder_frozen = True
+    ids = np.arange(n, dtype=np.uint32)
+    t = L.Trainer(L.TrainerConfig(n_shards=1, batch_size=128, seed=4, train_ids=ids[60:], tournament_ids=ids[:60]),
+                  ds, model)
+    assert t.stream_mode() == (not mode)
+    t.train_steps(8)  # 640 rows: one epoch of 5 steps (the last short) + 3
+    got = np.array([[s.d_loss, s.g_total, s.g_fwd, s.g_adv, s.g_cyc] for s in t.history().steps])
+    og = oracle.Gan(list(DESK.as_tuple()), oracle.Arch(), 13)
+    ot = oracle.Trainer(og, ds.x, ds.y, ids[60:], 128, 4)
+    ref, _, _, _ = ot.steps(8)
+    assert rel(got, ref) < REL_LOSS

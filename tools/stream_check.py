@@ -19,8 +19,9 @@ p = argparse.ArgumentParser()
 p.add_argument("--steps", type=int, default=40)
 p.add_argument("--n", type=int, default=2000)
 p.add_argument("--time-steps", type=int, default=0)
+p.add_argument("--dims", default="paper", choices=["paper", "desk"])
 a = p.parse_args()
-dims = L.ModalityDims.paper_scale()
+dims = L.ModalityDims.paper_scale() if a.dims == "paper" else L.ModalityDims()
 ds = L.SynthDataset(dims, a.n, sampling_seed=1, spec_seed=1)
 m = L.make_cyclegan(dims, L.SurrogateArch(), 5)
 m.autoencoder_frozen = True

@@ -62,13 +62,23 @@ __global__ void __launch_bounds__(et::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int out = a.m.out, rows = a.rows, nc = a.nc;
   const int ntiles = (out + kN - 1) / kN;
-  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int nrb = (rows + 127) / 128;
+  // CTA grid = column-tile lanes x row groups: with fewer column tiles than
+  // SMs (desk dims: 49) the 128-row blocks of a large slice are dealt over
+  // row groups too (block rbg = gr + rb * rgn), so a C5-size tournament
+  // slice keeps every SM busy; paper dims: one row group, as before
+  const int cgn = min((int)gridDim.x, ntiles);
+  const int rgn = max(1, (int)gridDim.x / max(cgn, 1));
+  const int cb = (int)blockIdx.x % max(cgn, 1), gr = (int)blockIdx.x / max(cgn, 1);
+  const int nrb_all = (rows + 127) / 128;
+  const bool active = gr < rgn && gr < nrb_all;
+  const int my_tiles = active && ntiles > cb ? (ntiles - 1 - cb) / cgn + 1 : 0;
+  const int nrb = active ? (nrb_all - gr + rgn - 1) / rgn : 0;  // this CTA's row blocks
   const int nitems = my_tiles * nrb;  // item q = rb * my_tiles + i
   auto Ys = [&](int s) { return sm + s * kStage; };
   auto Wh = [&](int s) { return sm + s * kStage + kY; };
   auto Wl = [&](int s) { return sm + s * kStage + kY + kWh; };
-  auto tile_c0 = [&](int i) { return ((int)blockIdx.x + i * (int)gridDim.x) * kN; };
+  auto tile_c0 = [&](int i) { return (cb + i * cgn) * kN; };
+  auto rb_row0 = [&](int rb) { return (gr + rb * rgn) * 128; };  // first slice row of local row block rb
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -102,8 +112,8 @@ __global__ void __launch_bounds__(et::kThreads, 1)
         if (q >= kStages) tc::mbar_wait(&empty[s], ((uint32_t)(q / kStages) & 1u) ^ 1u);
         const int rb = q / my_tiles, c0 = tile_c0(q % my_tiles);
         tc::mbar_expect_tx(&full[s], kY + kWh);
-        tc::tma_load_2d(Ys(s), &tp.tm_y, &full[s], c0, rb * 128);
-        tc::tma_load_2d(Ys(s) + kYHalf, &tp.tm_y, &full[s], c0 + 32, rb * 128);
+        tc::tma_load_2d(Ys(s), &tp.tm_y, &full[s], c0, rb_row0(rb));
+        tc::tma_load_2d(Ys(s) + kYHalf, &tp.tm_y, &full[s], c0 + 32, rb_row0(rb));
         tc::tma_load_2d(Wh(s), &tp.tm_wdt, &full[s], 0, c0);
         tc::tma_load_2d(Wh(s) + kWk, &tp.tm_wdt, &full[s], 32, c0);
       }
@@ -146,7 +156,7 @@ __global__ void __launch_bounds__(et::kThreads, 1)
         tc::mbar_wait(&rb_done, (uint32_t)(rb - 1) & 1u);
         tc::tc_fence_after();
       }
-      const int row = rb * 128 + r;
+      const int row = rb_row0(rb) + r;
       for (int c = 0; c < nc; ++c) {  // h rows of both candidates -> TMEM (tf32 hi / lo)
         const float4* hp = reinterpret_cast<const float4*>(a.h + ((long long)c * rows + row) * kW);
 #pragma unroll

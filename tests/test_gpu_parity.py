@@ -868,3 +868,43 @@ def test_desk_b128_matches_oracle(oracle, mode, monkeypatch):
     ot = oracle.Trainer(og, ds.x, ds.y, ids[60:], 128, 4)
     ref, _, _, _ = ot.steps(8)
     assert rel(got, ref) < REL_LOSS
+
+
+def test_single_process_two_gpus_matches_reference(golden):
+    """RunConfig(devices=(0, 1)): one process driving a trainer on each of two
+    GPUs (kernel attributes and the split-cluster probe are set per device;
+    rounds copy payloads peer to peer). desk_k2 with the reference's AE
+    injected: losses, decisions, evaluations and the best trainer as the
+    reference's run; the C++ run_experiment the same way on tiny_k2."""
+    import os
+    import subprocess
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    g = golden("tournament")
+    pfx = "desk_k2_"
+    gen_n, spf, spec_seed, sampling_seed, k, batch, interval, budget, ae_steps, seed, shards = (
+        int(v) for v in g[pfx + "cfg"])
+    dims = L.ModalityDims(*(int(v) for v in g[pfx + "dims"]))
+    arch = L.SurrogateArch()
+    ds = L.synthetic_dataset(dims, gen_n, sampling_seed=sampling_seed, spec_seed=spec_seed, samples_per_file=spf)
+    ae = L.make_cyclegan(dims, arch, 0)
+    ae.blobs["enc"][:] = g[pfx + "ae_enc"]
+    ae.blobs["dec"][:] = g[pfx + "ae_dec"]
+    cfg = L.RunConfig(dims=dims, arch=arch, mode="ltfb", trainers=k, shards=shards, batch_size=batch,
+                      interval=interval, step_budget=budget, ae_steps=ae_steps, seed=seed, devices=(0, 1))
+    res = L.run_experiment(cfg, ds, autoencoder=ae)
+    h = res.history
+    assert rel([s.g_total for s in h.steps], g[pfx + "steps_g_total"]) < REL_LOSS
+    assert rel([s.d_loss for s in h.steps], g[pfx + "steps_d_loss"]) < REL_LOSS
+    assert [int(r.kept_incoming) for r in h.trainer_rounds] == [int(v) for v in g[pfx + "tr_kept"]]
+    assert rel([e.combined for e in h.evals], g[pfx + "evals_combined"]) < REL_LOSS
+    assert res.best_trainer == int(g[pfx + "best_trainer"][0])
+    exe = os.path.join(os.path.dirname(L.LIB_PATH), "run_experiment_test")
+    if os.path.exists(exe):
+        import json
+        r = subprocess.run([exe, "1"], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        got = json.loads(r.stdout.strip().splitlines()[-1])
+        assert rel(got["steps_g_total"], g["tiny_k2_steps_g_total"]) < REL_LOSS
+        assert got["tr_kept"] == [int(v) for v in g["tiny_k2_tr_kept"]]

@@ -633,30 +633,67 @@ __device__ __noinline__ void pull_net(const NetS& n, int gr, int rbase, bool wT)
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   const int count = n.count;
-  // one element of every owner slice per thread and round: the kC remote
-  // loads of a round are independent and go out back to back
-  int slice = 0;
-  for (int r = 0; r < kC; ++r) slice = max(slice, owner_lo(count, r + 1) - owner_lo(count, r));
-  for (int base = 0; base < slice; base += kThreads) {
-    const int i = base + (int)threadIdx.x;
-    float v[kC];
-    int e[kC];
+  int olo[kC + 1];
 #pragma unroll
-    for (int r = 0; r < kC; ++r) {
-      const int lo = owner_lo(count, r), hi = owner_lo(count, r + 1);
-      e[r] = lo + i < hi ? lo + i : -1;
-      v[r] = e[r] >= 0 ? cl.map_shared_rank(s + gr, rbase + r)[i] : 0.0f;
+  for (int r = 0; r <= kC; ++r) olo[r] = owner_lo(count, r);
+  // kPer elements per thread and round: every remote load of the round is
+  // issued before any value is stored (one DSMEM round trip per round)
+  constexpr int kPer = 8;
+  for (int base = 0; base < count; base += kThreads * kPer) {
+    float v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = base + u * kThreads + (int)threadIdx.x;
+      v[u] = 0.0f;
+      if (e < count) {
+        int r = 0;
+#pragma unroll
+        for (int q = 1; q < kC; ++q) r += e >= olo[q] ? 1 : 0;
+        v[u] = *cl.map_shared_rank(s + gr + (e - olo[r]), rbase + r);
+      }
     }
 #pragma unroll
-    for (int r = 0; r < kC; ++r) {
-      if (e[r] < 0) continue;
-      s[n.blob + e[r]] = v[r];
+    for (int u = 0; u < kPer; ++u) {
+      const int e = base + u * kThreads + (int)threadIdx.x;
+      if (e >= count) continue;
+      s[n.blob + e] = v[u];
       if (wT)
         for (int l = 0; l < n.L; ++l) {
-          const int in = n.w[l], out = n.w[l + 1], q = e[r] - n.woff[l];
+          const int in = n.w[l], out = n.w[l + 1], q = e - n.woff[l];
           if (q >= 0 && q < in * out) {
-            const int k = q / out, j = q - k * out;
-            s[n.T[l] + j * (in + 1) + k] = v[r];
+            const int k = q / out, jj = q - k * out;
+            s[n.T[l] + jj * (in + 1) + k] = v[u];
+          }
+        }
+    }
+  }
+}
+
+/// Streamed step: net n's new parameters from global memory (the owners'
+/// adam_commit wrote them before the cluster barrier that precedes this
+/// call) into this CTA's blob image (and W^T image if wT).
+__device__ __noinline__ void refresh_net(const NetS& n, const float* p, bool wT) {
+  float* s = S();
+  const int count = n.count;
+  constexpr int kPer = 8;
+  for (int base = 0; base < count; base += kThreads * kPer) {
+    float v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = base + u * kThreads + (int)threadIdx.x;
+      v[u] = e < count ? __ldcg(p + e) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = base + u * kThreads + (int)threadIdx.x;
+      if (e >= count) continue;
+      s[n.blob + e] = v[u];
+      if (wT)
+        for (int l = 0; l < n.L; ++l) {
+          const int in = n.w[l], out = n.w[l + 1], q = e - n.woff[l];
+          if (q >= 0 && q < in * out) {
+            const int k = q / out, jj = q - k * out;
+            s[n.T[l] + jj * (in + 1) + k] = v[u];
           }
         }
     }
@@ -1522,10 +1559,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_res[1] = res[1];
         s_res[2] = res[2];
       }
-      // the generator's new parameters straight from the owners' slices
-      // (no push, no closing barrier): fwd (blob) and inv (blob + W^T)
-      if (res[1]) pull_net(F, Y.gr[1], 0, false);
-      if (res[2]) pull_net(Y.net[kI], Y.gr[2], kC, true);
+      // the generator's new parameters from global memory, where the owners
+      // wrote them before S6: fwd (blob) and inv (blob + W^T)
+      if (res[0]) cluster_sync();  // S6 (the D/G half reaches it only when the G-step ran)
+      if (res[1]) refresh_net(F, a.p[kFwd], false);
+      if (res[2]) refresh_net(Y.net[kI], a.p[kInv], true);
       cp_wait_all();   // the next step's x rows
       __syncthreads();
       for (int i = tid; i < kR * m.in; i += kThreads) S()[Y.xs + i] = S()[Y.xn + i];
@@ -1615,7 +1653,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         PSTAMP(12);
         // the new fwd blob straight from the owners' slices (its W^T image is
         // rebuilt next step while this half waits for the dec half)
-        if (g[4] != 0.0) pull_net(F, Y.gr[1], 0, false);
+        GSTAMP(90);
+        cluster_sync();  // S6: the owners' new fwd (and the cyc half's inv) are in global memory
+        if (g[4] != 0.0) refresh_net(F, a.p[kFwd], false);
+        GSTAMP(91);
         __syncthreads();
         PSTAMP(13);
       }

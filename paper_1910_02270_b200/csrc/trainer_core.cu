@@ -942,6 +942,9 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
       // phase-2 tiles of CTA 0 in step 3: producer issue, staged, MMA2 issued, epilogue done, MMA3 issued
       if (steps > 4) {
         const std::size_t k = 3;
+        std::fprintf(stderr, "\n  pull: start %.2f end %.2f (us from c.decwait)",
+                     ((double)h[512 * k + 90] - (double)h[512 * k + 7]) * 1e-3,
+                     ((double)h[512 * k + 91] - (double)h[512 * k + 7]) * 1e-3);
         std::fprintf(stderr, "\n  post (us from c.decwait): S3b-arrive %.2f S3b %.2f fwd-bwd-start %.2f pg-start %.2f S4-arr %.2f S4 %.2f adam %.2f S5 %.2f gupd %.2f S6 %.2f nexth %.2f",
                      ((double)h[512 * k + 94] - (double)h[512 * k + 7]) * 1e-3,
                      ((double)h[512 * k + 95] - (double)h[512 * k + 7]) * 1e-3,

@@ -373,6 +373,9 @@ def main():
         round_once()
         rounds_ms.append(max_over_ranks(tr.timer_stop()))
     round_ms = statistics.mean(rounds_ms) if rounds_ms else None
+    # stage timeline of the streamed step (%globaltimer stamps; a separate,
+    # untimed pass -- DESIGN §3a)
+    stream_profile = tr.stream_profile(80) if tr.stream_mode() else {}
 
     # ---- e2e: same step through the C ABI with HOST buffers (pinned) -------
     import torch
@@ -480,6 +483,7 @@ def main():
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": step_bytes, "units": "one training step of B rows",
                      "traffic_version": KERNEL_VERSION},
+        "stream_profile_us": stream_profile,
         "kernel_rooflines": {
             "wide": wide_rl,
             "post": {"kernel": "post (k_post_small)", "bound": "latency",

@@ -230,6 +230,11 @@ int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind);
 /* 1: store-path steps run as the streamed step (a persistent two-phase wide
    pass beside a persistent post cluster per run of steps), 0: launched steps */
 int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on);
+/* arm != 0: stamp the next streamed run (%globaltimer per stage);
+   arm == 0: its stage averages in µs (up to 8): step, phase 1, h -> phase 2
+   reduced, phase-2 tiles, phase-2 barrier + reduction, D-step (overlapped),
+   post chain after the dec half, number of steps averaged. */
+int ltfb_trainer_stream_profile(ltfb_trainer* t, int arm, double* out, int n);
 /* Number of kernels this trainer has launched so far (all of them ours). */
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches);
 

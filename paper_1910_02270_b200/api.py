@@ -731,6 +731,19 @@ class Trainer:
         check(lib.ltfb_trainer_stream_info(self._h, C.byref(k)))
         return bool(k.value)
 
+    def stream_profile(self, steps: int = 64) -> dict:
+        """Runs `steps` streamed steps with per-stage %globaltimer stamps and
+        returns the stage averages in µs; {} when not streamed."""
+        if not self.stream_mode():
+            return {}
+        check(lib.ltfb_trainer_stream_profile(self._h, 1, None, 0))
+        self.train_steps_raw(steps)
+        out = (C.c_double * 8)()
+        check(lib.ltfb_trainer_stream_profile(self._h, 0, out, 8))
+        keys = ("step_us", "wide_phase1_us", "h_to_phase2_reduced_us", "phase2_tiles_us",
+                "phase2_barrier_reduction_us", "d_step_overlapped_us", "post_chain_after_dec_us", "steps")
+        return {k: float(v) for k, v in zip(keys, out)}
+
     def eval_info(self, which: int = 0) -> int:
         """2 when slice `which` (0 tournament, 1 validation) is evaluated by
         the tcgen05 k_eval_tc, 1 for the SIMT k_eval_wide."""

@@ -479,6 +479,18 @@ int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on) {
   return guarded([&] { *on = T(const_cast<ltfb_trainer*>(t)).stream_mode() ? 1 : 0; });
 }
 
+int ltfb_trainer_stream_profile(ltfb_trainer* t, int arm, double* out, int n) {
+  return guarded([&] {
+    auto& tr = T(t);
+    if (arm) {
+      tr.stream_profile_next();
+      return;
+    }
+    if (!out || n < 0) throw ltfb::ContractError("stream_profile: bad output buffer");
+    for (int i = 0; i < n && i < 8; ++i) out[i] = tr.stream_profile()[i];
+  });
+}
+
 int ltfb_trainer_launch_count(const ltfb_trainer* t, uint64_t* launches) {
   return guarded([&] { *launches = T(const_cast<ltfb_trainer*>(t)).launch_count(); });
 }

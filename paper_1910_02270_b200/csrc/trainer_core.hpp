@@ -191,6 +191,11 @@ class DeviceTrainer {
   /// 1 when store-path steps run as the streamed step (persistent two-phase
   /// wide pass + persistent post cluster per run, launch_stream_run).
   bool stream_mode() const { return stream_on_; }
+  /// Stamps the next streamed run and keeps its stage averages (µs): step,
+  /// phase 1, h -> phase 2 reduced, phase-2 tiles, phase-2 barrier +
+  /// reduction, D-step, post chain after the dec half, steps averaged.
+  void stream_profile_next() { stream_prof_next_ = true; }
+  const double* stream_profile() const { return stream_prof_; }
   std::uint64_t launch_count() const { return launches_; }
 
  private:
@@ -216,6 +221,8 @@ class DeviceTrainer {
   void launch_stream_run(std::size_t steps);
   void check_stream_error();
   bool stream_on_ = false;
+  bool stream_prof_next_ = false;
+  double stream_prof_[8] = {};
   int S_stream_ = 0;
   int run_id_ = 0;
   cudaStream_t post_stream_ = nullptr;

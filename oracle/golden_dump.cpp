@@ -688,6 +688,34 @@ static void scenario_trainer(const fs::path& out, const fs::path& tmp) {
   }
 }
 
+// activations: trainer cases with the other hidden activations the
+// reference supports (nn/activation.hpp:43-77: relu, tanh, sigmoid), tiny and
+// desk dims, so the device's activation / derivative paths are pinned too.
+static void scenario_activations(const fs::path& out, const fs::path& tmp) {
+  Dump d(out / "activations.bin");
+  const std::pair<const char*, nn::Act> acts[3] = {
+      {"relu", nn::Act::kRelu}, {"tanh", nn::Act::kTanh}, {"sigmoid", nn::Act::kSigmoid}};
+  {
+    DataFixture fx(tmp / "act_tiny", tiny_dims(), 600, 100, 3, 17);
+    d.put("tiny_data", std::vector<std::uint64_t>{600, 100, 3, 17});
+    for (const auto& [name, act] : acts) {
+      auto arch = tiny_arch();
+      arch.hidden_act = nn::Activation{act, 0.0};
+      trainer_case(d, std::string("tiny_") + name + "_", fx, tiny_dims(), arch, 3, 1, 64, 7, 30, 20);
+    }
+  }
+  {
+    surrogate::ModalityDims dims;  // desk 16x16
+    DataFixture fx(tmp / "act_desk", dims, 400, 100, 1, 1);
+    d.put("desk_data", std::vector<std::uint64_t>{400, 100, 1, 1});
+    for (const auto& [name, act] : acts) {
+      surrogate::SurrogateArch arch;
+      arch.hidden_act = nn::Activation{act, 0.0};
+      trainer_case(d, std::string("desk_") + name + "_", fx, dims, arch, 3, 1, 32, 7, 30, 14);
+    }
+  }
+}
+
 // horizon: the trainer cases of scenario_trainer over 50 steps (SURVEY §7:
 // 1e-4 relative over 50 steps, tests/acceptance_test.cpp:210-244), at desk
 // and paper dims, several epochs each (the per-epoch reshuffle included).
@@ -1033,6 +1061,7 @@ int main(int argc, char** argv) {
     if (on("trainer")) scenario_trainer(out, tmp);
     if (on("tournament")) scenario_tournament(out, tmp);
     if (on("horizon")) scenario_horizon(out, tmp);
+    if (on("activations")) scenario_activations(out, tmp);
     if (on("tournament_paper")) scenario_tournament_paper(out, tmp);
     if (on("outputs")) scenario_outputs(out, tmp);
   } catch (const std::exception& e) {

@@ -23,7 +23,7 @@ REPO = os.path.dirname(HERE)
 DTYPES = {0: np.float32, 1: np.float64, 2: np.uint32, 3: np.uint64,
           4: np.int32, 5: np.int64, 6: np.uint8}
 SCENARIOS = ["rng", "plan", "synth", "nn", "surrogate", "trainer", "tournament", "outputs",
-             "horizon", "tournament_paper"]
+             "horizon", "tournament_paper", "activations"]
 RUN_DIRS = ["run_tiny_k2", "run_tiny_single"]  # written by the "outputs" scenario
 
 

@@ -10,6 +10,8 @@ Tolerances (stated per north_star):
     (SPEC.md:343, tests/acceptance_test.cpp:210-244);
   * evaluation metrics within REL_EVAL.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -908,3 +910,19 @@ def test_single_process_two_gpus_matches_reference(golden):
         got = json.loads(r.stdout.strip().splitlines()[-1])
         assert rel(got["steps_g_total"], g["tiny_k2_steps_g_total"]) < REL_LOSS
         assert got["tr_kept"] == [int(v) for v in g["tiny_k2_tr_kept"]]
+
+
+@pytest.mark.parametrize("dims_name", ["tiny", "desk"])
+@pytest.mark.parametrize("act", ["relu", "tanh", "sigmoid"])
+def test_trainer_hidden_activations_match_reference(golden, dims_name, act):
+    """The other hidden activations of nn/activation.hpp:43-77 (relu, tanh,
+    sigmoid; the default leaky relu is covered above) through every small
+    network and the enc layer-0 / dec-head activations of the wide pass:
+    losses, weights, evaluations and counters against the reference's runs
+    (tests/golden/activations.npz)."""
+    g = golden("activations")
+    base = L.SurrogateArch.tiny() if dims_name == "tiny" else L.SurrogateArch()
+    arch = dataclasses.replace(base, hidden_act=act, hidden_slope=0.0)
+    dims = TINY if dims_name == "tiny" else DESK
+    t, steps, _ = make_trainer(g, f"{dims_name}_{act}_", dims, arch, g[dims_name + "_data"])
+    check_against_golden(g, f"{dims_name}_{act}_", t, steps)

@@ -259,6 +259,31 @@ __global__ void k_stream_init(StepSync* sy, int run_id, unsigned* grid_bar) {
   __threadfence();
 }
 
+/// Concurrency probe of the streamed step: k_probe_spin waits (<= 50 ms) for
+/// k_probe_set, launched on another stream after it. Under tools that
+/// serialise kernels (ncu, compute-sanitizer) or when the GPU cannot run the
+/// two side by side, the spinner times out and the trainer uses the
+/// launched step.
+__global__ void k_probe_spin(const volatile int* flag, int* ok) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  int seen = 0;
+  for (;;) {
+    if (*flag) {
+      seen = 1;
+      break;
+    }
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 50000000ull) break;
+    __nanosleep(200);
+  }
+  *ok = seen;
+}
+__global__ void k_probe_set(volatile int* flag) {
+  *flag = 1;
+  __threadfence_system();
+}
+
 /// Timer gate (bench timed regions): holds the stream until the host has
 /// enqueued the work behind it (*flag != 0), so the device-timed region
 /// starts with a full queue; gives up after ~0.5 s so a missed release can
@@ -319,6 +344,21 @@ void launch_stream_init(StepSync* sy, int run_id, unsigned* grid_bar, cudaStream
 
 void launch_gather_rows(const float* src, const unsigned* slots, int n, float* dst, int out_pad, cudaStream_t s) {
   if (n > 0) k_gather_rows<<<n, 256, 0, s>>>(src, slots, n, dst, out_pad);
+}
+
+bool probe_concurrency(cudaStream_t a, cudaStream_t b) {
+  int* d = nullptr;
+  if (cudaMalloc(&d, 2 * sizeof(int)) != cudaSuccess) return false;
+  cudaMemsetAsync(d, 0, 2 * sizeof(int), a);
+  cudaStreamSynchronize(a);
+  k_probe_spin<<<1, 1, 0, a>>>(d, d + 1);
+  k_probe_set<<<1, 1, 0, b>>>(d);
+  int ok = 0;
+  const bool fine = cudaStreamSynchronize(a) == cudaSuccess && cudaStreamSynchronize(b) == cudaSuccess &&
+                    cudaMemcpy(&ok, d + 1, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+  cudaFree(d);
+  cudaGetLastError();
+  return fine && ok == 1;
 }
 
 void prepare_stream_kernels() {

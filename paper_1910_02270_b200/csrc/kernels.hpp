@@ -93,6 +93,9 @@ bool wide_ps_supported(const StepArgs& a, int S);
 /// happen while the persistent post cluster spins).
 void prepare_wide_ps();
 void prepare_stream_kernels();
+/// True if a kernel on stream b runs while one on stream a is resident
+/// (false under kernel-serialising tools: the streamed step then stays off).
+bool probe_concurrency(cudaStream_t a, cudaStream_t b);
 void launch_wide_ps(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r, int S, cudaStream_t s);
 /// 1 if the streamed post cluster (16 CTAs, split mode) can run this model here.
 int post_loop_supported(const StepArgs& a);

@@ -269,6 +269,10 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
       LTFB_CUDA(cudaStreamCreateWithFlags(&post_stream_, cudaStreamNonBlocking));
       for (auto& e : st_ev_) LTFB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ltfb_dev::prepare_stream_kernels();
+      // the two persistent kernels must run side by side: a tool that
+      // serialises kernels (ncu kernel replay, compute-sanitizer) or a
+      // shared GPU turns the streamed step off here, not in a 2 s hand-off timeout
+      if (!ltfb_dev::probe_concurrency(stream_, post_stream_)) stream_on_ = false;
     }
   }
   sync_stream();

@@ -596,8 +596,6 @@ __shared__ int g_nst;
 // 1 in the streamed step's persistent cluster (k_post_loop): parameters and
 // the owners' Adam moments stay resident in shared memory across steps
 __shared__ int g_persist;
-__device__ int g_dbg_flag;
-__device__ __forceinline__ bool getenv_dbg() { return g_dbg_flag != 0; }
 // LTFB_STREAM_PROF: this step's stamp row (cluster rank 0 only), else null
 __shared__ unsigned long long* g_pb;
 #define GSTAMP(slot) do { if (g_persist && g_pb && threadIdx.x == 0) g_pb[slot] = gtimer(); } while (0)
@@ -1287,10 +1285,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   prologue(a, Y, R, &s_bar);
-  if (R.rank == 0 && half == 0 && tid == 0 && getenv_dbg() && a.ctr->global_step == 0) {
-    const float* re = a.scratch + a.L.red_enc;
-    printf("DBG launch red_enc[0..3] %.9g %.9g %.9g %.9g red_enc[64*5+7] %.9g\n", re[0], re[1], re[2], re[3], re[64 * 5 + 7]);
-  }
   PH();
   if (half == 1) {
     cyc_half(a, Y, R, s_loss, s_ok, s_wl);
@@ -1574,9 +1568,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       PSTAMP(9);
       __syncthreads();
       stage_enc_rows(a, Y, R, r.red_enc[k & 1]);
-      if (a.phase_prof == 0 && k == 0 && crank == 0 && tid == 0 && getenv_dbg())
-        printf("DBG stream red_enc[0..3] %.9g %.9g %.9g %.9g red_enc[64*5+7] %.9g mae %.9g\n", r.red_enc[0][0], r.red_enc[0][1],
-               r.red_enc[0][2], r.red_enc[0][3], r.red_enc[0][64 * 5 + 7], *r.mae_total[0]);
       if (ET.L > 0) wnet_fwd(ET, Y.e1, 2, Y.stacked);  // real latents -> stacked[0, R)
       wnet_fwd(F, Y.xs, 2, latent);                    // fake latents -> stacked[R, 2R)
       wnet_fwd(C, Y.stacked, 4, -1);                   // disc on [real; fake]
@@ -1779,16 +1770,7 @@ int post_loop_supported(const StepArgs& a) {
   });
 }
 
-static void set_dbg_flag() {
-  static PerDevice dbg;
-  dbg.once([] {
-    const int v = std::getenv("LTFB_DBG") ? 1 : 0;
-    cudaMemcpyToSymbol(ps::g_dbg_flag, &v, sizeof v);
-  });
-}
-
 void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s) {
-  set_dbg_flag();
   static thread_local ps::Layout cache;
   static thread_local ModelArgs cache_m{};
   static thread_local bool have = false;
@@ -1815,7 +1797,6 @@ void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s) {
 
 void launch_post_tpl(int kind, const StepArgs& a, cudaStream_t s) {
   (void)kind;
-  set_dbg_flag();
   static PerDevice attr;
   attr.once([] { cudaFuncSetAttribute(ps::k_post_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap); });
   static thread_local ps::Layout cache;

@@ -347,6 +347,10 @@ void launch_gather_rows(const float* src, const unsigned* slots, int n, float* d
 }
 
 bool probe_concurrency(cudaStream_t a, cudaStream_t b) {
+  // load both kernels first: a lazily loaded module waits for the device to idle
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_probe_spin) != cudaSuccess || cudaFuncGetAttributes(&fa, k_probe_set) != cudaSuccess)
+    return false;
   int* d = nullptr;
   if (cudaMalloc(&d, 2 * sizeof(int)) != cudaSuccess) return false;
   cudaMemsetAsync(d, 0, 2 * sizeof(int), a);

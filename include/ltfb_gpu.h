@@ -227,6 +227,9 @@ int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* l
 int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
 /* which kernel evaluates slice `which` (0 tournament, 1 validation): 2 tcgen05 k_eval_tc, 1 SIMT */
 int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind);
+/* which column passes ltfb_trainer_ae_step runs for `rows` batch rows:
+   2 tcgen05 (k_ae_tc.cu), 1 SIMT (k_ae.cu) */
+int ltfb_trainer_ae_info(const ltfb_trainer* t, int32_t rows, int32_t* kind);
 /* 1: store-path steps run as the streamed step (a persistent two-phase wide
    pass beside a persistent post cluster per run of steps), 0: launched steps */
 int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on);

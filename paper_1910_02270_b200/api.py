@@ -751,6 +751,13 @@ class Trainer:
         check(lib.ltfb_trainer_eval_info(self._h, which, C.byref(k)))
         return k.value
 
+    def ae_info(self, rows: int = 128) -> int:
+        """2 when ae_step over `rows` batch rows runs the tcgen05 column
+        passes (k_ae_tc.cu), 1 for the SIMT ones (k_ae.cu)."""
+        k = C.c_int32(0)
+        check(lib.ltfb_trainer_ae_info(self._h, rows, C.byref(k)))
+        return k.value
+
     def launch_count(self) -> int:
         n = C.c_uint64(0)
         check(lib.ltfb_trainer_launch_count(self._h, C.byref(n)))
@@ -932,6 +939,13 @@ class AutoencoderPretrainer:
         loss = C.c_double(0.0)
         check(lib.ltfb_trainer_ae_step(self._h, idx, idx.size, C.byref(loss)))
         return loss.value
+
+    def kind(self, rows: int = 128) -> int:
+        """2: step() over `rows` rows runs the tcgen05 column passes
+        (k_ae_tc.cu); 1: the SIMT ones (k_ae.cu)."""
+        k = C.c_int32(0)
+        check(lib.ltfb_trainer_ae_info(self._h, rows, C.byref(k)))
+        return k.value
 
     def pull(self, model: CycleGan):
         for i, n in ((0, "enc"), (1, "dec")):

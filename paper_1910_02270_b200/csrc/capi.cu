@@ -475,6 +475,10 @@ int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind) {
   });
 }
 
+int ltfb_trainer_ae_info(const ltfb_trainer* t, int32_t rows, int32_t* kind) {
+  return guarded([&] { *kind = T(const_cast<ltfb_trainer*>(t)).ae_kind(rows); });
+}
+
 int ltfb_trainer_stream_info(const ltfb_trainer* t, int32_t* on) {
   return guarded([&] { *on = T(const_cast<ltfb_trainer*>(t)).stream_mode() ? 1 : 0; });
 }

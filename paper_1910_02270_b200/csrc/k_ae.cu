@@ -25,6 +25,8 @@
 // The column passes are SIMT fp32 (the AE runs once, before the experiment);
 // they are HBM-bound at ~3x the surrogate step's bytes.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "small_mlp.cuh"
@@ -277,7 +279,201 @@ __global__ void k_ae_ghreduce(const __grid_constant__ AeArgs a) {
   const int r = blockIdx.x, j = threadIdx.x, D = a.m.D, n = a.n;
   float acc = 0.0f;
   for (int s = 0; s < a.S; ++s) acc += a.Pg[((long long)s * n + r) * D + j];
-  a.gh[r * D + j] = acc;
+  a.gh[r * D + j] = acc * a.gscale;
+}
+
+// K2 / K5a for the tcgen05 passes (E1 == D == 64): the split-K sums spread
+// over n x 16 float4 outputs with 16 partial groups each (fixed group order).
+template <int kMode>  // 0: z0 / a0 from Pz, 1: gh from Pg
+__global__ void __launch_bounds__(256) k_ae_reduce_st(const __grid_constant__ AeArgs a) {
+  __shared__ float4 part[16][16];
+  const int o = threadIdx.x & 15, g = threadIdx.x >> 4;
+  const int nq = a.n * 16, q = blockIdx.x * 16 + o;
+  const float4* P = reinterpret_cast<const float4*>(kMode == 0 ? a.Pz : a.Pg);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (q < nq) {
+    float4 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int s = g + 16 * u;
+      v[u] = s < a.S ? __ldcg(P + (long long)s * nq + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      acc.x += v[u].x;
+      acc.y += v[u].y;
+      acc.z += v[u].z;
+      acc.w += v[u].w;
+    }
+  }
+  part[g][o] = acc;
+  __syncthreads();
+  if (g == 0 && q < nq) {
+    float4 t = part[0][o];
+    for (int k = 1; k < 16; ++k) {
+      t.x += part[k][o].x;
+      t.y += part[k][o].y;
+      t.z += part[k][o].z;
+      t.w += part[k][o].w;
+    }
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+    if (kMode == 0) {
+      const float* b0 = a.enc + a.m.enc_wide_b;
+      for (int c = 0; c < 4; ++c) {
+        const int e = 4 * (q & 15) + c, r = q >> 4;
+        const float zz = tv[c] + b0[e];
+        a.z0[r * 64 + e] = zz;
+        a.a0[r * 64 + e] = act_apply(a.m.enc_act0, a.m.enc_slope0, zz);
+      }
+    } else {
+      reinterpret_cast<float4*>(a.gh)[q] =
+          make_float4(tv[0] * a.gscale, tv[1] * a.gscale, tv[2] * a.gscale, tv[3] * a.gscale);
+    }
+  }
+}
+
+// Row-parallel small nets for the tcgen05 path (every width <= 64): four
+// batch rows per 256-thread CTA, each layer's W staged in shared memory once
+// per CTA. The forward and the backward's dz / dL/dinput chain are
+// row-local; the parameter gradients (sums over rows) follow in
+// k_ae_grads_rows. Every dot product keeps mlp_forward / mlp_backward's k
+// order, so the bits equal the one-CTA kernels'.
+constexpr int kRq = 4;  // rows per CTA
+
+__global__ void __launch_bounds__(256) k_ae_fwd_rows(const __grid_constant__ AeArgs a) {
+  __shared__ float W[64 * 64], Bv[64], xs[2][kRq][64];
+  const int q = threadIdx.x >> 6, j = threadIdx.x & 63;
+  const int r = blockIdx.x * kRq + q;
+  const bool live = r < a.n;
+  const ModelArgs& m = a.m;
+  int cur = 0;
+  xs[0][q][j] = live ? a.a0[r * 64 + j] : 0.0f;
+  auto run = [&](const NetDesc& nd, const float* blob, float* const* z, float* const* act) {
+    for (int l = 0; l < nd.L; ++l) {
+      const int in = nd.w[l], out = nd.w[l + 1];
+      __syncthreads();
+      const float* Wg = blob + nd.off_w[l];
+#pragma unroll 4
+      for (int i = threadIdx.x; i < in * out; i += 256) W[i] = __ldg(Wg + i);
+      if (threadIdx.x < out) Bv[threadIdx.x] = __ldg(blob + nd.off_b[l] + threadIdx.x);
+      __syncthreads();
+      if (live && j < out) {
+        const float* x = xs[cur][q];
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int k = 0; k < in; ++k) acc = fmaf(x[k], W[k * out + j], acc);
+        const float zz = acc + Bv[j];
+        const float av = act_apply(nd.act[l], nd.slope[l], zz);
+        z[l][r * out + j] = zz;
+        act[l][r * out + j] = av;
+        xs[cur ^ 1][q][j] = av;
+      }
+      cur ^= 1;
+    }
+  };
+  run(m.enc_tail, a.enc, a.etz, a.eta);
+  run(m.dec_head, a.dec, a.dhz, a.dha);
+}
+
+__global__ void __launch_bounds__(256) k_ae_bwd_rows(const __grid_constant__ AeArgs a) {
+  __shared__ float Wt[64 * 64], g[2][kRq][64], dz[kRq][64];
+  const int q = threadIdx.x >> 6, j = threadIdx.x & 63;
+  const int r = blockIdx.x * kRq + q;
+  const bool live = r < a.n;
+  const ModelArgs& m = a.m;
+  int cur = 0;
+  g[0][q][j] = live ? a.gh[r * 64 + j] : 0.0f;
+  auto run = [&](const NetDesc& nd, const float* blob, float* const* z, float* const* act, float* const* dzo) {
+    for (int l = nd.L - 1; l >= 0; --l) {
+      const int in = nd.w[l], out = nd.w[l + 1];
+      __syncthreads();
+      const float* Wg = blob + nd.off_w[l];
+#pragma unroll 4
+      for (int i = threadIdx.x; i < in * out; i += 256) {
+        const int k = i / out, jj = i - k * out;
+        Wt[jj * in + k] = __ldg(Wg + i);
+      }
+      if (live && j < out) {
+        const float d = g[cur][q][j] * act_deriv(nd.act[l], nd.slope[l], z[l][r * out + j], act[l][r * out + j]);
+        dz[q][j] = d;
+        dzo[l][r * out + j] = d;
+      }
+      __syncthreads();
+      if (live && j < in) {
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int jj = 0; jj < out; ++jj) acc = fmaf(dz[q][jj], Wt[jj * in + j], acc);
+        g[cur ^ 1][q][j] = acc;
+      }
+      cur ^= 1;
+    }
+  };
+  run(m.dec_head, a.dec, a.dhz, a.dha, a.dzh);  // -> dL/dlatent
+  run(m.enc_tail, a.enc, a.etz, a.eta, a.dze);  // -> dL/da0
+  __syncthreads();
+  if (live) {
+    const int i = r * 64 + j;
+    a.gz0[i] = g[cur][q][j] * act_deriv(m.enc_act0, m.enc_slope0, a.z0[i], a.a0[i]);
+  }
+}
+
+/// The over-rows sums of the small nets' parameter gradients, one thread
+/// per gradient element (rows ascending, as mlp.hpp:268-279 / col_sums):
+/// segment s covers dW (kind 0: sum_r below[r][k] dz[r][j], fmaf) or a
+/// bias (kind 1: sum_r dz[r][j]); the last block also writes the loss.
+struct GradSeg {
+  const float* below;
+  const float* dz;
+  float* dst;
+  int in, out, kind, net;
+  int start;  // first thread of the segment
+};
+struct GradSegs {
+  GradSeg s[4 * kMaxLayers + 1];
+  int n, total;
+};
+
+__global__ void __launch_bounds__(256) k_ae_grads_rows(const __grid_constant__ AeArgs a,
+                                                       const __grid_constant__ GradSegs gs) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = a.n;
+  if (tid < gs.total) {
+    int si = 0;
+    while (si + 1 < gs.n && tid >= gs.s[si + 1].start) ++si;
+    const GradSeg& sg = gs.s[si];
+    const int o = tid - sg.start;
+    float acc = 0.0f;
+    // 32 rows of operands in flight per round trip, summed in row order
+    const int k = sg.kind == 0 ? o / sg.out : 0, j = sg.kind == 0 ? o - k * sg.out : o;
+    for (int r0 = 0; r0 < rows; r0 += 32) {
+      float bv[32], dv[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int r = r0 + u;
+        dv[u] = r < rows ? __ldcg(sg.dz + r * sg.out + j) : 0.0f;
+        bv[u] = (sg.kind == 0 && r < rows) ? __ldcg(sg.below + r * sg.in + k) : 0.0f;
+      }
+      if (sg.kind == 0) {
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if (r0 + u < rows) acc = fmaf(bv[u], dv[u], acc);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+          if (r0 + u < rows) acc += dv[u];
+      }
+    }
+    sg.dst[o] = acc;
+    if (!isfinite(acc)) atomicOr(&a.flags[sg.net], 1);
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) {  // the loss: mae partials, fixed xor tree
+    const int lane = threadIdx.x;
+    double v = 0.0;
+    for (int s = lane; s < a.S; s += 32) v += a.mae_part[s];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) a.loss[0] = v / ((double)rows * (double)a.m.out);
+  }
 }
 
 // K5: small-network backward, gz0, db0, loss (one CTA)
@@ -387,13 +583,193 @@ __global__ void __launch_bounds__(256) k_ae_adam(float* __restrict__ p, float* _
   }
 }
 
+// K7 with the step's outcome decided on the device (train_ops.hpp:71-81,
+// adam.hpp:87-122): a non-finite loss or enc gradient applies nothing, a
+// non-finite dec gradient applies enc only; t + 1's bias corrections come
+// from the host-computed table (1 - std::pow(beta, t)).
+/// Adam(enc) and Adam(dec) in one launch, 4 elements per thread and pass
+/// (the blobs are 256-B aligned); the last block to finish commits t.
+struct AdamPair {
+  float* p[2];
+  float* m1[2];
+  float* m2[2];
+  const float* g[2];
+  long long count[2];
+  double lr[2];
+  double b1, b2, eps;
+  const double* adam_c;
+  Counters* ctr;
+  int* flags;  // [0] enc, [1] dec non-finite, [2] blocks done
+  const double* loss;
+};
+
+__global__ void __launch_bounds__(256) k_ae_adam_pair(const __grid_constant__ AdamPair a) {
+  const bool skip0 = !isfinite(*a.loss) || a.flags[0], skip1 = skip0 || a.flags[1];
+  const unsigned long long t0 = a.ctr->t[0] + 1, t1 = a.ctr->t[1] + 1;
+  const double c[2][2] = {{a.adam_c[2 * t0], a.adam_c[2 * t0 + 1]}, {a.adam_c[2 * t1], a.adam_c[2 * t1 + 1]}};
+  const long long q0 = skip0 ? 0 : a.count[0] / 4, q1 = skip1 ? 0 : a.count[1] / 4;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < q0 + q1; i += stride) {
+    const int net = i < q0 ? 0 : 1;
+    const long long j = net ? i - q0 : i;
+    float4* p4 = reinterpret_cast<float4*>(a.p[net]) + j;
+    float4* m4 = reinterpret_cast<float4*>(a.m1[net]) + j;
+    float4* v4 = reinterpret_cast<float4*>(a.m2[net]) + j;
+    const float4 g = __ldcs(reinterpret_cast<const float4*>(a.g[net]) + j);
+    float4 p = *p4, m = *m4, v = *v4;
+    const double lr = a.lr[net], c1 = c[net][0], c2 = c[net][1];
+    p.x = adam_elem(p.x, m.x, v.x, g.x, lr, a.b1, a.b2, a.eps, c1, c2);
+    p.y = adam_elem(p.y, m.y, v.y, g.y, lr, a.b1, a.b2, a.eps, c1, c2);
+    p.z = adam_elem(p.z, m.z, v.z, g.z, lr, a.b1, a.b2, a.eps, c1, c2);
+    p.w = adam_elem(p.w, m.w, v.w, g.w, lr, a.b1, a.b2, a.eps, c1, c2);
+    *p4 = p;
+    *m4 = m;
+    *v4 = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 8) {  // the < 4-element tails
+    const int net = threadIdx.x >> 2, k = threadIdx.x & 3;
+    const long long e = (a.count[net] / 4) * 4 + k;
+    if (!(net ? skip1 : skip0) && e < a.count[net]) {
+      float m = a.m1[net][e], v = a.m2[net][e];
+      a.p[net][e] = adam_elem(a.p[net][e], m, v, a.g[net][e], a.lr[net], a.b1, a.b2, a.eps, c[net][0], c[net][1]);
+      a.m1[net][e] = m;
+      a.m2[net][e] = v;
+    }
+  }
+  // every block has read t: the last one to finish advances it
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.flags[2], 1) == (int)gridDim.x - 1) {
+      if (!skip0) a.ctr->t[0] = t0;
+      if (!skip1) a.ctr->t[1] = t1;
+    }
+  }
+}
+
 }  // namespace ae
+
+// LTFB_AE_TIMING=1: CUDA events between the tcgen05 AE step's kernels, one
+// stderr line per step (µs): enc, reduce z, small fwd, dec, reduce gh,
+// small bwd, encw, adam enc, adam dec + t.
+namespace {
+struct AeTimer {
+  bool on = std::getenv("LTFB_AE_TIMING") != nullptr;
+  cudaEvent_t ev[12] = {};
+  int k = 0;
+  void mark(cudaStream_t s) {
+    if (!on || k >= 12) return;
+    if (!ev[k]) cudaEventCreate(&ev[k]);
+    cudaEventRecord(ev[k++], s);
+  }
+  void report() {
+    if (!on || k < 2) return;
+    cudaEventSynchronize(ev[k - 1]);
+    std::fprintf(stderr, "ae_timing_us");
+    for (int i = 1; i < k; ++i) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      std::fprintf(stderr, " %.2f", ms * 1e3f);
+    }
+    std::fprintf(stderr, "\n");
+    k = 0;
+  }
+};
+AeTimer& ae_timer() {
+  static thread_local AeTimer t;
+  return t;
+}
+}  // namespace
+
+void launch_ae_adam_dev(float* const* p, float* const* m1, float* const* m2, float* const* g, const long long* count,
+                        const double* lr, double b1, double b2, double eps, const double* adam_c, Counters* ctr,
+                        int* flags, const double* loss, int sms, cudaStream_t s) {
+  ae::AdamPair a;
+  for (int net = 0; net < 2; ++net) {
+    a.p[net] = p[net];
+    a.m1[net] = m1[net];
+    a.m2[net] = m2[net];
+    a.g[net] = g[net];
+    a.count[net] = count[net];
+    a.lr[net] = lr[net];
+  }
+  a.b1 = b1;
+  a.b2 = b2;
+  a.eps = eps;
+  a.adam_c = adam_c;
+  a.ctr = ctr;
+  a.flags = flags;
+  a.loss = loss;
+  const long long q = (count[0] + count[1]) / 4;
+  const long long blocks = std::min<long long>((q + 255) / 256, 8LL * sms);
+  AeTimer& tm = ae_timer();
+  ae::k_ae_adam_pair<<<(unsigned)std::max<long long>(1, blocks), 256, 0, s>>>(a);
+  tm.mark(s);
+  tm.report();
+}
 
 bool ae_supported(const ModelArgs& m, int rows) {
   return rows >= 1 && rows <= ae::kMaxRows && m.E1 <= ae::kMaxW && m.D <= ae::kMaxW;
 }
 
-void launch_ae_passes(const AeArgs& a, cudaStream_t s) {
+void launch_ae_passes(const AeArgs& a0, const void* ymap, cudaStream_t s) {
+  AeArgs a = a0;
+  a.prof = std::getenv("LTFB_AE_PROF") ? 1 : 0;
+  if (ymap) {
+    prepare_ae_tc();
+    a.gscale = (float)(1.0 / ((double)a.n * (double)a.m.out));
+    const int red_blocks = (a.n * 16 + 15) / 16;
+    AeTimer& tm = ae_timer();
+    tm.mark(s);
+    launch_ae_enc_tc(ymap, a, s);
+    tm.mark(s);
+    ae::k_ae_reduce_st<0><<<red_blocks, 256, 0, s>>>(a);
+    tm.mark(s);
+    const int row_blocks = (a.n + ae::kRq - 1) / ae::kRq;
+    ae::k_ae_fwd_rows<<<row_blocks, 256, 0, s>>>(a);
+    tm.mark(s);
+    launch_ae_dec_tc(ymap, a, s);
+    tm.mark(s);
+    ae::k_ae_reduce_st<1><<<red_blocks, 256, 0, s>>>(a);
+    tm.mark(s);
+    ae::k_ae_bwd_rows<<<row_blocks, 256, 0, s>>>(a);
+    tm.mark(s);
+    {
+      ae::GradSegs gs{};
+      int total = 0;
+      auto add = [&](const float* below, const float* dz, float* dst, int in, int out, int kind, int net) {
+        ae::GradSeg& g = gs.s[gs.n++];
+        g.below = below;
+        g.dz = dz;
+        g.dst = dst;
+        g.in = in;
+        g.out = out;
+        g.kind = kind;
+        g.net = net;
+        g.start = total;
+        total += kind == 0 ? in * out : out;
+      };
+      const ModelArgs& m = a.m;
+      for (int l = 0; l < m.dec_head.L; ++l) {
+        const NetDesc& nd = m.dec_head;
+        add(l == 0 ? a.latent : a.dha[l - 1], a.dzh[l], a.gdec + nd.off_w[l], nd.w[l], nd.w[l + 1], 0, 1);
+        add(nullptr, a.dzh[l], a.gdec + nd.off_b[l], nd.w[l], nd.w[l + 1], 1, 1);
+      }
+      for (int l = 0; l < m.enc_tail.L; ++l) {
+        const NetDesc& nd = m.enc_tail;
+        add(l == 0 ? a.a0 : a.eta[l - 1], a.dze[l], a.genc + nd.off_w[l], nd.w[l], nd.w[l + 1], 0, 0);
+        add(nullptr, a.dze[l], a.genc + nd.off_b[l], nd.w[l], nd.w[l + 1], 1, 0);
+      }
+      add(nullptr, a.gz0, a.genc + m.enc_wide_b, m.E1, m.E1, 1, 0);  // db0 = col_sums(gz0)
+      gs.total = total;
+      ae::k_ae_grads_rows<<<(total + 255) / 256, 256, 0, s>>>(a, gs);
+    }
+    tm.mark(s);
+    launch_ae_encw_tc(ymap, a, s);
+    tm.mark(s);
+    return;
+  }
+  a.gscale = 1.0f;  // the SIMT dec pass's partials carry G = (1/n) sign
   static PerDevice attr;
   const int sm_enc = (ae::kMaxRows * ae::kTN + ae::kTN * ae::kMaxW) * 4;
   const int sm_dec = (2 * ae::kMaxRows * ae::kMaxW + ae::kMaxRows * ae::kTN + 2 * ae::kMaxW * ae::kTN +

@@ -139,6 +139,8 @@ struct AeArgs {
   float* eta[kMaxLayers];
   float* dhz[kMaxLayers];      // dec-head tape
   float* dha[kMaxLayers];
+  float* dzh[kMaxLayers];      // dL/dz per layer of the dec head / enc tail [n x w_{l+1}]
+  float* dze[kMaxLayers];      // (row-parallel backward, then the over-rows sums)
   const float* latent;   // enc output [n x lat] (eta[L-1], or a0 if the tail is empty)
   const float* h;        // dec-head output [n x D] (dha[L-1], or latent)
   float* gh;             // dL/dh [n x D]
@@ -146,11 +148,26 @@ struct AeArgs {
   float* tA, *tB;        // [n x max width] backward scratch
   int* flags;            // [2] non-finite gradient: enc, dec
   double* loss;          // [1]
+  float gscale;          // dL/dh = gscale * sum_s Pg[s] (the tcgen05 dec pass leaves 1/n out)
+  int prof;              // LTFB_AE_PROF: CTA 0 of the tcgen05 dec pass prints per-tile stamps
 };
 bool ae_supported(const ModelArgs& m, int rows);
-void launch_ae_passes(const AeArgs& a, cudaStream_t s);
+/// K1-K6 of an AE step; ymap (a y tensor map over ysrc, encode_ae_y_map)
+/// selects the tcgen05 column passes (k_ae_tc.cu), nullptr the SIMT ones.
+void launch_ae_passes(const AeArgs& a, const void* ymap, cudaStream_t s);
+bool ae_tc_supported(const ModelArgs& m, int rows);
+void encode_ae_y_map(void* map, const float* ysrc, int rows, const ModelArgs& m);
+void prepare_ae_tc();
+void launch_ae_enc_tc(const void* map, const AeArgs& a, cudaStream_t s);
+void launch_ae_dec_tc(const void* map, const AeArgs& a, cudaStream_t s);
+void launch_ae_encw_tc(const void* map, const AeArgs& a, cudaStream_t s);
 void launch_ae_adam(float* p, float* m1, float* m2, const float* g, long long count, double lr, double b1, double b2,
                     double eps, double c1, double c2, int sms, cudaStream_t s);
+/// Adam(enc) then Adam(dec) and their t, applied or skipped on the device
+/// from the step's loss and non-finite flags (no host round trip).
+void launch_ae_adam_dev(float* const* p, float* const* m1, float* const* m2, float* const* g, const long long* count,
+                        const double* lr, double b1, double b2, double eps, const double* adam_c, Counters* ctr,
+                        int* flags, const double* loss, int sms, cudaStream_t s);
 
 /// Encodes a 2-D f32 tensor map (128-B swizzle) over [rows x cols].
 void encode_tile_map(void* map, const float* base, uint64_t cols, uint64_t rows, uint32_t box_cols,

@@ -290,6 +290,7 @@ DeviceTrainer::~DeviceTrainer() {
     if (e) cudaEventDestroy(e);
   if (sync_) cudaFree(sync_);
   if (resident_) cudaFreeHost(resident_);
+  if (ae_pin_) cudaFreeHost(ae_pin_);
   if (gate_) cudaFreeHost(gate_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
   for (int i = 0; i < 2; ++i) {
@@ -1267,6 +1268,12 @@ bool DeviceTrainer::train_steps_host(std::size_t n, const float* x, const float*
 }
 
 // ------------------------------------------------- autoencoder pre-training --
+int DeviceTrainer::ae_kind(int rows) const {
+  // LTFB_AE_SIMT=1: the SIMT column passes (A/B checks)
+  const bool simt = std::getenv("LTFB_AE_SIMT") != nullptr;
+  return !simt && ltfb_dev::ae_tc_supported(margs_, rows) ? 2 : 1;
+}
+
 void DeviceTrainer::ae_allocate() {
   if (ae_alloc_) return;
   const auto& m = margs_;
@@ -1285,11 +1292,14 @@ void DeviceTrainer::ae_allocate() {
   const std::size_t oz0 = take(R * m.E1), oa0 = take(R * m.E1), oga0 = take(R * m.E1), ogz0 = take(R * m.E1);
   std::size_t oet[ltfb_dev::kMaxLayers][2] = {}, odh[ltfb_dev::kMaxLayers][2] = {};
   int maxw = std::max(m.E1, m.D);
+  std::size_t odz[ltfb_dev::kMaxLayers][2] = {};
   for (int l = 0; l < m.enc_tail.L; ++l) {
     oet[l][0] = take((std::size_t)R * m.enc_tail.w[l + 1]);
     oet[l][1] = take((std::size_t)R * m.enc_tail.w[l + 1]);
+    odz[l][0] = take((std::size_t)R * m.enc_tail.w[l + 1]);
     maxw = std::max(maxw, m.enc_tail.max_w());
   }
+  for (int l = 0; l < m.dec_head.L; ++l) odz[l][1] = take((std::size_t)R * m.dec_head.w[l + 1]);
   for (int l = 0; l < m.dec_head.L; ++l) {
     odh[l][0] = take((std::size_t)R * m.dec_head.w[l + 1]);
     odh[l][1] = take((std::size_t)R * m.dec_head.w[l + 1]);
@@ -1299,7 +1309,7 @@ void DeviceTrainer::ae_allocate() {
   const std::size_t otA = take((std::size_t)R * maxw), otB = take((std::size_t)R * maxw);
   ae_scr_.alloc(need);
   ae_part_.alloc(a.S);
-  ae_flags_.alloc(2);
+  ae_flags_.alloc(4);  // enc / dec non-finite flags, Adam blocks done
   ae_loss_.alloc(1);
   ae_idx_.alloc(R);
   float* b = ae_scr_.p;
@@ -1312,7 +1322,9 @@ void DeviceTrainer::ae_allocate() {
   for (int l = 0; l < m.enc_tail.L; ++l) {
     a.etz[l] = b + oet[l][0];
     a.eta[l] = b + oet[l][1];
+    a.dze[l] = b + odz[l][0];
   }
+  for (int l = 0; l < m.dec_head.L; ++l) a.dzh[l] = b + odz[l][1];
   for (int l = 0; l < m.dec_head.L; ++l) {
     a.dhz[l] = b + odh[l][0];
     a.dha[l] = b + odh[l][1];
@@ -1385,10 +1397,47 @@ double DeviceTrainer::ae_step(const std::uint32_t* rows_idx, std::size_t n) {
   auto a = ae_args_;
   a.n = static_cast<int>(n);
   a.ysrc = ae_y_.p;
-  LTFB_CUDA(cudaMemcpyAsync(ae_idx_.p, rows_idx, n * 4, cudaMemcpyHostToDevice, stream_));
-  LTFB_CUDA(cudaMemsetAsync(ae_flags_.p, 0, 8, stream_));
-  ltfb_dev::launch_ae_passes(a, stream_);
+  if (!ae_pin_) LTFB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ae_pin_), sizeof(AePinned), cudaHostAllocDefault));
+  std::memcpy(ae_pin_->idx, rows_idx, n * 4);
+  LTFB_CUDA(cudaMemcpyAsync(ae_idx_.p, ae_pin_->idx, n * 4, cudaMemcpyHostToDevice, stream_));
+  LTFB_CUDA(cudaMemsetAsync(ae_flags_.p, 0, 16, stream_));
+  const void* map = nullptr;
+  if (ae_kind(static_cast<int>(n)) == 2) {
+    if (ae_map_base_ != ae_y_.p || ae_map_rows_ != ae_rows_) {
+      ltfb_dev::encode_ae_y_map(ae_map_, ae_y_.p, static_cast<int>(ae_rows_), margs_);
+      ae_map_base_ = ae_y_.p;
+      ae_map_rows_ = ae_rows_;
+    }
+    map = ae_map_;
+  }
+  ltfb_dev::launch_ae_passes(a, map, stream_);
   launches_ += 7;
+  if (map) {
+    // one host round trip per step: Adam(enc), Adam(dec) and t decided on
+    // the device; the host maps the flags onto the reference's exceptions
+    ensure_adam_table(t_host_max_ + 2);
+    const auto& h = spec_.arch.adam;
+    float* p[2] = {params_[0].p, params_[1].p};
+    float* m1[2] = {mom1_[0].p, mom1_[1].p};
+    float* m2[2] = {mom2_[0].p, mom2_[1].p};
+    float* g[2] = {grads_[0].p, grads_[1].p};
+    const long long cnt[2] = {static_cast<long long>(counts_[0]), static_cast<long long>(counts_[1])};
+    const double lr[2] = {spec_.lr[0] > 0 ? spec_.lr[0] : h.lr, spec_.lr[1] > 0 ? spec_.lr[1] : h.lr};
+    ltfb_dev::launch_ae_adam_dev(p, m1, m2, g, cnt, lr, h.beta1, h.beta2, h.eps, adam_c_.p, ctr_.p, ae_flags_.p,
+                                 ae_loss_.p, sm_count_, stream_);
+    launches_ += 1;
+    LTFB_CUDA(cudaMemcpyAsync(&ae_pin_->loss, ae_loss_.p, 8, cudaMemcpyDeviceToHost, stream_));
+    LTFB_CUDA(cudaMemcpyAsync(ae_pin_->flags, ae_flags_.p, 8, cudaMemcpyDeviceToHost, stream_));
+    sync_stream();
+    t_host_max_ += 1;
+    wide_dirty_ = true;
+    small_T_dirty_ = true;
+    h_ready_ = false;
+    const double loss = ae_pin_->loss;
+    if (!std::isfinite(loss)) throw ltfb::NumericError("autoencoder_step: non-finite loss");
+    if (ae_pin_->flags[0] || ae_pin_->flags[1]) throw ltfb::NumericError("adam_step: non-finite gradient component");
+    return loss;
+  }
   double loss = 0.0;
   int flags[2] = {0, 0};
   LTFB_CUDA(cudaMemcpyAsync(&loss, ae_loss_.p, 8, cudaMemcpyDeviceToHost, stream_));

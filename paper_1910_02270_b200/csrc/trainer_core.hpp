@@ -188,6 +188,8 @@ class DeviceTrainer {
   int wide_kernel_kind() const { return wide_kind_; }
   /// Wide part of evaluate() on slice `which`: 2 = k_eval_tc (tcgen05), 1 = SIMT k_eval_wide.
   int eval_kind(int which) const { return eval_tc_[which & 1].ready ? 2 : 1; }
+  /// Column passes of ae_step for `rows` batch rows: 2 tcgen05, 1 SIMT.
+  int ae_kind(int rows) const;
   /// 1 when store-path steps run as the streamed step (persistent two-phase
   /// wide pass + persistent post cluster per run, launch_stream_run).
   bool stream_mode() const { return stream_on_; }
@@ -353,6 +355,15 @@ class DeviceTrainer {
   DevBuf<int> ae_flags_;
   ltfb_dev::AeArgs ae_args_{};
   bool ae_alloc_ = false;
+  alignas(64) unsigned char ae_map_[128] = {};  // gather4 map over ae_y_ (tcgen05 passes)
+  struct AePinned {
+    std::uint32_t idx[128];
+    double loss;
+    int flags[2];
+  };
+  AePinned* ae_pin_ = nullptr;  // pinned staging of the batch index and the step's outcome
+  const float* ae_map_base_ = nullptr;
+  std::size_t ae_map_rows_ = 0;
   void ae_allocate();
 };
 

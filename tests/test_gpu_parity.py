@@ -426,6 +426,7 @@ def test_autoencoder_step_matches_oracle(oracle, dims, arch_name):
         assert np.array_equal(og.blob(i), model.blobs[name])
     draws = L.ae_batch_rows(5, n, 64, 3)
     p = L.AutoencoderPretrainer(model, ds.y, batch_size=64)
+    assert p.kind(64) == (1 if arch_name == "tiny" else 2)  # tcgen05 passes at 64-wide layers
     for s in range(3):
         y = np.ascontiguousarray(ds.y[draws[s]])
         ref_loss, eg, dg = og.ae_backward(y)
@@ -448,6 +449,63 @@ def test_autoencoder_step_matches_oracle(oracle, dims, arch_name):
         assert model.opt[name].t == og.t(i) == 3
         dm = np.abs(model.opt[name].m.astype(np.float64) - og.moment(i, 0))
         assert np.quantile(dm, 0.999) < 1e-4 * np.max(np.abs(og.moment(i, 0))) + 1e-12
+
+
+@pytest.mark.parametrize("dims,rows", [(PAPER, 128), (PAPER, 37), (DESK, 128), (DESK, 1)])
+def test_autoencoder_tc_gradients_match_oracle(oracle, dims, rows):
+    """The tcgen05 AE column passes (k_ae_tc.cu: P_z = y We0, O = h Wd with
+    the loss and S, dWd = h^T G, dbd = col_sums G, dL/dh = G Wd^T, dWe0 =
+    y^T gz0) against the oracle's autoencoder_backward (train_ops.hpp:52-67)
+    through the first Adam moment, m = (1 - beta1) g after one step from zero
+    moments -- full and ragged batches (rows past n, the last partial tile)."""
+    arch, oarch = L.SurrogateArch(), oracle.Arch()
+    n = 300
+    ds = L.synthetic_dataset(dims, n, sampling_seed=5, spec_seed=1)
+    model = L.make_cyclegan(dims, arch, 33)
+    og = oracle.Gan(list(dims.as_tuple()), oarch, 33)
+    draws = L.ae_batch_rows(9, n, rows, 1)
+    p = L.AutoencoderPretrainer(model, ds.y, batch_size=rows)
+    assert p.kind(rows) == 2
+    y = np.ascontiguousarray(ds.y[draws[0]])
+    ref_loss, eg, dg = og.ae_backward(y)
+    got = p.step(draws[0])
+    assert abs(got - ref_loss) <= REL_LOSS * abs(ref_loss)
+    p.pull(model)
+    for name, g in (("enc", eg), ("dec", dg)):
+        gd = model.opt[name].m.astype(np.float64) / (1.0 - arch.beta1)
+        gr = g.astype(np.float64)
+        scale = np.max(np.abs(gr))
+        err = np.abs(gd - gr)
+        # 3xTF32 keeps fp32-level sums; a few MAE signs of |o - y| ~ 0 may flip
+        # with the summation order, so the bound is on the bulk plus a cap
+        assert np.quantile(err, 0.999) <= 1e-5 * scale, name
+        assert np.quantile(err / (np.abs(gr) + 1e-3 * scale), 0.99) <= 1e-3, name
+        assert err.max() <= 0.05 * scale, name
+
+
+@pytest.mark.parametrize("dims,arch_name", [(TINY, "tiny"), (PAPER, "default")])
+def test_autoencoder_nonfinite_step_changes_nothing(dims, arch_name):
+    """train_ops.hpp:74-78: a non-finite loss throws NumericError before
+    either Adam step, so enc / dec, their moments and t stay as they were
+    (the tcgen05 path decides this on the device); the next clean step
+    applies normally."""
+    arch = L.SurrogateArch.tiny() if arch_name == "tiny" else L.SurrogateArch()
+    ds = L.synthetic_dataset(dims, 40, sampling_seed=4, spec_seed=1)
+    y = ds.y.copy()
+    y[3, 5] = np.nan
+    model = L.make_cyclegan(dims, arch, 5)
+    before = {k: model.blobs[k].copy() for k in ("enc", "dec")}
+    p = L.AutoencoderPretrainer(model, y, batch_size=8)
+    with pytest.raises(L.NumericError):
+        p.step(np.array([0, 1, 3, 7], np.uint32))
+    p.pull(model)
+    for k in ("enc", "dec"):
+        assert np.array_equal(model.blobs[k], before[k]) and model.opt[k].t == 0
+        assert not np.any(model.opt[k].m)
+    p.step(np.array([0, 1, 2, 7], np.uint32))
+    p.pull(model)
+    assert model.opt["enc"].t == 1 and model.opt["dec"].t == 1
+    assert not np.array_equal(model.blobs["enc"], before["enc"])
 
 
 def test_autoencoder_frozen_and_bad_rows():

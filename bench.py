@@ -37,6 +37,45 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 KERNEL_VERSION = "r02a"
 
 
+def ae_bench(L, dims, ds, ids, B, arch, source=1024, warmup=5, steps=40):
+    """Times AE pre-training steps at the bench's dims over a resident AE
+    source of `source` rows (random batches of B rows per step). Roofline:
+    HBM bytes of one step -- the batch's y rows, the two wide weight matrices
+    read by the column passes, Adam's p/m/v read+write and the gradient read
+    over both networks -- over the measured step time; flops: the five wide
+    products (y We0, h Wd, h^T G, G Wd^T, y^T gz0) in fp32-equivalent terms."""
+    import numpy as np
+    src_ids = ids[: min(source, ids.size)]
+    _, y = ds.rows(src_ids)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    model = L.make_cyclegan(dims, arch, 7)
+    p = L.AutoencoderPretrainer(model, y, batch_size=B)
+    kind = p.kind(B)
+    draws = L.ae_batch_rows(11, y.shape[0], B, warmup + steps)
+    for s_ in range(warmup):
+        p.step(draws[s_])
+    t0 = time.perf_counter()
+    for s_ in range(warmup, warmup + steps):
+        loss = p.step(draws[s_])
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    del p
+    out = dims.output_dim()
+    E1, D = arch.enc_hidden[0], arch.dec_hidden[-1]
+    n_params = sum(int(b.size) for k, b in model.blobs.items() if k in ("enc", "dec"))
+    hbm_bytes = B * out * 4 + (out * E1 + D * out) * 4 + n_params * 4 * 7
+    flops = 5 * 2.0 * B * out * 64
+    peaks, _ = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    ach = hbm_bytes / (ms / 1e3) / 1e9
+    return {"ms_per_step": ms, "steps": steps, "batch": B, "source_rows": int(y.shape[0]),
+            "kind": {2: "tcgen05 3xTF32 column passes + fused Adam", 1: "SIMT"}.get(kind, str(kind)),
+            "last_loss": float(loss), "params": n_params, "gflop_per_step": flops / 1e9,
+            "tflops": flops / (ms / 1e3) / 1e12,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                         "algorithmic_bytes_per_step": hbm_bytes},
+            "timing": "wall clock per host-synced step (perf_counter), as AutoencoderPretrainer.step runs"}
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -50,6 +89,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--rounds", type=int, default=10, help="tournament rounds timed on their own")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-ae", action="store_true", help="skip the autoencoder pre-training timing")
     p.add_argument("--wide-kernel", type=int, default=0)
     p.add_argument("--host-data", action="store_true",
                    help="generate the partition on the host and upload it (default: k_synth on the device)")
@@ -401,6 +441,12 @@ def main():
             dist.destroy_process_group()
         return 0
 
+    # ---- autoencoder pre-training step (train_ops.hpp:71-81, runner.hpp:249-279)
+    # on rank 0: the tcgen05 column passes + fused Adam over a resident AE
+    # source, each step through the public AutoencoderPretrainer.step() (the
+    # loss is read back per step, as the reference's loop checks it)
+    ae = ae_bench(L, dims, ds, my_train, B, arch) if not args.no_ae else None
+
     # ---- roofline ----------------------------------------------------------
     # headline: the whole step (both step kernels) against HBM -- the
     # compulsory bytes of a step over the
@@ -495,6 +541,7 @@ def main():
             "row": {"kernel": "row (k_row_h; graph heads only)", "ms_per_launch": per_launch("gather"),
                     "launches": kt["gather"][1]},
         },
+        "ae_pretrain": ae,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "samples/s",
                 "h2d_bytes_per_step": B * (dims.input_dim + out) * 4,

@@ -371,6 +371,7 @@ void prepare_stream_kernels() {
   cudaFuncGetAttributes(&fa, k_gate);
   cudaFuncGetAttributes(&fa, k_begin_epoch);
   prepare_wide_ps();
+  prepare_wide2();
 }
 
 }  // namespace ltfb_dev

@@ -684,6 +684,9 @@ void encode_wide_maps(WideTcParamsHost& p, const StepArgs& a, const float* yb, i
   encode_2d(&tp.tm_wd, p.wd, op, wt::kW, 32, 64);
   encode_2d(&tp.tm_wdt, p.wdt, wt::kW, op, 32, 32);
   std::memcpy(p.maps, &tp, sizeof tp);
+  CUtensorMap m64;
+  encode_2d(&m64, p.wdt, wt::kW, op, 32, 64);  // k_wide2: [64 columns x 32 j] per K-block
+  std::memcpy(p.wdt64, &m64, sizeof m64);
 }
 
 }  // namespace ltfb_dev

@@ -66,6 +66,7 @@ void launch_wide_tc(const StepArgs& a, cudaStream_t s);
 /// frozen wide-layer weights, the padded bias, and the TMA descriptors.
 struct WideTcParamsHost {
   alignas(64) unsigned char maps[4 * 128];  // CUtensorMap x4 (y, WeT, Wd, WdT)
+  alignas(64) unsigned char wdt64[128];     // WdT with 64-row boxes (k_wide2's 64-column tiles)
   alignas(64) unsigned char y_alt[2][128];  // y maps of the host-streamed (e2e) minibatch buffers
   int y_sel = -1;                           // -1: maps[0] (gathered minibatch), else y_alt[y_sel]
   bool precise = true;
@@ -97,6 +98,13 @@ void prepare_stream_kernels();
 /// (false under kernel-serialising tools: the streamed step then stays off).
 bool probe_concurrency(cudaStream_t a, cudaStream_t b);
 void launch_wide_ps(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r, int S, cudaStream_t s);
+/// The 64-column-tile wide pass (k_wide2.cu): the streamed step's persistent
+/// kernel and the launched step's cooperative one (same arithmetic).
+int wide2_tiles(const StepArgs& a);
+bool wide2_supported(const StepArgs& a, int S);
+void prepare_wide2();
+void launch_wide2_stream(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r, int S, cudaStream_t s);
+void launch_wide2_step(const WideTcParamsHost& p, const StepArgs& a, cudaStream_t s);
 /// 1 if the streamed post cluster (16 CTAs, split mode) can run this model here.
 int post_loop_supported(const StepArgs& a);
 void launch_post_loop(const StepArgs& a, const StreamArgs& r, cudaStream_t s);

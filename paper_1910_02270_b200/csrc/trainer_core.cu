@@ -149,7 +149,9 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   LTFB_CUDA(cudaMemsetAsync(ctr_.p, 0, sizeof(ltfb_dev::Counters), stream_));
   // [0..1]: the launched wide pass's barrier; from 64 on: the streamed wide
   // pass's per-CTA release flags (one 128-B line each) and its arrival count
-  grid_bar_.alloc(96 + 32 * 160);
+  // (k_wide2's launched mode keeps its own region from 5248 on: epoch base,
+  // arrival count, per-CTA flags)
+  grid_bar_.alloc(5248 + 64 + 32 * 160);
   LTFB_CUDA(cudaMemsetAsync(grid_bar_.p, 0, grid_bar_.bytes(), stream_));
   rec_.alloc(4096);
   for (int i = 0; i < 2; ++i) {
@@ -245,16 +247,23 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   // run, the persistent wide pass the others (and, for one split-K order on
   // every path, so do the launched wide passes)
   {
-    const int Ss = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, static_cast<int>((ma.out + 31) / 32));
     const bool tool = std::getenv("CUDA_INJECTION64_PATH") != nullptr;  // ncu / compute-sanitizer serialise kernels
+    // LTFB_WIDE_V2=1: the 64-column-tile wide pass (k_wide2, in development)
+    // for both step modes, on the SMs the post cluster leaves free; default:
+    // k_wide_ps streamed, k_wide_tc launched
+    const int Ss2 = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, ltfb_dev::wide2_tiles(a));
+    wide2_ = wide_kind_ >= 2 && std::getenv("LTFB_WIDE_V2") && ltfb_dev::wide2_supported(a, Ss2);
+    const int Ss = wide2_ ? Ss2
+                          : std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, static_cast<int>((ma.out + 31) / 32));
     // LTFB_NO_STREAM=1: launched steps; =2: launched steps with the streamed
     // step's wide CTA count (the two paths then sum in the same order)
     const char* ns = std::getenv("LTFB_NO_STREAM");
     const bool able = wide_kind_ >= 2 && post_tpl_ && a.h_in_gather && spec_.n_shards == 1 && !a.phase_prof &&
-                      static_cast<std::size_t>(Ss) <= (ma.out + 31) / 32 && ltfb_dev::wide_ps_supported(a, Ss) &&
+                      (wide2_ || (static_cast<std::size_t>(Ss) <= (ma.out + 31) / 32 &&
+                                  ltfb_dev::wide_ps_supported(a, Ss))) &&
                       ltfb_dev::post_loop_supported(a);
     stream_on_ = able && !ns && !tool;
-    if (able && (stream_on_ || tool || (ns && ns[0] == '2'))) {
+    if (wide2_ || (able && (stream_on_ || tool || (ns && ns[0] == '2')))) {
       S_ = static_cast<std::size_t>(Ss);
       a.S = Ss;
     }
@@ -676,7 +685,8 @@ void DeviceTrainer::launch_step_kernels(bool gather, bool row_h) {
     ++n;
   }
   kernel_mark(2, true);
-  if (wide_kind_ >= 2) ltfb_dev::launch_wide_tc_params(wtp_, args_, stream_);
+  if (wide_kind_ >= 2 && wide2_) ltfb_dev::launch_wide2_step(wtp_, args_, stream_);
+  else if (wide_kind_ >= 2) ltfb_dev::launch_wide_tc_params(wtp_, args_, stream_);
   else ltfb_dev::launch_wide_generic(args_, stream_);
   kernel_mark(2, false);
   ++n;
@@ -900,7 +910,7 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
   const bool prof = std::getenv("LTFB_STREAM_PROF") != nullptr || (stream_prof_next_ && steps >= 8);
   if (prof) stream_prof_next_ = false;
   if (prof) {
-    if (prof_.n < 512 * steps) prof_.alloc(512 * steps);
+    if (prof_.n < 512 * steps + 256) prof_.alloc(512 * steps + 256);
     LTFB_CUDA(cudaMemsetAsync(prof_.p, 0, prof_.bytes(), stream_));
     r.prof = prof_.p;
   }
@@ -919,7 +929,8 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
     }
     std::this_thread::yield();
   }
-  ltfb_dev::launch_wide_ps(wtp_, args_, r, S_stream_, stream_);
+  if (wide2_) ltfb_dev::launch_wide2_stream(wtp_, args_, r, S_stream_, stream_);
+  else ltfb_dev::launch_wide_ps(wtp_, args_, r, S_stream_, stream_);
   LTFB_CUDA(cudaEventRecord(st_ev_[1], post_stream_));
   LTFB_CUDA(cudaStreamWaitEvent(stream_, st_ev_[1], 0));
   launches_ += 3;
@@ -992,11 +1003,20 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
                          b.front(), b[b.size() / 2], b.back(),
                          ((double)h[512 * k + 299] - (double)h[512 * k + 128]) * 1e-3);
         }
-        std::fprintf(stderr, "\n  tiles of step 3 (us from w.p2): prod / staged / mma2 / epi / mma3\n");
-        for (int j = 0; j < 12; ++j) {
+        if (std::getenv("LTFB_STREAM_PROF") && std::getenv("LTFB_STREAM_PROF")[0] == '2') {
+          std::vector<unsigned long long> sm(S_stream_);
+          LTFB_CUDA(cudaMemcpy(sm.data(), prof_.p + 512 * steps, S_stream_ * 8, cudaMemcpyDeviceToHost));
+          std::fprintf(stderr, "\n  per CTA (cta:sm p2part barrier, us vs CTA 0 partials):");
+          for (int c = 0; c < S_stream_; ++c)
+            std::fprintf(stderr, " %d:%llu %.1f %.1f", c, sm[c],
+                         ((double)h[512 * k + 128 + c] - (double)h[512 * k + 128]) * 1e-3,
+                         ((double)h[512 * k + 300 + c] - (double)h[512 * k + 128]) * 1e-3);
+        }
+        std::fprintf(stderr, "\n  tiles of step 3 (us from w.p2): prod / staged / mma2 / epi / mma3 / O-ready\n");
+        for (int j = 0; j < 8; ++j) {
           std::fprintf(stderr, "   t%2d", j);
-          for (int e = 0; e < 5; ++e) {
-            const unsigned long long v = h[512 * k + 32 + 5 * j + e];
+          for (int e = 0; e < 6; ++e) {
+            const unsigned long long v = h[512 * k + 32 + 6 * j + e];
             std::fprintf(stderr, " %7.2f", v ? ((double)v - (double)h[512 * k + 2]) * 1e-3 : -1.0);
           }
           std::fprintf(stderr, "\n");

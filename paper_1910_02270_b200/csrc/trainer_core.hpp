@@ -271,6 +271,7 @@ class DeviceTrainer {
   // tcgen05 wide pass: K-major fp32 copies of the frozen wide-layer weights + bias
   DevBuf<float> wide_w_;  // WeT | Wd | WdT | bias (one range for the L2 persistence window)
   ltfb_dev::WideTcParamsHost wtp_{};
+  bool wide2_ = false;  // k_wide2 (64-column tiles) is the wide pass of both step modes
   bool wide_dirty_ = false;
   bool small_T_dirty_ = true;  // StepArgs::pT images need a rebuild
   DevBuf<float> pT_[5];

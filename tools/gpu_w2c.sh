@@ -1,0 +1,9 @@
+# k_wide2: reduction loads in flight; bench with stream profile (x2), launched kernel timing
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x -k "stream or paper" > gpurun_out/w2c_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/w2c_pytest.log
+tail -n 3 gpurun_out/w2c_pytest.log
+for i in 1 2; do
+LTFB_STREAM_PROF=1 timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/w2c_bench20_$i.json 2> gpurun_out/w2c_bench20_$i.err; echo "bench20 rc=$?"; python -c "
+import json; d=json.loads(open('gpurun_out/w2c_bench20_$i.json').read().strip().splitlines()[-1]); print(d['ms_per_step'], d['kernels_ms_per_launch'], d['stream_profile_us'])"
+grep -A 20 "stream prof" gpurun_out/w2c_bench20_$i.err | tail -12
+done

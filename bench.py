@@ -34,7 +34,7 @@ sys.path.insert(0, REPO)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 # profiles/traffic.json keys carry this tag: a DRAM-traffic figure measured on
 # another version of the step kernels is not reported (bump on kernel changes)
-KERNEL_VERSION = "r02a"
+KERNEL_VERSION = "r02g"
 
 
 def ae_bench(L, dims, ds, ids, B, arch, source=1024, warmup=5, steps=40):
@@ -481,7 +481,8 @@ def main():
     wide_rl = None
     if wide_ms:
         a = wide_bytes / (wide_ms / 1e3) / 1e9
-        wide_rl = {"kernel": "wide (k_wide_tc)" if kind == 2 else "wide", "bound": "hbm", "achieved": a,
+        wname = {64: "wide (k_wide2, launched: phase 1 + phase 2)", 32: "wide (k_wide_tc)"}.get(tr.wide_tile(), "wide")
+        wide_rl = {"kernel": wname, "bound": "hbm", "achieved": a,
                    "peak": hbm, "unit": "GB/s", "frac": a / hbm, "traffic": traffic.get("wide"),
                    "traffic_warm_l2": traffic.get("wide_warm"),
                    "algorithmic_bytes_per_launch": wide_bytes, "ms_per_launch": wide_ms,
@@ -514,6 +515,7 @@ def main():
                          f"{my_train.size * out_pad * 4 / 1e9:.2f} GB HBM store; the frozen wide-layer "
                          "weights (model state, not inputs) sit in an L2 persistence window",
                    "wide_kernel": {1: "generic SIMT fp32", 2: "tcgen05 3xTF32"}.get(kind, str(kind)),
+                   "wide_tile_cols": tr.wide_tile(),
                    "wide_ctas": ctas,
                    "step_mode": ("streamed: per run of steps inside an epoch, one persistent two-phase wide pass "
                                  f"({ctas} CTAs) beside one persistent 16-CTA post cluster, hand-offs through "
@@ -523,7 +525,7 @@ def main():
         # per-kernel times of the launched step (one kernel at a time, CUDA events):
         # the kernel-level roofline below; the timed region runs the streamed step
         "kernels_ms_per_launch": {n: (v[0] / v[1] if v[1] else None) for n, v in kt.items()},
-        "roofline": {"kernel": "step (k_wide_tc + k_post_small, one CUDA-graph step)", "bound": "hbm",
+        "roofline": {"kernel": "step (the streamed step: wide pass + post cluster)", "bound": "hbm",
                      "achieved": step_ach, "peak": hbm, "unit": "GB/s", "frac": step_ach / hbm,
                      "traffic": traffic.get("step"), "traffic_warm_l2": traffic.get("step_warm"),
                      "peak_source": peak_src,

@@ -225,6 +225,9 @@ int ltfb_trainer_kernel_timing(ltfb_trainer* t, int on);
 int ltfb_trainer_kernel_time(ltfb_trainer* t, int which, double* ms, uint64_t* launches);
 /* Which wide-pass kernel is active (1 generic SIMT, 2 tcgen05) and its grid. */
 int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas);
+/* Column-tile width of the tcgen05 wide pass: 64 (k_wide2, both step modes)
+ * or 32 (k_wide_ps / k_wide_tc); 0 for the generic SIMT pass. */
+int ltfb_trainer_wide_tile(const ltfb_trainer* t, int32_t* cols);
 /* which kernel evaluates slice `which` (0 tournament, 1 validation): 2 tcgen05 k_eval_tc, 1 SIMT */
 int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind);
 /* which column passes ltfb_trainer_ae_step runs for `rows` batch rows:

@@ -109,7 +109,7 @@ EXPORTS = (
     "ltfb_trainer_get_generator", "ltfb_trainer_set_incoming", "ltfb_trainer_copy_incoming",
     "ltfb_trainer_tournament_decide", "ltfb_trainer_adopt", "ltfb_trainer_train_steps_host",
     "ltfb_trainer_timer_start", "ltfb_trainer_timer_stop", "ltfb_trainer_kernel_timing",
-    "ltfb_trainer_kernel_time", "ltfb_trainer_wide_info", "ltfb_trainer_eval_info", "ltfb_trainer_ae_info", "ltfb_trainer_stream_info", "ltfb_trainer_stream_profile", "ltfb_trainer_launch_count",
+    "ltfb_trainer_kernel_time", "ltfb_trainer_wide_info", "ltfb_trainer_wide_tile", "ltfb_trainer_eval_info", "ltfb_trainer_ae_info", "ltfb_trainer_stream_info", "ltfb_trainer_stream_profile", "ltfb_trainer_launch_count",
     "ltfb_nccl_available", "ltfb_synth_generate_ids", "ltfb_selftest_tcgen05",
     "ltfb_nccl_unique_id", "ltfb_comm_create", "ltfb_comm_destroy", "ltfb_trainer_exchange",
     "ltfb_trainer_broadcast", "ltfb_mix_seed", "ltfb_fnv1a64", "ltfb_pair_trainers",
@@ -181,6 +181,7 @@ _sig("ltfb_trainer_timer_stop", C.c_int, P, C.POINTER(C.c_double))
 _sig("ltfb_trainer_kernel_timing", C.c_int, P, C.c_int)
 _sig("ltfb_trainer_kernel_time", C.c_int, P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_uint64))
 _sig("ltfb_trainer_wide_info", C.c_int, P, C.POINTER(C.c_int32), C.POINTER(C.c_int32))
+_sig("ltfb_trainer_wide_tile", C.c_int, P, C.POINTER(C.c_int32))
 _sig("ltfb_trainer_eval_info", C.c_int, P, C.c_int, C.POINTER(C.c_int32))
 _sig("ltfb_trainer_ae_info", C.c_int, P, C.c_int32, C.POINTER(C.c_int32))
 _sig("ltfb_trainer_stream_info", C.c_int, P, C.POINTER(C.c_int32))

@@ -724,6 +724,13 @@ class Trainer:
         check(lib.ltfb_trainer_wide_info(self._h, C.byref(k), C.byref(c)))
         return k.value, c.value
 
+    def wide_tile(self) -> int:
+        """Column-tile width of the tcgen05 wide pass (64: k_wide2; 32: the
+        round-2a kernels; 0: generic SIMT)."""
+        c = C.c_int32(0)
+        check(lib.ltfb_trainer_wide_tile(self._h, C.byref(c)))
+        return c.value
+
     def stream_mode(self) -> bool:
         """True when store-path steps run as the streamed step (persistent
         two-phase wide pass beside a persistent post cluster per run)."""

@@ -468,6 +468,13 @@ int ltfb_trainer_wide_info(const ltfb_trainer* t, int32_t* kind, int32_t* ctas) 
   });
 }
 
+int ltfb_trainer_wide_tile(const ltfb_trainer* t, int32_t* cols) {
+  return guarded([&] {
+    auto& tr = T(const_cast<ltfb_trainer*>(t));
+    *cols = tr.wide_kernel_kind() >= 2 ? (tr.wide2() ? 64 : 32) : 0;
+  });
+}
+
 int ltfb_trainer_eval_info(const ltfb_trainer* t, int which, int32_t* kind) {
   return guarded([&] {
     if (which < 0 || which > 1) throw ltfb::ContractError("eval_info: which must be 0 or 1");

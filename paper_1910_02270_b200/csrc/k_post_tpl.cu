@@ -1413,10 +1413,21 @@ __device__ __noinline__ void stage_enc_rows(const StepArgs& a, const Layout& Y, 
   const ModelArgs& m = a.m;
   const int E1 = m.E1;
   const int e1 = Y.net[kET].L > 0 ? Y.e1 : Y.stacked;
-  for (int i = threadIdx.x; i < kR * E1; i += kThreads) {
-    const int r = i / E1, c = i - r * E1;
-    const float v = r < R.nr ? __ldcg(red_enc + (long long)(R.r0 + r) * E1 + c) : 0.0f;
-    s[e1 + i] = act_f(m.enc_act0, m.enc_slope0, v + s[Y.be + c]);
+  // every load issued before any is used (one L2 round trip)
+  constexpr int kPer = kR * kMaxW / kThreads;
+  float v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = (int)threadIdx.x + u * kThreads, r = i / E1;
+    v[u] = i < kR * E1 && r < R.nr ? __ldcg(red_enc + (long long)R.r0 * E1 + i) : 0.0f;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = (int)threadIdx.x + u * kThreads;
+    if (i < kR * E1) {
+      const int c = i - (i / E1) * E1;
+      s[e1 + i] = act_f(m.enc_act0, m.enc_slope0, v[u] + s[Y.be + c]);
+    }
   }
   __syncthreads();
 }
@@ -1428,10 +1439,17 @@ __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R
   const int D = m.D;
   const float gscale = (float)(1.0 / ((double)R.rows * (double)m.out));
   const int gh = Y.net[kDH].L > 0 ? Y.gh : Y.gl_dec;
-  for (int i = threadIdx.x; i < kR * D; i += kThreads) {
-    const int r = i / D;
-    const float v = r < R.nr ? __ldcg(red_dec + (long long)R.r0 * D + i) : 0.0f;
-    s[gh + i] = v * gscale;
+  constexpr int kPer = kR * kMaxW / kThreads;
+  float v[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = (int)threadIdx.x + u * kThreads;
+    v[u] = i < kR * D && i / D < R.nr ? __ldcg(red_dec + (long long)R.r0 * D + i) : 0.0f;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = (int)threadIdx.x + u * kThreads;
+    if (i < kR * D) s[gh + i] = v[u] * gscale;
   }
   __syncthreads();
 }
@@ -1568,21 +1586,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       PSTAMP(9);
       __syncthreads();
       stage_enc_rows(a, Y, R, r.red_enc[k & 1]);
+      GSTAMP(100);
       if (ET.L > 0) wnet_fwd(ET, Y.e1, 2, Y.stacked);  // real latents -> stacked[0, R)
+      GSTAMP(101);
       wnet_fwd(F, Y.xs, 2, latent);                    // fake latents -> stacked[R, 2R)
+      GSTAMP(102);
       wnet_fwd(C, Y.stacked, 4, -1);                   // disc on [real; fake]
+      GSTAMP(103);
       {
         const double lv = bce_warp(C.a[C.L - 1], C.dz[C.L - 1], 4, kR, nr, 2.0 * (double)rows, 1.0f);
         if (lane == 0) s_wl[warp] = lv;
         __syncwarp();
       }
+      GSTAMP(104);
       wnet_bwd(C, 4, -1, -1, -1);
+      GSTAMP(105);
       __syncthreads();
       pg_net(C, Y.stacked, 2 * kR, Y.pg[0]);
+      GSTAMP(106);
       if (tid == 0) s_loss[0] = sum_warps(s_wl);
       __syncthreads();
       cluster_arrive();  // S1
       cluster_wait();
+      GSTAMP(107);
       PSTAMP(10);
       double d_loss = 0.0;
       const bool d_ok = d_update(a, Y, R, s_loss, s_ok, &d_loss);

@@ -63,10 +63,17 @@ constexpr int kThreads = 320;
 constexpr int kG = 10;      // reduction groups (10 x 32 threads)
 constexpr int kMaxQ = 32;   // float4 outputs per reduction chunk
 constexpr int kMaxS = 150;  // <= kG * 15 partials
-constexpr uint32_t kPartOff = kStages * kStage;
-constexpr uint32_t kSmem = kPartOff + kG * kMaxQ * 16 + 1024;
+// phase 2's y tiles land here (one [128 x 32] block per slot, TMA gather4)
+// and are copied into the stage's TMEM y slot; the reduction scratch and the
+// MAE row sums reuse the slots (idle at phase ends)
+constexpr uint32_t kLandOff = kStages * kStage;
+constexpr uint32_t kPartOff = kLandOff;
+constexpr uint32_t kRedOff = kLandOff + kYBlk;
+constexpr uint32_t kSmem = kLandOff + 2 * kYBlk + 1024;
+static_assert(kG * kMaxQ * 16 <= kYBlk, "reduction scratch in a landing slot");
 // TMEM columns: split-K accumulator (P_enc in phase 1, P_dec in phase 2),
-// two O / S buffers, h hi / lo, a y-lo slot per stage
+// two O / S buffers, h hi / lo, a y slot per stage (phase 1: y lo; phase 2:
+// the raw y tile the epilogue compares against)
 constexpr uint32_t kPacc = 0, kO0 = 64, kHhi = 192, kHlo = 256, kYlo = 320;
 static_assert(kYlo + 64 * kStages <= 512, "TMEM columns");
 static_assert(kSmem <= 227 * 1024, "shared memory");
@@ -158,9 +165,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kStages], split_done[kStages], empty[kStages];
-  __shared__ uint64_t ofull[2], oempty[2], sready[2], h_ready, done;
+  __shared__ uint64_t ofull[2], oempty[2], sready[2], h_ready, done, lfull;
   __shared__ uint32_t tmem_base;
-  __shared__ double red[128];
   __shared__ int s_go;
   __shared__ unsigned s_base;
 
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     }
     tc::mbar_init(&h_ready, 128);
     tc::mbar_init(&done, 1);
+    tc::mbar_init(&lfull, 1);
     tc::fence_barrier_init();
     // launched mode: this launch's barrier epochs continue from the last one
     s_base = kStream ? 0u : *reinterpret_cast<volatile unsigned*>(a.grid_bar + kLaunchBar);
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   int rw[4] = {0, 0, 0, 0};
   uint32_t hr_par = 0, done_par = 0;
   int o_run = 0;      // running phase-2 tile count (O / S double buffer)
+  uint32_t l_par = 0; // w6-9: landing-slot phase
 
   // w0: issue the operands of running tiles [prod_next, upto)
   auto produce = [&](int upto) {
@@ -288,8 +296,16 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     const int i0 = q * my_tiles, i1 = i0 + my_tiles;
     if (warp == 0) {
       // ------------------------------------------------ TMA producer --
+      // phase 2: the gather rows of the next step's phase 1 now (perm loads
+      // off the phase end), so the prefetch below is only TMA issues
+      if (ph2 && k + 1 < nsteps && prod_k != k + 1) {
+        const int rows1 = rows_of(k + 1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rw[u] = row_index(k + 1, 4 * lane + u, rows1);
+        prod_k = k + 1;
+      }
       produce(i1);
-      produce(min(i1 + kStages, nphase * my_tiles));  // the next phase's first tiles
+      produce(min(i1 + kStages, nphase * my_tiles));  // the next phase's first tiles, under the barrier
     } else if (warp == 1) {
       // ---------------------------------------------------- MMA issuer --
       if (lane == 0 && my_tiles > 0) {
@@ -342,7 +358,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
             tc::tc_fence_after();
             const uint32_t Sa = T + kO0 + 64u * (uint32_t)ob;
             const uint32_t wdh = tc::smem_u32(WdH(s)), wdl = tc::smem_u32(WdL(s));
-            for (int kb = 0; kb < ((r.w2_flags & 8) ? 0 : nkb); ++kb)
+            for (int kb = 0; kb < nkb; ++kb)
               for (int kk = 0; kk < 4; ++kk) {
                 const uint32_t aoff = 32 * kb + 8 * kk;
                 tc::mma_tf32_ts(T + kPacc, Sa + aoff, tc::sdesc_sw128(wdh + kb * kWBlk + 32 * kk, 16, 1024), id64,
@@ -412,36 +428,32 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         tc::tc_fence_before();
         tc::mbar_arrive(&h_ready);
         for (int e = 0; e < 4; ++e) mae_e[e] = 0.0;
-        const float* yrow = ysrc + (long long)row_index(k, rr, rows) * out_pad;
         for (int i = i0; i < i1; ++i) {
           const int j = i - i0;
           const int oi = o_run + j, ob = oi & 1;
           const int c0 = col0(j);
-          // this row's y of the tile, from L2 (phase 1 gathered it from HBM):
-          // 32-B loads, one full sector per lane and instruction
-          float yv[64];
-          const bool ny = (r.w2_flags & 2) != 0;  // experiment: no y loads
-#pragma unroll
-          for (int u = 0; u < 8; ++u) ld_nc_v8(yrow + c0 + 8 * u, !ny && c0 + 8 * u < out_pad, yv + 8 * u);
+          // O of the tile (MMA2 ran after the split warps put the tile's y
+          // into the stage's TMEM y slot)
           mbar_wait2(&ofull[ob], (uint32_t)(oi >> 1) & 1u);
           tc::tc_fence_after();
           if (rr == 0) TSTAMP(k, j, 5);
           const uint32_t Ob = T + lane_addr + kO0 + 64u * (uint32_t)ob;
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            float o[32];
+            float o[32], yv[32];
             tc::tmem_ld32(Ob + 32 * half, o);
+            tc::tmem_ld32(T + lane_addr + kYlo + 64 * (i % kStages) + 32 * half, yv);
             const int cb = c0 + 32 * half;
             const int nvalid = rr < rows ? max(0, min(32, out - cb)) : 0;
             float tsum[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               float bq[8];
-              ld_nc_v8(bias_pad + cb + 8 * u, (r.w2_flags & 4) == 0 && cb + 8 * u < out_pad, bq);
+              ld_nc_v8(bias_pad + cb + 8 * u, cb + 8 * u < out_pad, bq);
 #pragma unroll
               for (int e8 = 0; e8 < 8; ++e8) {
                 const int c = 8 * u + e8;
-                const float yq = yv[32 * half + c];
+                const float yq = yv[c];
                 const float of = o[c] + bq[e8];  // mlp.hpp:209-213
                 const bool ok = c < nvalid;
                 tsum[c & 3] += ok ? fabsf(of - yq) : 0.0f;  // loss.hpp:25-41
@@ -480,13 +492,15 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
       if (prof && blockIdx.x == 0 && rr == 0) prof[512 * k + (ph2 ? 20 : 19)] = gtimer();
       if (prof && ph2 && rr == 0) prof[512 * k + 128 + blockIdx.x] = gtimer();
       if (ph2) {
-        red[rr] = (mae_e[0] + mae_e[1]) + (mae_e[2] + mae_e[3]);
+        // the CTA's MAE partial: a fixed xor tree per warp, then the four
+        // warp sums in quadrant order (deterministic)
+        double* red = reinterpret_cast<double*>(sm + kRedOff);
+        double t = (mae_e[0] + mae_e[1]) + (mae_e[2] + mae_e[3]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane == 0) red[quad] = t;
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (rr == 0) {
-          double t = 0.0;
-          for (int u = 0; u < 128; ++u) t += red[u];
-          a.mae_part[blockIdx.x] = t;
-        }
+        if (rr == 0) a.mae_part[blockIdx.x] = ((red[0] + red[1]) + red[2]) + red[3];
       }
     } else {
       // ----------------------------------------------------- tf32 split --
@@ -508,10 +522,49 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
                                 v.w - tc::tf32_hi(v.w));
         }
       };
+      // phase 2: the y tile of running tile i is gathered into the landing
+      // slots during tile i - 1 and copied into the stage's TMEM y slot
+      int grw[4] = {0, 0, 0, 0};
+      const int gslot = (warp - 6) * 8 + lane;  // lanes 0-7 of each split warp: rows 4 g .. 4 g + 3
+      auto issue_y = [&](int j) {  // all 128 split threads call this
+        const int c0 = col0(j), nkb = nkb_of(c0);
+        if (tg == 0) tc::mbar_expect_tx(&lfull, (uint32_t)nkb * kYBlk);
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // expect_tx first; every thread done reading the slots
+        if (lane < 8)
+          for (int kb = 0; kb < nkb; ++kb)
+            tc::tma_gather4(sm + kLandOff + kb * kYBlk + 512 * gslot, &tp.tm_y, &lfull, c0 + 32 * kb, grw[0], grw[1],
+                            grw[2], grw[3]);
+      };
+      if (ph2 && my_tiles > 0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) grw[u] = row_index(k, 4 * gslot + u, rows);
+        issue_y(0);
+      }
       for (int i = i0; i < i1; ++i) {
         const int s = i % kStages;
         const int c0 = col0(i - i0), nkb = nkb_of(c0);
         mbar_wait2(&full[s], (uint32_t)(i / kStages) & 1u);
+        if (ph2) {
+          // the tile's raw y rows -> TMEM y slot s (this thread's row), then
+          // the landing slots take the next tile's rows
+          mbar_wait2(&lfull, l_par);
+          l_par ^= 1u;
+          for (int kb = 0; kb < nkb; ++kb) {
+            const unsigned char* yrow = sm + kLandOff + kb * kYBlk + rr * 128;
+            float v[32];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t off = (uint32_t)(((u ^ (rr & 7)) & 7) << 4);
+              const float4 y4 = *reinterpret_cast<const float4*>(yrow + off);
+              v[4 * u + 0] = y4.x;
+              v[4 * u + 1] = y4.y;
+              v[4 * u + 2] = y4.z;
+              v[4 * u + 3] = y4.w;
+            }
+            tc::tmem_st32(T + lane_addr + kYlo + 64 * s + 32 * kb, v);
+          }
+          if (i + 1 < i1) issue_y(i + 1 - i0);
+        }
         if (kPrecise) {
           if (!ph2) {
             // y: this thread's row of each K-block, hi in place, lo -> TMEM
@@ -609,8 +662,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
             t.z += w.z;
             t.w += w.w;
           }
-          reinterpret_cast<float4*>(dst)[c0 + o] = t;
-          if (kStream) __threadfence();
+          reinterpret_cast<float4*>(dst)[c0 + o] = t;  // published by thread 0's fence + release below
         }
         __syncthreads();  // part is refilled by the next chunk
       }
@@ -621,10 +673,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         double t = (((v[0] + v[1]) + v[2]) + v[3]) + v[4];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-        if (lane == 0) {
-          *mae_dst = t;
-          if (kStream) __threadfence();
-        }
+        if (lane == 0) *mae_dst = t;
       }
       if (kStream) {
         __syncthreads();
@@ -702,8 +751,7 @@ void prepare_wide2() {
 static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r0, int S, bool stream,
                          cudaStream_t s) {
   prepare_wide2();
-  StreamArgs r = r0;
-  if (const char* f = std::getenv("LTFB_W2_FLAGS")) r.w2_flags = std::atoi(f);
+  const StreamArgs& r = r0;
   Wide2Params tp;
   std::memcpy(&tp.tm_y, p.y_sel >= 0 ? p.y_alt[p.y_sel] : p.maps, sizeof(CUtensorMap));
   std::memcpy(&tp.tm_wet, p.maps + 128, sizeof(CUtensorMap));

@@ -120,7 +120,6 @@ struct StreamArgs {
   float* red_dec[2];
   double* mae_total[2];
   unsigned long long* prof;  // LTFB_STREAM_PROF: [n x 16] %globaltimer stamps per step, else null
-  int w2_flags;              // k_wide2 experiments (LTFB_W2_FLAGS): bit 0 = no in-place tf32 hi writes
 };
 
 /// Candidate evaluation (train_ops.hpp:191-205) over a resident slice.

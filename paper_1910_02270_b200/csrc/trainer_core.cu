@@ -248,11 +248,12 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
   // every path, so do the launched wide passes)
   {
     const bool tool = std::getenv("CUDA_INJECTION64_PATH") != nullptr;  // ncu / compute-sanitizer serialise kernels
-    // LTFB_WIDE_V2=1: the 64-column-tile wide pass (k_wide2, in development)
-    // for both step modes, on the SMs the post cluster leaves free; default:
-    // k_wide_ps streamed, k_wide_tc launched
+    // the 64-column-tile wide pass (k_wide2) for both step modes, on the SMs
+    // the post cluster leaves free; LTFB_WIDE_V1=1 (A/B runs) or a shape
+    // k_wide2 does not cover: the 32-column kernels (k_wide_ps streamed,
+    // k_wide_tc launched)
     const int Ss2 = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, ltfb_dev::wide2_tiles(a));
-    wide2_ = wide_kind_ >= 2 && std::getenv("LTFB_WIDE_V2") && ltfb_dev::wide2_supported(a, Ss2);
+    wide2_ = wide_kind_ >= 2 && !std::getenv("LTFB_WIDE_V1") && ltfb_dev::wide2_supported(a, Ss2);
     const int Ss = wide2_ ? Ss2
                           : std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, static_cast<int>((ma.out + 31) / 32));
     // LTFB_NO_STREAM=1: launched steps; =2: launched steps with the streamed
@@ -974,6 +975,15 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
         std::fprintf(stderr, "\n  pull: start %.2f end %.2f (us from c.decwait)",
                      ((double)h[512 * k + 90] - (double)h[512 * k + 7]) * 1e-3,
                      ((double)h[512 * k + 91] - (double)h[512 * k + 7]) * 1e-3);
+        std::fprintf(stderr, "\n  D-step (us from d.encwait): enc rows %.2f enc tail %.2f fwd %.2f disc fwd %.2f bce %.2f disc bwd %.2f pg %.2f S1 %.2f",
+                     ((double)h[512 * k + 100] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 101] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 102] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 103] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 104] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 105] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 106] - (double)h[512 * k + 9]) * 1e-3,
+                     ((double)h[512 * k + 107] - (double)h[512 * k + 9]) * 1e-3);
         std::fprintf(stderr, "\n  post (us from c.decwait): S3b-arrive %.2f S3b %.2f fwd-bwd-start %.2f pg-start %.2f S4-arr %.2f S4 %.2f adam %.2f S5 %.2f gupd %.2f S6 %.2f nexth %.2f",
                      ((double)h[512 * k + 94] - (double)h[512 * k + 7]) * 1e-3,
                      ((double)h[512 * k + 95] - (double)h[512 * k + 7]) * 1e-3,

@@ -186,6 +186,7 @@ class DeviceTrainer {
   std::size_t wide_ctas() const { return S_; }
   const ltfb_dev::StepArgs& step_args() const { return args_; }
   int wide_kernel_kind() const { return wide_kind_; }
+  bool wide2() const { return wide2_; }
   /// Wide part of evaluate() on slice `which`: 2 = k_eval_tc (tcgen05), 1 = SIMT k_eval_wide.
   int eval_kind(int which) const { return eval_tc_[which & 1].ready ? 2 : 1; }
   /// Column passes of ae_step for `rows` batch rows: 2 tcgen05, 1 SIMT.

@@ -60,9 +60,9 @@ constexpr uint32_t kWBlk = 8192;    // [64 x 32] f32, SW128 (one weight K-block)
 constexpr uint32_t kStage = 65536;  // phase 1: Y (2 blk) | WeT hi | WeT lo; phase 2: WdT hi | WdT lo | Wd hi | Wd lo
 constexpr int kStages = 3;
 constexpr int kThreads = 320;
-constexpr int kG = 10;      // reduction groups (10 x 32 threads)
+constexpr int kG = 9;       // reduction groups: warps 1-9 (the producer warp prefetches meanwhile)
 constexpr int kMaxQ = 32;   // float4 outputs per reduction chunk
-constexpr int kMaxS = 150;  // <= kG * 15 partials
+constexpr int kMaxS = 153;  // <= kG * 17 partials
 // phase 2's y tiles land here (one [128 x 32] block per slot, TMA gather4)
 // and are copied into the stage's TMEM y slot; the reduction scratch and the
 // MAE row sums reuse the slots (idle at phase ends)
@@ -92,10 +92,15 @@ struct Wide2Params {
 /// (flags[32 c]), so waiters poll disjoint lines. `epoch` only grows. A
 /// missing CTA raises sy->error after the timeout (streamed mode) instead of
 /// hanging the GPU; launched mode traps.
+/// kFull: every thread of the CTA takes part (leader thread 0); else warps
+/// 1-9 only (named barrier 3, leader thread 32): the phase-end barrier, which
+/// the producer warp skips so its next-phase prefetch never delays it.
+template <bool kFull>
 __device__ __forceinline__ void grid_sync2(unsigned* cnt, unsigned* flags, unsigned n, StepSync* sy,
                                            unsigned epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (kFull) __syncthreads();
+  else asm volatile("bar.sync 3, 288;" ::: "memory");
+  if (threadIdx.x == (kFull ? 0u : 32u)) {
     unsigned old;
     asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
     if (old + 1 == n * epoch) {
@@ -119,7 +124,8 @@ __device__ __forceinline__ void grid_sync2(unsigned* cnt, unsigned* flags, unsig
       }
     }
   }
-  __syncthreads();
+  if (kFull) __syncthreads();
+  else asm volatile("bar.sync 3, 288;" ::: "memory");
 }
 
 /// 8 floats (one 32-B sector) through the non-coherent path, 32-B aligned;
@@ -175,7 +181,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   const int out = a.m.out, out_pad = a.m.out_pad;
   const int ntiles = (out + kTileN - 1) / kTileN;
   const int S = (int)gridDim.x;
-  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / S + 1 : 0;
+  const int lcta = ((int)blockIdx.x + r.tile_rot) % S;  // column-tile owner index (A/B: LTFB_W2_ROT)
+  const int my_tiles = ntiles > lcta ? (ntiles - 1 - lcta) / S + 1 : 0;
   const int nsteps = kStream ? r.n : 1;
   const int sie0 = kStream ? r.sie0 : (int)a.ctr->step_in_epoch;
   const unsigned epoch = kStream ? r.epoch : a.ctr->epoch;
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   unsigned* bar_cnt = kStream ? a.grid_bar + 64 : a.grid_bar + kLaunchBar + 32;
   unsigned* bar_flags = bar_cnt + 32;
   const int nphase = 2 * nsteps;
-  auto col0 = [&](int j) { return ((int)blockIdx.x + j * S) * kTileN; };
+  auto col0 = [&](int j) { return (lcta + j * S) * kTileN; };
   auto rows_of = [&](int k) { return min(a.B, a.n_part - (sie0 + k) * a.B); };
   auto nkb_of = [&](int c0) { return c0 + 32 < out ? 2 : 1; };  // y / We / Wd K-blocks inside the matrix
   auto row_index = [&](int k, int rr, int rows) {
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
 
   double mae_e[4] = {0.0, 0.0, 0.0, 0.0};
   int q_done = 0;
-  const bool stamp = prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool stamp = prof != nullptr && blockIdx.x == 0 && threadIdx.x == 32;
 #define WSTAMP(slot) do { if (stamp) prof[512 * k + (slot)] = gtimer(); } while (0)
   for (int q = 0; q < nphase; ++q) {
     q_done = q + 1;
@@ -602,88 +609,103 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
       hr_par ^= 1u;
     }
 
-    // ---- phase end: grid-wide fixed-order reduction of this phase's partials ----
+    // ---- phase end: grid-wide fixed-order reduction of the partials, by
+    // warps 1-9 (the producer is already issuing the next phase's first
+    // tiles). Streamed: after each phase (the post cluster needs P_enc
+    // before phase 2 ends). Launched: once, after phase 2, for both (the
+    // post kernel runs after this kernel) -- the phase-1 partials are in
+    // global memory before the epilogue loads h, which phase 2's first MMA
+    // waits for, so the shared TMEM accumulator is never overwritten early.
+    if (kStream || ph2) {
+    ++bar_epoch;
+    if (warp != 0) {
     if (ph2) WSTAMP(3);
     if (ph2 && prof && blockIdx.x == 0 && threadIdx.x == 64) prof[512 * k + 299] = gtimer();
     if (ph2 && prof) {
-      __syncthreads();
-      if (threadIdx.x == 0) prof[512 * k + 300 + blockIdx.x] = gtimer();
+      asm volatile("bar.sync 3, 288;" ::: "memory");
+      if (threadIdx.x == 32) prof[512 * k + 300 + blockIdx.x] = gtimer();
     }
-    grid_sync2(bar_cnt, bar_flags, (unsigned)S, sy, ++bar_epoch);
+    grid_sync2<false>(bar_cnt, bar_flags, (unsigned)S, sy, bar_epoch);
     WSTAMP(ph2 ? 22 : 21);
     {
-      float* dst = kStream ? (ph2 ? r.red_dec[k & 1] : r.red_enc[k & 1])
-                           : a.scratch + (ph2 ? a.L.red_dec : a.L.red_enc);
-      double* mae_dst = kStream ? r.mae_total[k & 1] : a.mae_total;
       const int q_all = rows * (kW / 4);  // float4 outputs of P_enc or P_dec
       const int lo = (int)((long long)q_all * blockIdx.x / S);
       const int hi = (int)((long long)q_all * (blockIdx.x + 1) / S);
       float4* part = reinterpret_cast<float4*>(sm + kPartOff);  // [kG][kMaxQ]
-      const int g = threadIdx.x / 32, o = threadIdx.x % 32;
+      const int g = warp - 1, o = lane;
       const long long pstride4 = (long long)a.B * kW / 4;
-      const float4* P4 = reinterpret_cast<const float4*>(ph2 ? a.P_dec : a.P_enc);
-      // this CTA's slice [lo, hi) in chunks of kMaxQ outputs: thread (g, o)
-      // loads partials g, g + kG, ... of output o (every load issued before
-      // the adds: one L2 round trip), sums them in ascending order, then the
-      // kG group sums are added in group order -- a fixed order, so the
-      // result is deterministic and the same in both step modes
-      for (int c0 = lo; c0 < hi; c0 += kMaxQ) {
-        const int nq = min(kMaxQ, hi - c0);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (o < nq) {
-          // every load issued before the adds (absent partials re-read
-          // partial g and are not added)
-          float4 v[kMaxS / kG];
+      // this CTA's slice [lo, hi) of one reduced matrix, in chunks of kMaxQ
+      // outputs: thread (g, o) loads partials g, g + kG, ... of output o
+      // (every load issued before the adds: one L2 round trip), sums them
+      // in ascending order, then the kG group sums are added in group order
+      // -- a fixed order, so the result is deterministic and the same in
+      // both step modes
+      auto reduce = [&](const float* Pm, float* dst) {
+        const float4* P4 = reinterpret_cast<const float4*>(Pm);
+        for (int c0 = lo; c0 < hi; c0 += kMaxQ) {
+          const int nq = min(kMaxQ, hi - c0);
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (o < nq) {
+            // absent partials re-read partial g and are not added
+            float4 v[kMaxS / kG];
 #pragma unroll
-          for (int u = 0; u < kMaxS / kG; ++u) {
-            const int sidx = g + u * kG < S ? g + u * kG : g;
-            const float4* src = P4 + sidx * pstride4 + c0 + o;
-            asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
-                         : "l"(src));
-          }
-#pragma unroll
-          for (int u = 0; u < kMaxS / kG; ++u)
-            if (g + u * kG < S) {
-              acc.x += v[u].x;
-              acc.y += v[u].y;
-              acc.z += v[u].z;
-              acc.w += v[u].w;
+            for (int u = 0; u < kMaxS / kG; ++u) {
+              const int sidx = g + u * kG < S ? g + u * kG : g;
+              const float4* src = P4 + sidx * pstride4 + c0 + o;
+              asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                           : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                           : "l"(src));
             }
-        }
-        part[g * kMaxQ + o] = acc;
-        __syncthreads();
-        if (g == 0 && o < nq) {
-          float4 t = part[o];
-          for (int u = 1; u < kG; ++u) {
-            const float4 w = part[u * kMaxQ + o];
-            t.x += w.x;
-            t.y += w.y;
-            t.z += w.z;
-            t.w += w.w;
+#pragma unroll
+            for (int u = 0; u < kMaxS / kG; ++u)
+              if (g + u * kG < S) {
+                acc.x += v[u].x;
+                acc.y += v[u].y;
+                acc.z += v[u].z;
+                acc.w += v[u].w;
+              }
           }
-          reinterpret_cast<float4*>(dst)[c0 + o] = t;  // published by thread 0's fence + release below
+          part[g * kMaxQ + o] = acc;
+          asm volatile("bar.sync 3, 288;" ::: "memory");
+          if (g == 0 && o < nq) {
+            float4 t = part[o];
+            for (int u = 1; u < kG; ++u) {
+              const float4 w = part[u * kMaxQ + o];
+              t.x += w.x;
+              t.y += w.y;
+              t.z += w.z;
+              t.w += w.w;
+            }
+            reinterpret_cast<float4*>(dst)[c0 + o] = t;  // published by the fence + release below (streamed)
+          }
+          asm volatile("bar.sync 3, 288;" ::: "memory");  // part is refilled by the next chunk
         }
-        __syncthreads();  // part is refilled by the next chunk
+      };
+      if (kStream) reduce(ph2 ? a.P_dec : a.P_enc, ph2 ? r.red_dec[k & 1] : r.red_enc[k & 1]);
+      else {
+        reduce(a.P_enc, a.scratch + a.L.red_enc);
+        reduce(a.P_dec, a.scratch + a.L.red_dec);
       }
-      if (ph2 && blockIdx.x == 0 && warp == 0) {  // forward-MAE total: strided partials, fixed xor tree
+      if (ph2 && blockIdx.x == 0 && warp == 1) {  // forward-MAE total: strided partials, fixed xor tree
         double v[5];
 #pragma unroll
         for (int u = 0; u < 5; ++u) v[u] = lane + 32 * u < S ? __ldcg(a.mae_part + lane + 32 * u) : 0.0;
         double t = (((v[0] + v[1]) + v[2]) + v[3]) + v[4];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-        if (lane == 0) *mae_dst = t;
+        if (lane == 0) *(kStream ? r.mae_total[k & 1] : a.mae_total) = t;
       }
       if (kStream) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        asm volatile("bar.sync 3, 288;" ::: "memory");
+        if (threadIdx.x == 32) {
           __threadfence();
           atomicAdd(ph2 ? &sy->dec_done : &sy->enc_done, 1ull);
         }
       }
       WSTAMP(ph2 ? 4 : 1);
     }
+    }  // warp != 0
+    }  // kStream || ph2
     if (kStream) {
       // before phase 2: the epilogue warps wait for this step's h (post
       // cluster / row kernel); the producer and the split warps run on
@@ -697,7 +719,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
       // after phase 2: a failed wait (abort / timeout) anywhere -- every CTA
       // sees the flags at the same grid barrier, so all leave together
       if (ph2) {
-        grid_sync2(bar_cnt, bar_flags, (unsigned)S, sy, ++bar_epoch);
+        grid_sync2<true>(bar_cnt, bar_flags, (unsigned)S, sy, ++bar_epoch);
         if (threadIdx.x == 0) s_go = (ld_acquire_i(&sy->abort) | ld_acquire_i(&sy->error)) ? 0 : 1;
         __syncthreads();
         if (!s_go) break;
@@ -751,7 +773,8 @@ void prepare_wide2() {
 static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const StreamArgs& r0, int S, bool stream,
                          cudaStream_t s) {
   prepare_wide2();
-  const StreamArgs& r = r0;
+  StreamArgs r = r0;
+  if (const char* rot = std::getenv("LTFB_W2_ROT")) r.tile_rot = std::atoi(rot) % std::max(S, 1);
   Wide2Params tp;
   std::memcpy(&tp.tm_y, p.y_sel >= 0 ? p.y_alt[p.y_sel] : p.maps, sizeof(CUtensorMap));
   std::memcpy(&tp.tm_wet, p.maps + 128, sizeof(CUtensorMap));

@@ -120,6 +120,7 @@ struct StreamArgs {
   float* red_dec[2];
   double* mae_total[2];
   unsigned long long* prof;  // LTFB_STREAM_PROF: [n x 16] %globaltimer stamps per step, else null
+  int tile_rot;              // k_wide2: CTA c owns the column tiles of index (c + tile_rot) % S
 };
 
 /// Candidate evaluation (train_ops.hpp:191-205) over a resident slice.

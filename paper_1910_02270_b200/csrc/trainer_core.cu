@@ -252,7 +252,8 @@ DeviceTrainer::DeviceTrainer(const TrainerSpec& spec) : spec_(spec) {
     // the post cluster leaves free; LTFB_WIDE_V1=1 (A/B runs) or a shape
     // k_wide2 does not cover: the 32-column kernels (k_wide_ps streamed,
     // k_wide_tc launched)
-    const int Ss2 = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, ltfb_dev::wide2_tiles(a));
+    int Ss2 = std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, ltfb_dev::wide2_tiles(a));
+    if (const char* ws = std::getenv("LTFB_WIDE_CTAS")) Ss2 = std::max(1, std::min(Ss2, std::atoi(ws)));  // A/B runs
     wide2_ = wide_kind_ >= 2 && !std::getenv("LTFB_WIDE_V1") && ltfb_dev::wide2_supported(a, Ss2);
     const int Ss = wide2_ ? Ss2
                           : std::min<int>(sm_count_ - 2 * ltfb_dev::kPostCluster, static_cast<int>((ma.out + 31) / 32));
@@ -1016,11 +1017,16 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
         if (std::getenv("LTFB_STREAM_PROF") && std::getenv("LTFB_STREAM_PROF")[0] == '2') {
           std::vector<unsigned long long> sm(S_stream_);
           LTFB_CUDA(cudaMemcpy(sm.data(), prof_.p + 512 * steps, S_stream_ * 8, cudaMemcpyDeviceToHost));
-          std::fprintf(stderr, "\n  per CTA (cta:sm p2part barrier, us vs CTA 0 partials):");
-          for (int c = 0; c < S_stream_; ++c)
-            std::fprintf(stderr, " %d:%llu %.1f %.1f", c, sm[c],
-                         ((double)h[512 * k + 128 + c] - (double)h[512 * k + 128]) * 1e-3,
-                         ((double)h[512 * k + 300 + c] - (double)h[512 * k + 128]) * 1e-3);
+          for (std::size_t kk = 2; kk + 1 < steps && kk < 12; ++kk) {
+            std::fprintf(stderr, "\n  per CTA step %zu (cta:sm p2part, us vs median, > 1.5 us):", kk);
+            std::vector<double> d;
+            for (int c = 0; c < S_stream_; ++c) d.push_back((double)h[512 * kk + 128 + c]);
+            std::vector<double> srt = d;
+            std::sort(srt.begin(), srt.end());
+            const double med = srt[srt.size() / 2];
+            for (int c = 0; c < S_stream_; ++c)
+              if ((d[c] - med) * 1e-3 > 1.5) std::fprintf(stderr, " %d:%llu %.1f", c, sm[c], (d[c] - med) * 1e-3);
+          }
         }
         std::fprintf(stderr, "\n  tiles of step 3 (us from w.p2): prod / staged / mma2 / epi / mma3 / O-ready\n");
         for (int j = 0; j < 8; ++j) {

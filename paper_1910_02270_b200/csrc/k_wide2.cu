@@ -774,6 +774,18 @@ static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const Str
                          cudaStream_t s) {
   prepare_wide2();
   StreamArgs r = r0;
+  // Which CTAs own one column tile fewer (when S does not divide the tile
+  // count): the 'short' owner indices are the last n_short; the rotation
+  // puts grid CTAs 16, 17, ... on them. Measured: those two CTAs land on the
+  // one TPC that shares a GPC with the post cluster (SMs 122/123 on every box
+  // measured, whichever tiles they own -- LTFB_W2_ROT A/B) and run each
+  // tile ~1.5x slower, so the step's phase-2 barrier waited for them
+  // (-2.3 us per step with the rotation). A placement heuristic only: the
+  // arithmetic is the same for any rotation given the same rotation in both
+  // step modes (it is a property of the trainer's launches, not of the data).
+  const int ntiles = wide2_tiles(a);
+  const int n_short = ntiles % S ? S - ntiles % S : 0;
+  r.tile_rot = n_short > 0 ? ((S - n_short - 16) % S + S) % S : 0;
   if (const char* rot = std::getenv("LTFB_W2_ROT")) r.tile_rot = std::atoi(rot) % std::max(S, 1);
   Wide2Params tp;
   std::memcpy(&tp.tm_y, p.y_sel >= 0 ? p.y_alt[p.y_sel] : p.maps, sizeof(CUtensorMap));

@@ -1112,7 +1112,7 @@ __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R
 /// decision every CTA of the cluster computes).
 __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const Rows& R, double* s_loss, int* s_ok,
                                       double* s_wl, const StreamArgs* rs = nullptr, int k = 0,
-                                      int* out = nullptr) {
+                                      int* out = nullptr, unsigned* dflag = nullptr) {
   cg::cluster_group cl = cg::this_cluster();
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1178,7 +1178,24 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
       wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
     }
     __syncthreads();
-    cluster_sync();  // S3b
+    // push dL/dlatent (dec, cycle) into the D/G partner (same rows), then
+    // raise its flag; it reads them locally (no cluster barrier)
+    {
+      float* s = S();
+      float* peer = cl.map_shared_rank(s, R.rank);
+      for (int i = tid; i < kR * m.lat; i += kThreads) {
+        peer[Y.gl_dec + i] = s[Y.gl_dec + i];
+        peer[Y.gl_inv + i] = s[Y.gl_inv + i];
+      }
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        const uint32_t fa = tc::smem_u32(dflag);
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(fa), "r"((unsigned)R.rank));
+        asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"((unsigned)(k + 1)) : "memory");
+      }
+    }
   }
   bool f_app = false, i_app = false;
   if (d_ok) {
@@ -1502,6 +1519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int s_res[3];    // d_ok, fwd applied, inv applied of the step
   __shared__ int s_err[2];    // StepSync::error seen before S6 (step parity; read from rank 0)
   __shared__ int s_w;
+  __shared__ unsigned s_dflag;  // D/G half: steps whose gl_dec / gl_inv the cyc partner has pushed
   __shared__ __align__(8) uint64_t s_bar;
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1527,6 +1545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned long long t_disc = a.ctr->t[kDisc], t_fwd = a.ctr->t[kFwd], t_inv = a.ctr->t[kInv];
   unsigned long long skipped = a.ctr->skipped;
   if (tid == 0) {
+    s_dflag = 0;
     g_nst = 0;
     g_persist = 1;
     tc::mbar_init(&s_bar, 1);
@@ -1564,7 +1583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (half == 1) {
       int res[3];
-      cyc_half(a, Y, R, s_loss, s_ok, s_wl, &r, k, res);
+      cyc_half(a, Y, R, s_loss, s_ok, s_wl, &r, k, res, &s_dflag);
       PSTAMP(15);
       if (tid == 0) {
         s_res[0] = res[0];
@@ -1604,7 +1623,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncthreads();
       pg_net(C, Y.stacked, 2 * kR, Y.pg[0]);
       GSTAMP(106);
-      if (tid == 0) s_loss[0] = sum_warps(s_wl);
+      if (tid == 0) {
+        s_loss[0] = sum_warps(s_wl);
+        s_err[k & 1] = ld_acquire_i(&sy->error);  // read by every CTA at the end of the step (after S1)
+      }
       __syncthreads();
       cluster_arrive();  // S1
       cluster_wait();
@@ -1626,26 +1648,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         wnet_bwd(C, 2, Y.gd, -1, -1);
       }
-      if (tid == 0) s_err[k & 1] = ld_acquire_i(&sy->error);  // read by every CTA after S3b
       if (k > 0) transpose_net(F);  // W^T of the fwd pulled last step (input gradients below)
-      __syncthreads();
       GSTAMP(94);
-      cluster_sync();  // S3b: the partner's dec-head backward (after the wide pass's dec half) is done
-      GSTAMP(95);
-      {
-        float* s = S();
-        const float* pdec = cl.map_shared_rank(s + Y.gl_dec, kC + R.rank);
-        const float* pinv = cl.map_shared_rank(s + Y.gl_inv, kC + R.rank);
-        for (int i = tid; i < kR * m.lat; i += kThreads) {
-          s[Y.gl_dec + i] = pdec[i];
-          s[Y.gl_inv + i] = pinv[i];
+      // the partner's dec-head backward (after the wide pass's dec half):
+      // it pushes gl_dec and gl_inv into this CTA's shared memory and then
+      // raises s_dflag (release, cluster scope) -- a pairwise hand-off, no
+      // cluster barrier
+      if (tid == 0) {
+        const unsigned want = (unsigned)(k + 1);
+        const unsigned long long t0 = gtimer();
+        unsigned v;
+        for (;;) {
+          asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(tc::smem_u32(&s_dflag)) : "memory");
+          if (v >= want) break;
+          if (gtimer() - t0 > kStreamTimeoutNs) {
+            if (atomicCAS(&sy->error, 0, 1) == 0) sy->err_site = 7;
+            break;
+          }
         }
-        if (tid == 0) {  // the partner saw dec_done(k) before S3b; the MAE total of step k
-          wait_counter(&sy->dec_done, (unsigned long long)r.S_wide * (k + 1), sy, 5);
-          g_pre[6] = __ldcg(r.mae_total[k & 1]);
-        }
-        __syncthreads();
+        // the partner saw dec_done(k) before its push; the MAE total of step k
+        wait_counter(&sy->dec_done, (unsigned long long)r.S_wide * (k + 1), sy, 5);
+        g_pre[6] = __ldcg(r.mae_total[k & 1]);
       }
+      __syncthreads();
+      GSTAMP(95);
       if (d_ok) {
         {  // grad_latent = (dec + disc) + inv (train_ops.hpp:104, 116-117, 126-127), the warp's rows
           float* s = S();

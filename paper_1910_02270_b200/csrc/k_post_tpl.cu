@@ -667,6 +667,15 @@ __device__ __noinline__ void pull_net(const NetS& n, int gr, int rbase, bool wT)
   }
 }
 
+/// Streamed step: this owner's new parameters [lo, hi) (adam_compute left
+/// them in its gr slice) into the net's global staging copy, which every CTA
+/// refreshes from once the step's decision is known (no extra barrier: the
+/// copy is written before the cluster barrier that publishes the decision).
+__device__ __forceinline__ void stage_new_params(float* dst, int gr, int lo, int hi) {
+  const float* s = S();
+  for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) dst[e] = s[gr + e - lo];
+}
+
 /// Streamed step: net n's new parameters from global memory (the owners'
 /// adam_commit wrote them before the cluster barrier that precedes this
 /// call) into this CTA's blob image (and W^T image if wT).
@@ -960,6 +969,7 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   const int iok = R.split ? 1 : reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2]);
   adam_compute(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], g_pre[2], g_pre[3], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1],
                Y.vt[1]);
+  if (g_persist) stage_new_params(a.g[kFwd], Y.gr[1], R.lo[1], R.hi[1]);  // published by S5
   if (!R.split)
     adam_compute(a, kInv, Y.net[kI], R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2],
                  Y.vt[2]);
@@ -1007,9 +1017,10 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
-    if (g_persist)  // streamed step: every CTA pulls the new fwd from the owners (pull_net)
-      adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 0);
-    else
+    if (g_persist) {
+      // streamed step: every CTA refreshes the new fwd from the staging copy;
+      // the owners commit p / m / v after next_h (off the critical path)
+    } else
       adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1],
                   a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
     out[4] = 1.0;
@@ -1144,6 +1155,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
   const int iok = reduce_owned(Y.pg[2], R.lo[2], R.hi[2], Y.gr[2], kC);
   if (tid == 0) s_ok[2] = iok;
   adam_compute(a, kInv, I, R.lo[2], R.hi[2], g_pre[4], g_pre[5], Y.gr[2], Y.mo[2], Y.vo[2], Y.mt[2], Y.vt[2]);
+  if (rs) stage_new_params(a.g[kInv], Y.gr[2], R.lo[2], R.hi[2]);  // published by S2
   cluster_sync();  // S2 (d_update's flags)
   double d_sum = 0.0;
   int all_ok = 1;
@@ -1590,11 +1602,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_res[1] = res[1];
         s_res[2] = res[2];
       }
-      // the generator's new parameters from global memory, where the owners
-      // wrote them before S6: fwd (blob) and inv (blob + W^T)
-      if (res[0]) cluster_sync();  // S6 (the D/G half reaches it only when the G-step ran)
-      if (res[1]) refresh_net(F, a.p[kFwd], false);
-      if (res[2]) refresh_net(Y.net[kI], a.p[kInv], true);
+      // the generator's new parameters from the owners' staging copies
+      // (fwd: written before S5, inv: before S2): fwd (blob) and inv (blob
+      // + W^T); no further cluster barrier this step
+      if (res[1]) refresh_net(F, a.g[kFwd], false);
+      if (res[2]) refresh_net(Y.net[kI], a.g[kInv], true);
       cp_wait_all();   // the next step's x rows
       __syncthreads();
       for (int i = tid; i < kR * m.in; i += kThreads) S()[Y.xs + i] = S()[Y.xn + i];
@@ -1633,6 +1645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       GSTAMP(107);
       PSTAMP(10);
       double d_loss = 0.0;
+      bool commit_fwd = false;
       const bool d_ok = d_update(a, Y, R, s_loss, s_ok, &d_loss);
       PSTAMP(11);
       if (tid == 0)
@@ -1697,8 +1710,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the new fwd blob straight from the owners' slices (its W^T image is
         // rebuilt next step while this half waits for the dec half)
         GSTAMP(90);
-        cluster_sync();  // S6: the owners' new fwd (and the cyc half's inv) are in global memory
-        if (g[4] != 0.0) refresh_net(F, a.p[kFwd], false);
+        // the new fwd from the owners' staging copy (written before S5)
+        if (g[4] != 0.0) refresh_net(F, a.g[kFwd], false);
+        commit_fwd = g[4] != 0.0;
         GSTAMP(91);
         __syncthreads();
         PSTAMP(13);
@@ -1717,6 +1731,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       PSTAMP(14);
+      if (commit_fwd)  // the owners' fwd p / m / v (and W^T) into global memory and their moment images
+        adam_commit(a, kFwd, F, R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 0);
       if (R.rank == 0 && tid == 0) finish(a, d_ok, d_loss, s_g);
     }
     // ---- the step's decision, identical in every CTA ----

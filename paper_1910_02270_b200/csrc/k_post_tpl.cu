@@ -458,7 +458,7 @@ __device__ __noinline__ void adam_compute(const StepArgs& a, int net, const NetS
 /// has to pull or re-transpose the updated network.
 __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS& n, int lo, int hi, int gr, int mo,
                                          int vo, int mt, int vt, int push /* 1 blob, 2 blob + W^T */,
-                                         int rbase = 0, int rcount = kC) {
+                                         int rbase = 0, int rcount = kC, bool globals = true) {
   cg::cluster_group cl = cg::this_cluster();
   float* s = S();
   float* p = a.p[net];
@@ -470,9 +470,13 @@ __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS&
     const float mn = s[mt + e - lo], vn = s[vt + e - lo];
     s[mo + e - lo] = mn;  // the owner slice's moments stay resident (streamed step)
     s[vo + e - lo] = vn;
-    m1[e] = mn;
-    m2[e] = vn;
-    p[e] = pn;
+    if (globals) {
+      m1[e] = mn;
+      m2[e] = vn;
+      p[e] = pn;
+    } else if (!push) {
+      continue;  // nothing else to write
+    }
     int t = -1;  // W^T position of a weight element (biases have none)
     for (int l = 0; l < n.L; ++l) {
       const int in = n.w[l], out = n.w[l + 1], q = e - n.woff[l];
@@ -481,12 +485,35 @@ __device__ __noinline__ void adam_commit(const StepArgs& a, int net, const NetS&
         t = n.T[l] + j * (in + 1) + k;
       }
     }
-    if (t >= 0) pT[t - n.Tall] = pn;
+    if (globals && t >= 0) pT[t - n.Tall] = pn;
     if (push) {
       for (int r = rbase; r < rbase + rcount; ++r) {
         float* peer = cl.map_shared_rank(s, r);
         peer[n.blob + e] = pn;
         if (push == 2 && t >= 0) peer[t] = pn;
+      }
+    }
+  }
+}
+
+/// The streamed step defers the global p / m / v / W^T writes of the D/G
+/// half's commits (disc, fwd) to the end of the run: the owner slice of `net`
+/// from this CTA's resident images (blob, moment images), written once.
+__device__ __noinline__ void commit_globals(const StepArgs& a, int net, const NetS& n, int lo, int hi, int mo,
+                                            int vo) {
+  const float* s = S();
+  float* p = a.p[net];
+  float* pT = a.pT[net];
+  for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
+    const float pn = s[n.blob + e];
+    a.mom1[net][e] = s[mo + e - lo];
+    a.mom2[net][e] = s[vo + e - lo];
+    p[e] = pn;
+    for (int l = 0; l < n.L; ++l) {
+      const int in = n.w[l], out = n.w[l + 1], q = e - n.woff[l];
+      if (q >= 0 && q < in * out) {
+        const int k = q / out, j = q - k * out;
+        pT[n.T[l] - n.Tall + j * (in + 1) + k] = pn;
       }
     }
   }
@@ -944,7 +971,8 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
     for (int r = 0; r < kC; ++r) all_ok &= v[r];
   }
   const bool d_ok = isfinite(*d_loss) && all_ok;
-  if (d_ok) adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0], 2);
+  if (d_ok)
+    adam_commit(a, kDisc, C, R.lo[0], R.hi[0], Y.gr[0], Y.mo[0], Y.vo[0], Y.mt[0], Y.vt[0], 2, 0, kC, !g_persist);
   ST();
   cluster_sync();  // S3: every owner's updated disc slice (blob + W^T) pushed into every CTA
   return d_ok;
@@ -1504,6 +1532,43 @@ __device__ __noinline__ void prefetch_next_x(const StepArgs& a, const Layout& Y,
   }
 }
 
+/// D/G half of the streamed step: the next step's row indices into s_xidx
+/// by cp.async (no thread waits on the index loads at the top of the step);
+/// prefetch_next_x_from_idx issues the x-row copies once they have landed.
+__device__ __forceinline__ void prefetch_next_idx(const StepArgs& a, const Rows& R, int nxt, unsigned epoch,
+                                                  unsigned* s_xidx) {
+  if ((long long)nxt * a.B >= (long long)a.n_part) return;
+  const int rows = min(a.B, a.n_part - nxt * a.B);
+  const int per = (rows + kC - 1) / kC;
+  const int r0 = min(R.rank * per, rows), nr = max(0, min(per, rows - r0));
+  const unsigned* perm = a.perm[epoch & 1u] + (long long)nxt * a.B + r0;
+  if ((int)threadIdx.x < nr)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(s_xidx + threadIdx.x)),
+                 "l"(perm + threadIdx.x)
+                 : "memory");
+}
+
+/// x rows of step `nxt` into xn from the landed indices (after a cp_wait_all
+/// and a CTA barrier), async; same copies as prefetch_next_x.
+__device__ __noinline__ void prefetch_next_x_from_idx(const StepArgs& a, const Layout& Y, const Rows& R, int nxt,
+                                                      const unsigned* s_xidx) {
+  float* s = S();
+  const int in = a.m.in;
+  if ((long long)nxt * a.B >= (long long)a.n_part) return;
+  const int rows = min(a.B, a.n_part - nxt * a.B);
+  const int per = (rows + kC - 1) / kC;
+  const int r0 = min(R.rank * per, rows), nr = max(0, min(per, rows - r0));
+  for (int i = threadIdx.x; i < kR * in; i += kThreads) {
+    const int r = i / in, c = i - r * in;
+    if (r < nr)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_u32(s + Y.xn + i)),
+                   "l"(a.sx + (long long)s_xidx[r] * in + c)
+                   : "memory");
+    else
+      s[Y.xn + i] = 0.0f;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_post_loop(const __grid_constant__ StepArgs ap, const __grid_constant__ Layout Lp,
                 const __grid_constant__ StreamArgs rp) {
@@ -1532,6 +1597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int s_err[2];    // StepSync::error seen before S6 (step parity; read from rank 0)
   __shared__ int s_w;
   __shared__ unsigned s_dflag;  // D/G half: steps whose gl_dec / gl_inv the cyc partner has pushed
+  __shared__ unsigned s_xidx[kR];  // D/G half: the next step's row indices (cp.async)
   __shared__ __align__(8) uint64_t s_bar;
   const ModelArgs& m = a.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1587,11 +1653,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) g_pb = (r.prof && crank == 0) ? r.prof + 512 * k : nullptr;
     set_rows(sie);
     const int nr = R.nr, rows = R.rows;
-    prefetch_next_x(a, Y, R, sie + 1, r.epoch);
-    if (tid < 3) {  // Adam bias corrections 1 - b^t of this step's t (host std::pow table)
-      const unsigned long long t = (tid == 0 ? t_disc : (tid == 1 ? t_fwd : t_inv)) + 1;
-      g_pre[2 * tid] = a.adam_c[2 * t];
-      g_pre[2 * tid + 1] = a.adam_c[2 * t + 1];
+    if (half == 1) prefetch_next_x(a, Y, R, sie + 1, r.epoch);
+    else prefetch_next_idx(a, R, sie + 1, r.epoch, s_xidx);  // rows issued after d_update
+    if (tid >= 32 && tid < 35) {  // Adam bias corrections 1 - b^t of this step's t (host std::pow table)
+      const int q = tid - 32;     // (not thread 0: it polls the wide pass's counters)
+      const unsigned long long t = (q == 0 ? t_disc : (q == 1 ? t_fwd : t_inv)) + 1;
+      g_pre[2 * q] = a.adam_c[2 * t];
+      g_pre[2 * q + 1] = a.adam_c[2 * t + 1];
     }
     if (half == 1) {
       int res[3];
@@ -1620,7 +1688,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       GSTAMP(100);
       if (ET.L > 0) wnet_fwd(ET, Y.e1, 2, Y.stacked);  // real latents -> stacked[0, R)
       GSTAMP(101);
-      wnet_fwd(F, Y.xs, 2, latent);                    // fake latents -> stacked[R, 2R)
+      // fake latents -> stacked[R, 2R): from step 1 of the run on, next_h of
+      // the previous step computed exactly this tape (same updated fwd, same
+      // x rows, same routine; train_ops.hpp:165 and :97 use the same fwd)
+      if (k == 0) wnet_fwd(F, Y.xs, 2, latent);
       GSTAMP(102);
       wnet_fwd(C, Y.stacked, 4, -1);                   // disc on [real; fake]
       GSTAMP(103);
@@ -1648,6 +1719,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool commit_fwd = false;
       const bool d_ok = d_update(a, Y, R, s_loss, s_ok, &d_loss);
       PSTAMP(11);
+      prefetch_next_x_from_idx(a, Y, R, sie + 1, s_xidx);  // indices landed (d_update's wait + barriers)
       if (tid == 0)
         for (int i = 0; i < 6; ++i) s_g[i] = 0.0;
       if (d_ok) {
@@ -1732,7 +1804,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       PSTAMP(14);
       if (commit_fwd)  // the owners' fwd p / m / v (and W^T) into global memory and their moment images
-        adam_commit(a, kFwd, F, R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 0);
+        adam_commit(a, kFwd, F, R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1], 0, 0, kC, false);
       if (R.rank == 0 && tid == 0) finish(a, d_ok, d_loss, s_g);
     }
     // ---- the step's decision, identical in every CTA ----
@@ -1756,6 +1828,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 #undef PSTAMP
   cp_wait_all();
+  if (half == 0) {  // the deferred global writes of the run's disc / fwd commits
+    __syncthreads();
+    commit_globals(a, kDisc, Y.net[kCd], R.lo[0], R.hi[0], Y.mo[0], Y.vo[0]);
+    commit_globals(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.mo[1], Y.vo[1]);
+  }
   cluster_sync();  // no CTA leaves while peers may still read its shared memory
 }
 

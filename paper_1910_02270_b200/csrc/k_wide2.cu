@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         if (lane == 0) red[quad] = t;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (rr == 0) a.mae_part[blockIdx.x] = ((red[0] + red[1]) + red[2]) + red[3];
+        if (prof && rr == 0 && blockIdx.x < 40) prof[512 * k + 432 + blockIdx.x] = gtimer();
       }
     } else {
       // ----------------------------------------------------- tf32 split --
@@ -621,6 +622,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     if (warp != 0) {
     if (ph2) WSTAMP(3);
     if (ph2 && prof && blockIdx.x == 0 && threadIdx.x == 64) prof[512 * k + 299] = gtimer();
+    if (ph2 && prof && blockIdx.x < 40 && threadIdx.x == 32) prof[512 * k + 472 + blockIdx.x] = gtimer();
     if (ph2 && prof) {
       asm volatile("bar.sync 3, 288;" ::: "memory");
       if (threadIdx.x == 32) prof[512 * k + 300 + blockIdx.x] = gtimer();

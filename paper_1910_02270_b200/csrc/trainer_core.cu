@@ -1013,6 +1013,12 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
             std::fprintf(stderr, "\n  phase-2 barrier arrival per CTA vs CTA 0 partials (us): min %.2f median %.2f max %.2f; CTA0 pre-sync %.2f",
                          b.front(), b[b.size() / 2], b.back(),
                          ((double)h[512 * k + 299] - (double)h[512 * k + 128]) * 1e-3);
+          std::fprintf(stderr, "\n  CTA c<40 (us vs own partials): mae-done / warp1-at-end / arrival:");
+          for (int c = 0; c < std::min(40, S_stream_); ++c) {
+            const double p0 = (double)h[512 * k + 128 + c];
+            std::fprintf(stderr, " [%d %.2f %.2f %.2f]", c, ((double)h[512 * k + 432 + c] - p0) * 1e-3,
+                         ((double)h[512 * k + 472 + c] - p0) * 1e-3, ((double)h[512 * k + 300 + c] - p0) * 1e-3);
+          }
         }
         if (std::getenv("LTFB_STREAM_PROF") && std::getenv("LTFB_STREAM_PROF")[0] == '2') {
           std::vector<unsigned long long> sm(S_stream_);

@@ -87,40 +87,36 @@ struct Wide2Params {
   CUtensorMap tm_y, tm_wet, tm_wd, tm_wdt;  // y rows (gather4), WeT / Wd [64 x out_pad], WdT [out_pad x 64] (box 64 rows)
 };
 
-/// Grid barrier over `n` CTAs that are all resident: arrival is one acq_rel
-/// atomic on cnt; the last arriver releases every CTA's own flag line
-/// (flags[32 c]), so waiters poll disjoint lines. `epoch` only grows. A
-/// missing CTA raises sy->error after the timeout (streamed mode) instead of
-/// hanging the GPU; launched mode traps.
+/// Grid barrier over `n` CTAs that are all resident: arrival is one release
+/// reduction on cnt, and every CTA's leader polls cnt itself (acquire) until
+/// it reaches n * epoch (no flag fan-out by the last arriver: measured ~4 us
+/// from the last arrival to the release with per-CTA flags after a fence).
+/// `epoch` only grows; the comparison is modular. A missing CTA raises
+/// sy->error after the timeout (streamed mode) instead of hanging the GPU;
+/// launched mode traps.
 /// kFull: every thread of the CTA takes part (leader thread 0); else warps
 /// 1-9 only (named barrier 3, leader thread 32): the phase-end barrier, which
 /// the producer warp skips so its next-phase prefetch never delays it.
 template <bool kFull>
 __device__ __forceinline__ void grid_sync2(unsigned* cnt, unsigned* flags, unsigned n, StepSync* sy,
                                            unsigned epoch) {
+  (void)flags;
   if (kFull) __syncthreads();
   else asm volatile("bar.sync 3, 288;" ::: "memory");
   if (threadIdx.x == (kFull ? 0u : 32u)) {
-    unsigned old;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-    if (old + 1 == n * epoch) {
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      for (unsigned c = 0; c < n; ++c)
-        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + 32 * c), "r"(epoch) : "memory");
-    } else {
-      const unsigned long long t0 = gtimer();
-      unsigned cur;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(flags + 32 * blockIdx.x) : "memory");
-        if (cur >= epoch) break;
-        if (gtimer() - t0 > kStreamTimeoutNs) {
-          if (sy) {
-            if (atomicCAS(&sy->error, 0, 2) == 0) sy->err_site = 6;
-            break;
-          }
-          __trap();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    const unsigned target = n * epoch;
+    const unsigned long long t0 = gtimer();
+    unsigned cur;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(cnt) : "memory");
+      if ((int)(cur - target) >= 0) break;
+      if (gtimer() - t0 > kStreamTimeoutNs) {
+        if (sy) {
+          if (atomicCAS(&sy->error, 0, 2) == 0) sy->err_site = 6;
+          break;
         }
-        __nanosleep(32);
+        __trap();
       }
     }
   }
@@ -508,7 +504,6 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         if (lane == 0) red[quad] = t;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (rr == 0) a.mae_part[blockIdx.x] = ((red[0] + red[1]) + red[2]) + red[3];
-        if (prof && rr == 0 && blockIdx.x < 40) prof[512 * k + 432 + blockIdx.x] = gtimer();
       }
     } else {
       // ----------------------------------------------------- tf32 split --
@@ -629,6 +624,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
     }
     grid_sync2<false>(bar_cnt, bar_flags, (unsigned)S, sy, bar_epoch);
     WSTAMP(ph2 ? 22 : 21);
+    if (ph2 && prof && blockIdx.x < 40 && threadIdx.x == 32) prof[512 * k + 432 + blockIdx.x] = gtimer();
     {
       const int q_all = rows * (kW / 4);  // float4 outputs of P_enc or P_dec
       const int lo = (int)((long long)q_all * blockIdx.x / S);

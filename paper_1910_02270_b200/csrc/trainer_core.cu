@@ -1013,11 +1013,18 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
             std::fprintf(stderr, "\n  phase-2 barrier arrival per CTA vs CTA 0 partials (us): min %.2f median %.2f max %.2f; CTA0 pre-sync %.2f",
                          b.front(), b[b.size() / 2], b.back(),
                          ((double)h[512 * k + 299] - (double)h[512 * k + 128]) * 1e-3);
-          std::fprintf(stderr, "\n  CTA c<40 (us vs own partials): mae-done / warp1-at-end / arrival:");
-          for (int c = 0; c < std::min(40, S_stream_); ++c) {
-            const double p0 = (double)h[512 * k + 128 + c];
-            std::fprintf(stderr, " [%d %.2f %.2f %.2f]", c, ((double)h[512 * k + 432 + c] - p0) * 1e-3,
-                         ((double)h[512 * k + 472 + c] - p0) * 1e-3, ((double)h[512 * k + 300 + c] - p0) * 1e-3);
+          {  // barrier latency: last arrival vs release, all in us from CTA 0's partials
+            const double p0 = (double)h[512 * k + 128];
+            double last = -1e30, rel_min = 1e30, rel_max = -1e30;
+            for (int c = 0; c < S_stream_; ++c)
+              if (h[512 * k + 300 + c]) last = std::max(last, ((double)h[512 * k + 300 + c] - p0) * 1e-3);
+            for (int c = 0; c < std::min(40, S_stream_); ++c)
+              if (h[512 * k + 432 + c]) {
+                rel_min = std::min(rel_min, ((double)h[512 * k + 432 + c] - p0) * 1e-3);
+                rel_max = std::max(rel_max, ((double)h[512 * k + 432 + c] - p0) * 1e-3);
+              }
+            std::fprintf(stderr, "\n  phase-2 barrier (us vs CTA 0 partials): last arrival %.2f, release (CTAs < 40) %.2f .. %.2f",
+                         last, rel_min, rel_max);
           }
         }
         if (std::getenv("LTFB_STREAM_PROF") && std::getenv("LTFB_STREAM_PROF")[0] == '2') {

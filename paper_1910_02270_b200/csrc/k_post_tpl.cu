@@ -1630,11 +1630,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc::fence_barrier_init();
   }
   __syncthreads();
-  if (crank == 0 && tid == 0) {  // resident: the host may launch the wide pass now
+  if (crank == 0 && tid == 0) {  // resident (host-visible flag: the k_wide_ps path waits for it)
     sy->t_post0 = gtimer();
     *reinterpret_cast<volatile int*>(r.resident_host) = r.run_id;
     __threadfence_system();
   }
+  // the wide pass (k_wide2) is a programmatic dependent launch on this
+  // stream: it may start as soon as every CTA of this cluster is resident
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.ctr->aborted) {  // trainer.hpp:282-288: a run after the abort is all no-ops
     if (crank == 0 && tid == 0) atomicExch(&sy->abort, 1);
     return;

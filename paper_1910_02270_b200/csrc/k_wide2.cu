@@ -798,8 +798,19 @@ static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const Str
   cfg.blockDim = dim3(w2::kThreads);
   cfg.dynamicSmemBytes = w2::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int nat = 0;
+  if (stream) {
+    // programmatic dependent launch behind the post cluster on the same
+    // stream: this grid is scheduled once every post CTA has signalled
+    // (griddepcontrol.launch_dependents right after it became resident), so
+    // it finds exactly the SMs the cluster leaves free -- no host round trip
+    // between the two launches. (This kernel never waits on the post grid's
+    // completion: it synchronises with it through StepSync counters.)
+    at[nat].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[nat].val.programmaticStreamSerializationAllowed = 1;
+    ++nat;
+  }
   if (!stream) {
     // launched mode: cooperative, the grid barrier needs every CTA resident.
     // (Streamed mode is not: a cooperative grid does not start while the post

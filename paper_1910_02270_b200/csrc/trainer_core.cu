@@ -922,17 +922,24 @@ void DeviceTrainer::launch_stream_run(std::size_t steps) {
   LTFB_CUDA(cudaEventRecord(st_ev_[0], stream_));
   LTFB_CUDA(cudaStreamWaitEvent(post_stream_, st_ev_[0], 0));
   ltfb_dev::launch_post_loop(args_, r, post_stream_);
-  release_gate();
-  const auto t0 = std::chrono::steady_clock::now();
-  while (*reinterpret_cast<volatile int*>(resident_) != run_id_) {
-    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
-      stream_on_ = false;
-      throw ltfb::Error("CUDA error: streamed step: the post cluster did not become resident");
+  if (wide2_) {
+    // programmatic dependent launch right behind the cluster on its stream:
+    // the device starts the wide pass once the cluster is resident (no host
+    // wait between the launches, so the host can run ahead of the device)
+    ltfb_dev::launch_wide2_stream(wtp_, args_, r, S_stream_, post_stream_);
+    release_gate();
+  } else {
+    release_gate();
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*reinterpret_cast<volatile int*>(resident_) != run_id_) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20)) {
+        stream_on_ = false;
+        throw ltfb::Error("CUDA error: streamed step: the post cluster did not become resident");
+      }
+      std::this_thread::yield();
     }
-    std::this_thread::yield();
+    ltfb_dev::launch_wide_ps(wtp_, args_, r, S_stream_, stream_);
   }
-  if (wide2_) ltfb_dev::launch_wide2_stream(wtp_, args_, r, S_stream_, stream_);
-  else ltfb_dev::launch_wide_ps(wtp_, args_, r, S_stream_, stream_);
   LTFB_CUDA(cudaEventRecord(st_ev_[1], post_stream_));
   LTFB_CUDA(cudaStreamWaitEvent(stream_, st_ev_[1], 0));
   launches_ += 3;

@@ -554,12 +554,32 @@ void DeviceTrainer::finish_slice(int which, std::size_t rows) {
 
 // -------------------------------------------------------------- training --
 cudaEvent_t DeviceTrainer::next_event() {
-  if (ev_used_ == ev_pool_.size()) {
-    cudaEvent_t e;
-    LTFB_CUDA(cudaEventCreate(&e));
-    ev_pool_.push_back(e);
+  if (!ev_free_.empty()) {
+    cudaEvent_t e = ev_free_.back();
+    ev_free_.pop_back();
+    return e;
   }
-  return ev_pool_[ev_used_++];
+  cudaEvent_t e;
+  LTFB_CUDA(cudaEventCreate(&e));
+  ev_pool_.push_back(e);
+  return e;
+}
+
+void DeviceTrainer::resolve_epoch_times() {
+  if (pending_epochs_.empty()) return;
+  sync_stream();
+  for (auto& pe : pending_epochs_) {
+    double sec = 0;
+    for (const auto& sg : pe.segs) {
+      float ms = 0;
+      LTFB_CUDA(cudaEventElapsedTime(&ms, sg.a, sg.b));
+      sec += ms * 1e-3;
+      release_event(sg.a);
+      release_event(sg.b);
+    }
+    if (pe.idx < closed_.size()) closed_[pe.idx].seconds += sec;
+  }
+  pending_epochs_.clear();
 }
 
 void DeviceTrainer::close_epoch_segment(bool epoch_done, bool partial) {
@@ -570,16 +590,11 @@ void DeviceTrainer::close_epoch_segment(bool epoch_done, bool partial) {
     seg_open_ = false;
   }
   if (epoch_done) {
-    // resolve timings of this epoch's segments (all recorded on stream_)
-    sync_stream();
-    for (const auto& s : open_segments_) {
-      float ms = 0;
-      LTFB_CUDA(cudaEventElapsedTime(&ms, s.a, s.b));
-      epoch_seconds_ += ms * 1e-3;
-    }
-    open_segments_.clear();
-    ev_used_ = 0;
+    // this epoch's segments (all recorded on stream_) are timed at the next
+    // sync (resolve_epoch_times), so the boundary does not drain the device
     closed_.push_back({epoch_, epoch_steps_, epoch_shuffled_, epoch_seconds_, partial});
+    pending_epochs_.push_back({closed_.size() - 1, std::move(open_segments_)});
+    open_segments_.clear();
     epoch_steps_ = epoch_shuffled_ = 0;
     epoch_seconds_ = 0;
   }
@@ -1093,6 +1108,7 @@ bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepReco
     close_epoch_segment(false, false);
     sync_stream();
     check_stream_error();
+    resolve_epoch_times();
     if (ktime_on_) resolve_kernel_times();
     std::vector<ltfb_dev::StepRec> recs(chunk);
     const std::size_t at = first % rec_.n;
@@ -1144,6 +1160,8 @@ bool DeviceTrainer::train_steps(std::size_t n, std::vector<ltfb::train::StepReco
 }
 
 std::vector<DeviceTrainer::EpochInfo> DeviceTrainer::take_epochs() {
+  DeviceGuard g(spec_.device);
+  resolve_epoch_times();
   std::vector<EpochInfo> out;
   out.swap(closed_);
   return out;
@@ -1154,6 +1172,7 @@ void DeviceTrainer::flush_epoch() {
   if (have_plan_ && step_in_epoch_ > 0) {
     close_epoch_segment(true, step_in_epoch_ < steps_per_epoch_);
   }
+  resolve_epoch_times();
 }
 
 void DeviceTrainer::synchronize() {

@@ -310,12 +310,22 @@ class DeviceTrainer {
   };
   std::vector<EpochMark> epoch_marks_;
   bool aborted_ = false;  // the device abort flag was seen: later steps are refused
-  std::vector<cudaEvent_t> ev_pool_;
-  std::size_t ev_used_ = 0;
+  std::vector<cudaEvent_t> ev_pool_;  // every event created (destroyed with the trainer)
+  std::vector<cudaEvent_t> ev_free_;  // events not in use
   struct Segment {
     cudaEvent_t a, b;
   };
   std::vector<Segment> open_segments_;
+  // closed epochs whose device time is not resolved yet: the epoch boundary
+  // does not wait for the device (closed_[idx].seconds gets the segments'
+  // elapsed times at the next sync, resolve_epoch_times)
+  struct PendingEpoch {
+    std::size_t idx;
+    std::vector<Segment> segs;
+  };
+  std::vector<PendingEpoch> pending_epochs_;
+  void resolve_epoch_times();
+  void release_event(cudaEvent_t e) { ev_free_.push_back(e); }
   cudaEvent_t seg_start_ = nullptr;
   bool seg_open_ = false;
   cudaEvent_t next_event();

@@ -39,7 +39,9 @@ def test_bench_line_contract():
                                           rel=1e-6)
     w = d["kernel_rooflines"]["wide"]
     assert w["frac"] == pytest.approx(w["achieved"] / w["peak"], rel=1e-9)
-    assert 0 < r["frac"] < w["frac"] < 1  # the step is slower than its wide pass alone
+    # (the streamed step overlaps the wide pass's phase 1 with the post cluster, so
+    # since round 2h it is faster than the launched wide pass timed alone)
+    assert 0 < r["frac"] < 1 and 0 < w["frac"] < 1
     # a tournament round is timed at N = 1 too (own payload, device decision)
     assert d["round_ms"] is not None and d["round_ms"] > 0 and d["rounds_timed"] >= 1
     out = d["config"]["output_dim"]

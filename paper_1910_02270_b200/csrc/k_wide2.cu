@@ -178,7 +178,26 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   const int ntiles = (out + kTileN - 1) / kTileN;
   const int S = (int)gridDim.x;
   const int lcta = ((int)blockIdx.x + r.tile_rot) % S;  // column-tile owner index (A/B: LTFB_W2_ROT)
-  const int my_tiles = ntiles > lcta ? (ntiles - 1 - lcta) / S + 1 : 0;
+  // owner lcta holds tiles lcta, lcta + S, ... (base_tiles of them), except
+  // that the first two 'short' owners (lcta L0, L0 + 1: the rotation places
+  // them on the SMs that run tiles slowest) hand their last tile_donate tiles
+  // to the next 2 * tile_donate short owners, one each (the same map in both
+  // step modes: it fixes which tiles a CTA's partial sums)
+  const int base_tiles = ntiles > lcta ? (ntiles - 1 - lcta) / S + 1 : 0;
+  int my_tiles = base_tiles, extra_tile = -1;
+  {
+    const int dn = r.tile_donate, n_short = ntiles % S ? S - ntiles % S : 0, L0 = S - n_short;
+    if (dn > 0 && n_short >= 2 * (1 + dn) && base_tiles > dn && lcta >= L0) {
+      const int o = lcta - L0;
+      if (o < 2) {
+        my_tiles -= dn;
+      } else if (o < 2 + 2 * dn) {
+        const int rr = o - 2;
+        extra_tile = (L0 + rr / dn) + (base_tiles - 1 - rr % dn) * S;
+        my_tiles += 1;
+      }
+    }
+  }
   const int nsteps = kStream ? r.n : 1;
   const int sie0 = kStream ? r.sie0 : (int)a.ctr->step_in_epoch;
   const unsigned epoch = kStream ? r.epoch : a.ctr->epoch;
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
   unsigned* bar_cnt = kStream ? a.grid_bar + 64 : a.grid_bar + kLaunchBar + 32;
   unsigned* bar_flags = bar_cnt + 32;
   const int nphase = 2 * nsteps;
-  auto col0 = [&](int j) { return (lcta + j * S) * kTileN; };
+  auto col0 = [&](int j) { return (j < base_tiles ? lcta + j * S : extra_tile) * kTileN; };
   auto rows_of = [&](int k) { return min(a.B, a.n_part - (sie0 + k) * a.B); };
   auto nkb_of = [&](int c0) { return c0 + 32 < out ? 2 : 1; };  // y / We / Wd K-blocks inside the matrix
   auto row_index = [&](int k, int rr, int rows) {
@@ -785,6 +804,8 @@ static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const Str
   const int n_short = ntiles % S ? S - ntiles % S : 0;
   r.tile_rot = n_short > 0 ? ((S - n_short - 16) % S + S) % S : 0;
   if (const char* rot = std::getenv("LTFB_W2_ROT")) r.tile_rot = std::atoi(rot) % std::max(S, 1);
+  r.tile_donate = 2;  // (those two CTAs ran 2-6 us behind the median with 5 tiles; measured)
+  if (const char* dn = std::getenv("LTFB_W2_DONATE")) r.tile_donate = std::max(0, std::atoi(dn));
   Wide2Params tp;
   std::memcpy(&tp.tm_y, p.y_sel >= 0 ? p.y_alt[p.y_sel] : p.maps, sizeof(CUtensorMap));
   std::memcpy(&tp.tm_wet, p.maps + 128, sizeof(CUtensorMap));

@@ -121,6 +121,7 @@ struct StreamArgs {
   double* mae_total[2];
   unsigned long long* prof;  // LTFB_STREAM_PROF: [n x 16] %globaltimer stamps per step, else null
   int tile_rot;              // k_wide2: CTA c owns the column tiles of index (c + tile_rot) % S
+  int tile_donate;           // k_wide2: tiles each of the two slow-placed owners hands to other short owners
 };
 
 /// Candidate evaluation (train_ops.hpp:191-205) over a resident slice.

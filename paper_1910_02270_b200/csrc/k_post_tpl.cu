@@ -1143,7 +1143,8 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
 /// the inv partials over its own ranks, and applies Adam(inv) on its owner
 /// slices once the step's decision (computed identically from the shared
 /// flags and loss sums) says so.
-__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec);
+__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec,
+                               const double* mae_total);
 
 /// Streamed step (rs != nullptr): the cycle path runs first, then the wait
 /// for the wide pass's dec half of step k (red_dec, the MAE total) and the
@@ -1209,10 +1210,9 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
     if (tid == 0) {
       s_w = wait_counter(&rs->sync->dec_done, (unsigned long long)rs->S_wide * (k + 1), rs->sync, 3) ? 1 : 0;
       if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[512 * k + 7] = gtimer();
-      g_pre[6] = __ldcg(rs->mae_total[k & 1]);
     }
     __syncthreads();
-    stage_dec_rows(a, Y, R, rs->red_dec[k & 1]);
+    stage_dec_rows(a, Y, R, rs->red_dec[k & 1], rs->mae_total[k & 1]);
     if (DH.L > 0) {
       dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
       wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
@@ -1229,6 +1229,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
       }
       __syncthreads();
       if (tid == 0) {
+        cl.map_shared_rank(g_pre, R.rank)[6] = g_pre[6];  // the step's forward-MAE total, for g_update
         asm volatile("fence.acq_rel.cluster;" ::: "memory");
         const uint32_t fa = tc::smem_u32(dflag);
         uint32_t ra;
@@ -1490,7 +1491,8 @@ __device__ __noinline__ void stage_enc_rows(const StepArgs& a, const Layout& Y, 
 }
 
 /// This CTA's rows of dL/dh = (1/n) S Wd^T (cyc half), as the launched prologue.
-__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec) {
+__device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec,
+                               const double* mae_total) {
   float* s = S();
   const ModelArgs& m = a.m;
   const int D = m.D;
@@ -1503,11 +1505,14 @@ __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R
     const int i = (int)threadIdx.x + u * kThreads;
     v[u] = i < kR * D && i / D < R.nr ? __ldcg(red_dec + (long long)R.r0 * D + i) : 0.0f;
   }
+  // the wide pass's forward-MAE total in the same round trip (streamed step)
+  const double mt = (mae_total && threadIdx.x == 0) ? __ldcg(mae_total) : 0.0;
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int i = (int)threadIdx.x + u * kThreads;
     if (i < kR * D) s[gh + i] = v[u] * gscale;
   }
+  if (mae_total && threadIdx.x == 0) g_pre[6] = mt;
   __syncthreads();
 }
 
@@ -1754,9 +1759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             break;
           }
         }
-        // the partner saw dec_done(k) before its push; the MAE total of step k
-        wait_counter(&sy->dec_done, (unsigned long long)r.S_wide * (k + 1), sy, 5);
-        g_pre[6] = __ldcg(r.mae_total[k & 1]);
+        // (the partner pushed the step's MAE total into g_pre[6] with them)
       }
       __syncthreads();
       GSTAMP(95);

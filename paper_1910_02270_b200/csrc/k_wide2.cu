@@ -804,7 +804,7 @@ static void launch_wide2(const WideTcParamsHost& p, const StepArgs& a, const Str
   const int n_short = ntiles % S ? S - ntiles % S : 0;
   r.tile_rot = n_short > 0 ? ((S - n_short - 16) % S + S) % S : 0;
   if (const char* rot = std::getenv("LTFB_W2_ROT")) r.tile_rot = std::atoi(rot) % std::max(S, 1);
-  r.tile_donate = 2;  // (those two CTAs ran 2-6 us behind the median with 5 tiles; measured)
+  r.tile_donate = 3;  // (those two CTAs ran 2-6 us behind the median with 5 tiles; A/B: 1, 2, 3 tiles -0.7, -1.3, -1.5 us)
   if (const char* dn = std::getenv("LTFB_W2_DONATE")) r.tile_donate = std::max(0, std::atoi(dn));
   Wide2Params tp;
   std::memcpy(&tp.tm_y, p.y_sel >= 0 ? p.y_alt[p.y_sel] : p.maps, sizeof(CUtensorMap));

@@ -1144,7 +1144,7 @@ __device__ __noinline__ void next_h(const StepArgs& a, const Layout& Y, int sie,
 /// slices once the step's decision (computed identically from the shared
 /// flags and loss sums) says so.
 __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec,
-                               const double* mae_total);
+                               int S_wide);
 
 /// Streamed step (rs != nullptr): the cycle path runs first, then the wait
 /// for the wide pass's dec half of step k (red_dec, the MAE total) and the
@@ -1212,7 +1212,7 @@ __device__ __noinline__ void cyc_half(const StepArgs& a, const Layout& Y, const 
       if (rs->prof && cg::this_cluster().block_rank() == kC) rs->prof[512 * k + 7] = gtimer();
     }
     __syncthreads();
-    stage_dec_rows(a, Y, R, rs->red_dec[k & 1], rs->mae_total[k & 1]);
+    stage_dec_rows(a, Y, R, rs->red_dec[k & 1], rs->S_wide);
     if (DH.L > 0) {
       dz_warp(Y.gh, DH, DH.L - 1, DH.dz[DH.L - 1]);
       wnet_bwd(DH, 2, Y.gl_dec, -1, -1);
@@ -1492,7 +1492,7 @@ __device__ __noinline__ void stage_enc_rows(const StepArgs& a, const Layout& Y, 
 
 /// This CTA's rows of dL/dh = (1/n) S Wd^T (cyc half), as the launched prologue.
 __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R, const float* red_dec,
-                               const double* mae_total) {
+                               int S_wide) {
   float* s = S();
   const ModelArgs& m = a.m;
   const int D = m.D;
@@ -1505,14 +1505,25 @@ __device__ void stage_dec_rows(const StepArgs& a, const Layout& Y, const Rows& R
     const int i = (int)threadIdx.x + u * kThreads;
     v[u] = i < kR * D && i / D < R.nr ? __ldcg(red_dec + (long long)R.r0 * D + i) : 0.0f;
   }
-  // the wide pass's forward-MAE total in the same round trip (streamed step)
-  const double mt = (mae_total && threadIdx.x == 0) ? __ldcg(mae_total) : 0.0;
+  // the forward-MAE total from the wide CTAs' partials in the same round trip
+  // (streamed step; warp 0; the launched wide pass's fixed order: strided
+  // partials per lane, then an xor tree)
+  double mv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int lane = (int)threadIdx.x & 31;
+  if (S_wide > 0 && threadIdx.x < 32)
+#pragma unroll
+    for (int u = 0; u < 5; ++u) mv[u] = lane + 32 * u < S_wide ? __ldcg(a.mae_part + lane + 32 * u) : 0.0;
 #pragma unroll
   for (int u = 0; u < kPer; ++u) {
     const int i = (int)threadIdx.x + u * kThreads;
     if (i < kR * D) s[gh + i] = v[u] * gscale;
   }
-  if (mae_total && threadIdx.x == 0) g_pre[6] = mt;
+  if (S_wide > 0 && threadIdx.x < 32) {
+    double t = (((mv[0] + mv[1]) + mv[2]) + mv[3]) + mv[4];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0) g_pre[6] = t;
+  }
   __syncthreads();
 }
 

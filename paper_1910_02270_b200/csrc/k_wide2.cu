@@ -703,7 +703,8 @@ __global__ void __launch_bounds__(w2::kThreads, 1)
         reduce(a.P_enc, a.scratch + a.L.red_enc);
         reduce(a.P_dec, a.scratch + a.L.red_dec);
       }
-      if (ph2 && blockIdx.x == 0 && warp == 1) {  // forward-MAE total: strided partials, fixed xor tree
+      if (!kStream && ph2 && blockIdx.x == 0 && warp == 1) {  // forward-MAE total: strided partials, fixed xor tree
+        // (streamed: the post cluster's cyc half sums the partials itself, off this signal's path)
         double v[5];
 #pragma unroll
         for (int u = 0; u < 5; ++u) v[u] = lane + 32 * u < S ? __ldcg(a.mae_part + lane + 32 * u) : 0.0;

@@ -1020,6 +1020,19 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   cluster_sync();  // S5: flags
   GSTAMP(27);
   ST();
+  // streamed step: the new fwd from the owners' staging copy (written before
+  // S5), loaded now so the L2 round trip overlaps the decision below; it
+  // replaces this CTA's blob image only if the fwd update is applied
+  constexpr int kRf = 8;
+  float rv[kRf];
+  const NetS& Fn = Y.net[kF];
+  const bool prefetch_fwd = g_persist && Fn.count <= kRf * kThreads;
+  if (prefetch_fwd)
+#pragma unroll
+    for (int u = 0; u < kRf; ++u) {
+      const int e = u * kThreads + tid;
+      rv[u] = e < Fn.count ? __ldcg(a.g[kFwd] + e) : 0.0f;
+    }
   int all_f = 1, all_i = 1;
   {
     int vf[kC], vi[kC];
@@ -1046,8 +1059,15 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {
     if (g_persist) {
-      // streamed step: every CTA refreshes the new fwd from the staging copy;
-      // the owners commit p / m / v after next_h (off the critical path)
+      // streamed step: every CTA takes the new fwd from the staging copy
+      // (here if prefetched, else the caller refreshes); the owners commit
+      // p / m / v after next_h (off the critical path)
+      if (prefetch_fwd)
+#pragma unroll
+        for (int u = 0; u < kRf; ++u) {
+          const int e = u * kThreads + tid;
+          if (e < Fn.count) S()[Fn.blob + e] = rv[u];
+        }
     } else
       adam_commit(a, kFwd, Y.net[kF], R.lo[1], R.hi[1], Y.gr[1], Y.mo[1], Y.vo[1], Y.mt[1], Y.vt[1],
                   a.post_next_h ? 1 : 0);  // every CTA needs the new fwd blob for next_h
@@ -1799,8 +1819,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the new fwd blob straight from the owners' slices (its W^T image is
         // rebuilt next step while this half waits for the dec half)
         GSTAMP(90);
-        // the new fwd from the owners' staging copy (written before S5)
-        if (g[4] != 0.0) refresh_net(F, a.g[kFwd], false);
+        // the new fwd from the owners' staging copy (written before S5),
+        // unless g_update already took it (prefetched under its decision)
+        if (g[4] != 0.0 && F.count > 8 * kThreads) refresh_net(F, a.g[kFwd], false);
         commit_fwd = g[4] != 0.0;
         GSTAMP(91);
         __syncthreads();

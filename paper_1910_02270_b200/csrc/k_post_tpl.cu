@@ -960,9 +960,10 @@ __device__ __noinline__ bool d_update(const StepArgs& a, const Layout& Y, const 
     from_ranks(s_loss, 0, 0, v);
     for (int r = 0; r < kC; ++r) d_sum += v[r];
   }
+  cluster_arrive();  // S2: flags (arrive; the loss below overlaps the other CTAs' arrivals)
   const double n2 = 2.0 * (double)R.rows;
   *d_loss = ((double)R.rows * (d_sum / n2)) / (double)R.rows;
-  cluster_sync();  // S2: flags
+  cluster_wait();  // S2
   ST();
   int all_ok = 1;
   {
@@ -1017,7 +1018,20 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
       cyc_sum += vc[r];
     }
   }
-  cluster_sync();  // S5: flags
+  cluster_arrive();  // S5: flags (arrive; the loss terms below overlap the other CTAs' arrivals)
+  const int rows = R.rows;
+  const long long n_fwd = (long long)rows * m.out;
+  const long long n_cyc = (long long)rows * m.in;
+  const double adv = adv_sum / (double)rows;
+  const double cyc = cyc_sum / (double)n_cyc;
+  const double fm = g_pre[6] / (double)n_fwd;
+  const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
+  out[0] = ((double)rows * total_raw) / (double)rows;
+  out[1] = ((double)rows * fm) / (double)rows;
+  out[2] = ((double)rows * adv) / (double)rows;
+  out[3] = ((double)rows * cyc) / (double)rows;
+  out[4] = out[5] = 0.0;
+  cluster_wait();  // S5
   GSTAMP(27);
   ST();
   // streamed step: the new fwd from the owners' staging copy (written before
@@ -1043,18 +1057,6 @@ __device__ __noinline__ void g_update(const StepArgs& a, const Layout& Y, const 
       all_i &= vi[r];
     }
   }
-  const int rows = R.rows;
-  const long long n_fwd = (long long)rows * m.out;
-  const long long n_cyc = (long long)rows * m.in;
-  const double adv = adv_sum / (double)rows;
-  const double cyc = cyc_sum / (double)n_cyc;
-  const double fm = g_pre[6] / (double)n_fwd;
-  const double total_raw = fm + (double)m.lambda_adv * adv + (double)m.lambda_cyc * cyc;
-  out[0] = ((double)rows * total_raw) / (double)rows;
-  out[1] = ((double)rows * fm) / (double)rows;
-  out[2] = ((double)rows * adv) / (double)rows;
-  out[3] = ((double)rows * cyc) / (double)rows;
-  out[4] = out[5] = 0.0;
   // trainer.hpp:256-264: g_total, then fwd (throws before any change),
   // then inv (fwd already applied)
   if (isfinite(out[0]) && all_f) {

@@ -34,7 +34,7 @@ sys.path.insert(0, REPO)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 # profiles/traffic.json keys carry this tag: a DRAM-traffic figure measured on
 # another version of the step kernels is not reported (bump on kernel changes)
-KERNEL_VERSION = "r02h"
+KERNEL_VERSION = "r02i"
 
 
 def ae_bench(L, dims, ds, ids, B, arch, source=1024, warmup=5, steps=40):

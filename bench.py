@@ -542,6 +542,14 @@ def main():
                              "~0.1 MB of traffic, so no HBM or tensor roofline applies (DESIGN.md)"},
             "row": {"kernel": "row (k_row_h; graph heads only)", "ms_per_launch": per_launch("gather"),
                     "launches": kt["gather"][1]},
+            # the product path's post work (streamed step, one persistent cluster per run): the
+            # per-step chain on the critical path after the wide pass's dec half, and the D-step
+            # that runs underneath phase 2 (LTFB_STREAM_PROF stamps, averaged over a run)
+            "post_streamed": {"kernel": "post cluster (k_post_loop, streamed; per step)", "bound": "latency",
+                              "critical_ms_per_step": (stream_profile.get("post_chain_after_dec_us", 0) / 1e3
+                                                       if stream_profile else None),
+                              "overlapped_d_step_ms": (stream_profile.get("d_step_overlapped_us", 0) / 1e3
+                                                       if stream_profile else None)},
         },
         "ae_pretrain": ae,
         "cpu_baseline": cpu,

@@ -14,6 +14,9 @@
 //                    incoming_wins, and (decide mode) adoption: copy the
 //                    incoming fwd/inv blobs and zero their Adam moments,
 //                    keeping t (trainer.hpp:117-127)
+#include <algorithm>
+#include <cstdlib>
+
 #include "kernels.hpp"
 #include "small_mlp.cuh"
 
@@ -54,6 +57,87 @@ __global__ void __launch_bounds__(128) k_eval_small(EvalArgs a) {
     mlp_forward(m.dec_head, a.dec, lat, m.lat, nr, (float* const*)nullptr, pp, sync);
     const float* hh = pp[m.dec_head.L - 1];
     for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = hh[i];
+  } else {
+    for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = lat[i];
+  }
+}
+
+// k_eval_small for C5-size slices: 64 rows per CTA (256 threads), the three
+// small nets' parameters staged into shared memory once per CTA (the 8-row
+// CTAs above re-read them from L1 / L2 for every FMA: 0.57 ms for a 225 k-row
+// slice). Same outputs bit for bit: every output is the same k-ordered fmaf
+// chain + bias + activation (nn/mlp.hpp:201-217), every inverse row sum the
+// same k-ordered double sum.
+constexpr int kER2 = 64;
+
+__device__ __forceinline__ void mlp_forward_sm(const NetDesc& n, const float* w, const float* x, int ldx, int rows,
+                                               float* bufA, float* bufB, int ldbuf) {
+  const float* cur = x;
+  int ldc = ldx;
+  for (int l = 0; l < n.L; ++l) {
+    const int in = n.w[l], out = n.w[l + 1];
+    const float* W = w + (n.off_w[l] - n.base);
+    const float* b = w + (n.off_b[l] - n.base);
+    const int kind = n.act[l];
+    const float slope = n.slope[l];
+    float* dst = (l & 1) ? bufB : bufA;
+    for (int idx = threadIdx.x; idx < rows * out; idx += blockDim.x) {
+      const int r = idx / out, j = idx - r * out;
+      const float* xr = cur + r * ldc;
+      float acc = 0.0f;
+      for (int k = 0; k < in; ++k) acc = fmaf(xr[k], W[k * out + j], acc);
+      dst[r * ldbuf + j] = act_apply(kind, slope, acc + b[j]);
+    }
+    __syncthreads();
+    cur = dst;
+    ldc = ldbuf;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_eval_small_wide(EvalArgs a, int ldbuf) {
+  extern __shared__ float4 sm4[];
+  float* sm = reinterpret_cast<float*>(sm4);
+  const ModelArgs& m = a.m;
+  const int c = blockIdx.y;
+  const int r0 = blockIdx.x * kER2;
+  const int nr = min(kER2, a.rows - r0);
+  if (nr <= 0) return;
+  const NetDesc& F = m.fwd;
+  const NetDesc& I = m.inv;
+  const NetDesc& H = m.dec_head;
+  float* wf = sm;
+  float* wi = wf + F.count;
+  float* wh = wi + I.count;
+  float* bufA = wh + (H.L > 0 ? H.count : 0);
+  float* bufB = bufA + kER2 * ldbuf;
+  float* lat = bufB + kER2 * ldbuf;
+  float* xs = lat + kER2 * m.lat;
+  for (int i = threadIdx.x; i < F.count; i += blockDim.x) wf[i] = a.cf[c][F.base + i];
+  for (int i = threadIdx.x; i < I.count; i += blockDim.x) wi[i] = a.ci[c][I.base + i];
+  if (H.L > 0)
+    for (int i = threadIdx.x; i < H.count; i += blockDim.x) wh[i] = a.dec[H.base + i];
+  for (int i = threadIdx.x; i < nr * m.in; i += blockDim.x) xs[i] = a.x[(long long)r0 * m.in + i];
+  __syncthreads();
+  // latent = fwd(x)
+  mlp_forward_sm(F, wf, xs, m.in, nr, bufA, bufB, ldbuf);
+  const float* latent = ((F.L - 1) & 1) ? bufB : bufA;
+  for (int i = threadIdx.x; i < nr * m.lat; i += blockDim.x) lat[i] = latent[(i / m.lat) * ldbuf + i % m.lat];
+  __syncthreads();
+  // recovered = inv(latent); per-row sum of |recovered - x| in double
+  mlp_forward_sm(I, wi, lat, m.lat, nr, bufA, bufB, ldbuf);
+  const float* recov = ((I.L - 1) & 1) ? bufB : bufA;
+  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < m.in; ++k) acc += fabs((double)recov[r * ldbuf + k] - (double)xs[r * m.in + k]);
+    a.inv_row[(long long)c * a.rows + r0 + r] = acc;
+  }
+  __syncthreads();
+  // h = dec head(latent)
+  float* hdst = a.h + ((long long)c * a.rows + r0) * m.D;
+  if (H.L > 0) {
+    mlp_forward_sm(H, wh, lat, m.lat, nr, bufA, bufB, ldbuf);
+    const float* hh = ((H.L - 1) & 1) ? bufB : bufA;
+    for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = hh[(i / m.D) * ldbuf + i % m.D];
   } else {
     for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = lat[i];
   }
@@ -148,7 +232,19 @@ __global__ void __launch_bounds__(256) k_eval_finalize(EvalArgs a) {
   for (int c = 0; c < a.nc; ++c) {  // fixed-order strided sums + tree: deterministic
     double f = 0.0, inv = 0.0;
     for (int s = threadIdx.x; s < a.S; s += blockDim.x) f += a.part[(long long)s * a.nc + c];
-    for (int r = threadIdx.x; r < a.rows; r += blockDim.x) inv += a.inv_row[(long long)c * a.rows + r];
+    // the same strided order, 16 loads in flight per thread (a C5-size slice
+    // has ~900 rows per thread: one dependent L2 round trip each was 0.4 ms)
+    const double* ir = a.inv_row + (long long)c * a.rows;
+    constexpr int kU = 16;
+    int r = threadIdx.x;
+    for (; r + (kU - 1) * (int)blockDim.x < a.rows; r += kU * (int)blockDim.x) {
+      double v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) v[u] = __ldcg(ir + r + u * (int)blockDim.x);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) inv += v[u];
+    }
+    for (; r < a.rows; r += blockDim.x) inv += ir[r];
     fsum[c] = block_sum_det(f, red);
     isum[c] = block_sum_det(inv, red);
   }
@@ -196,7 +292,18 @@ std::size_t eval_wide_smem(const ModelArgs& m) {
 void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc, bool precise) {
   static PerDevice attr;
   attr.once([] { cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
-  k_eval_small<<<dim3((a.rows + kEvalRows - 1) / kEvalRows, a.nc), 128, 0, s>>>(a);
+  const ModelArgs& m = a.m;
+  const int ldbuf = std::max({m.fwd.max_w(), m.inv.max_w(), m.dec_head.L > 0 ? m.dec_head.max_w() : 0, m.lat, m.in});
+  const std::size_t sm2 = sizeof(float) * (std::size_t)(m.fwd.count + m.inv.count +
+                                                        (m.dec_head.L > 0 ? m.dec_head.count : 0) +
+                                                        2 * kER2 * ldbuf + kER2 * m.lat + kER2 * m.in);
+  if (a.rows >= 64 * kER2 && sm2 <= 200 * 1024 && !std::getenv("LTFB_EVAL_SMALL8")) {  // large slices (C5)
+    static PerDevice attr;
+    attr.once([] { cudaFuncSetAttribute(k_eval_small_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+    k_eval_small_wide<<<dim3((a.rows + kER2 - 1) / kER2, a.nc), 256, sm2, s>>>(a, ldbuf);
+  } else {
+    k_eval_small<<<dim3((a.rows + kEvalRows - 1) / kEvalRows, a.nc), 128, 0, s>>>(a);
+  }
   if (tc)
     launch_eval_tc(a, *tc, precise, s);
   else

@@ -66,10 +66,16 @@ __global__ void __launch_bounds__(et::kThreads, 1)
   // SMs (desk dims: 49) the 128-row blocks of a large slice are dealt over
   // row groups too (block rbg = gr + rb * rgn), so a C5-size tournament
   // slice keeps every SM busy; paper dims: one row group, as before
-  const int cgn = min((int)gridDim.x, ntiles);
+  // A slice with at least one 128-row block per CTA (C5-size slices) is dealt
+  // by rows only: each CTA sweeps every column tile of its row blocks, so the
+  // rows' h (both candidates, 64 KB per block, not L2-resident at that size)
+  // is staged once per block instead of once per column lane (at desk dims
+  // 49 lanes re-read it: ~2x the y bytes); the WdT tiles it re-reads instead
+  // are L2-resident.
+  const int nrb_all = (rows + 127) / 128;
+  const int cgn = nrb_all >= (int)gridDim.x ? 1 : min((int)gridDim.x, ntiles);
   const int rgn = max(1, (int)gridDim.x / max(cgn, 1));
   const int cb = (int)blockIdx.x % max(cgn, 1), gr = (int)blockIdx.x / max(cgn, 1);
-  const int nrb_all = (rows + 127) / 128;
   const bool active = gr < rgn && gr < nrb_all;
   const int my_tiles = active && ntiles > cb ? (ntiles - 1 - cb) / cgn + 1 : 0;
   const int nrb = active ? (nrb_all - gr + rgn - 1) / rgn : 0;  // this CTA's row blocks

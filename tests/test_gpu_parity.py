@@ -984,3 +984,26 @@ def test_trainer_hidden_activations_match_reference(golden, dims_name, act):
     dims = TINY if dims_name == "tiny" else DESK
     t, steps, _ = make_trainer(g, f"{dims_name}_{act}_", dims, arch, g[dims_name + "_data"])
     check_against_golden(g, f"{dims_name}_{act}_", t, steps)
+
+
+@pytest.mark.gpu
+def test_large_slice_eval_kernels_agree(monkeypatch):
+    """C5-size tournament slices take the 64-row, parameter-staging k_eval_small
+    variant and the row-major k_eval_tc mapping (>= one 128-row block per CTA);
+    their metrics must equal the 8-row kernel's bit for bit (same fmaf chains,
+    same double row sums; the forward MAE differs only in its f64 summation
+    order across CTAs), for both candidates of a decision."""
+    rows = 20000
+    n = rows + 512
+    ds = L.SynthDataset(DESK, n, sampling_seed=1, spec_seed=1)
+    m = L.make_cyclegan(DESK, L.SurrogateArch(), 5)
+    m.autoencoder_frozen = True
+    ids = np.arange(n, dtype=np.uint32)
+    t = L.Trainer(L.TrainerConfig(n_shards=1, batch_size=128, seed=3, prefetch_depth=0, train_ids=ids[rows:],
+                                  tournament_ids=ids[:rows]), ds, m)
+    e_new = t.eval_tournament()
+    monkeypatch.setenv("LTFB_EVAL_SMALL8", "1")
+    e_old = t.eval_tournament()
+    assert e_new.inverse_mae == e_old.inverse_mae
+    assert e_new.forward_mae == pytest.approx(e_old.forward_mae, rel=1e-12)
+    assert e_new.combined == pytest.approx(e_old.combined, rel=1e-12)

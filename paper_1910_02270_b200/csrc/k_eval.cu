@@ -62,35 +62,65 @@ __global__ void __launch_bounds__(128) k_eval_small(EvalArgs a) {
   }
 }
 
-// k_eval_small for C5-size slices: 64 rows per CTA (256 threads), the three
-// small nets' parameters staged into shared memory once per CTA (the 8-row
-// CTAs above re-read them from L1 / L2 for every FMA: 0.57 ms for a 225 k-row
-// slice). Same outputs bit for bit: every output is the same k-ordered fmaf
-// chain + bias + activation (nn/mlp.hpp:201-217), every inverse row sum the
-// same k-ordered double sum.
+// k_eval_small for C5-size slices: 64 rows per CTA (8 warps x 8 rows, each
+// warp keeps its rows through every layer: no block barrier between layers),
+// the three small nets' parameters staged into shared memory once per CTA,
+// lanes = output neurons, each lane 8 k-ordered fmaf chains (one per row) fed
+// by one weight load and 8 broadcast row loads (float4 over k where the
+// widths allow) -- the 8-row CTAs above re-read the weights through L1 for
+// every FMA (0.57 ms for a 225 k-row slice). Same outputs bit for bit: every
+// output is the same k-ordered fmaf chain + bias + activation
+// (nn/mlp.hpp:201-217), every inverse row sum the same k-ordered double sum.
 constexpr int kER2 = 64;
 
-__device__ __forceinline__ void mlp_forward_sm(const NetDesc& n, const float* w, const float* x, int ldx, int rows,
-                                               float* bufA, float* bufB, int ldbuf) {
+__device__ __forceinline__ void warp_layer(const float* W, const float* b, int in, int out, int kind, float slope,
+                                           const float* x, int ldx, float* dst, int ldd) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = lane; j < out; j += 32) {
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+    const float* xr = x + warp * ldx;
+    if (((in | ldx) & 3) == 0) {
+      for (int k = 0; k < in; k += 4) {
+        const float w0 = W[k * out + j], w1 = W[(k + 1) * out + j], w2 = W[(k + 2) * out + j],
+                    w3 = W[(k + 3) * out + j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 xv = *reinterpret_cast<const float4*>(xr + 8 * i * ldx + k);
+          acc[i] = fmaf(xv.x, w0, acc[i]);
+          acc[i] = fmaf(xv.y, w1, acc[i]);
+          acc[i] = fmaf(xv.z, w2, acc[i]);
+          acc[i] = fmaf(xv.w, w3, acc[i]);
+        }
+      }
+    } else {
+      for (int k = 0; k < in; ++k) {
+        const float wv = W[k * out + j];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(xr[8 * i * ldx + k], wv, acc[i]);
+      }
+    }
+    const float bj = b[j];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[(warp + 8 * i) * ldd + j] = act_apply(kind, slope, acc[i] + bj);
+  }
+  __syncwarp();
+}
+
+/// Layers of n for the warp's 8 rows; the last layer writes `last` (ld ldl).
+__device__ __forceinline__ void warp_mlp(const NetDesc& n, const float* w, const float* x, int ldx, float* bufA,
+                                         float* bufB, int ldbuf, float* last, int ldl) {
   const float* cur = x;
   int ldc = ldx;
   for (int l = 0; l < n.L; ++l) {
-    const int in = n.w[l], out = n.w[l + 1];
-    const float* W = w + (n.off_w[l] - n.base);
-    const float* b = w + (n.off_b[l] - n.base);
-    const int kind = n.act[l];
-    const float slope = n.slope[l];
-    float* dst = (l & 1) ? bufB : bufA;
-    for (int idx = threadIdx.x; idx < rows * out; idx += blockDim.x) {
-      const int r = idx / out, j = idx - r * out;
-      const float* xr = cur + r * ldc;
-      float acc = 0.0f;
-      for (int k = 0; k < in; ++k) acc = fmaf(xr[k], W[k * out + j], acc);
-      dst[r * ldbuf + j] = act_apply(kind, slope, acc + b[j]);
-    }
-    __syncthreads();
+    const bool top = l + 1 == n.L;
+    float* dst = top ? last : ((l & 1) ? bufB : bufA);
+    const int ldd = top ? ldl : ldbuf;
+    warp_layer(w + (n.off_w[l] - n.base), w + (n.off_b[l] - n.base), n.w[l], n.w[l + 1], n.act[l], n.slope[l],
+               cur, ldc, dst, ldd);
     cur = dst;
-    ldc = ldbuf;
+    ldc = ldd;
   }
 }
 
@@ -102,44 +132,68 @@ __global__ void __launch_bounds__(256) k_eval_small_wide(EvalArgs a, int ldbuf) 
   const int r0 = blockIdx.x * kER2;
   const int nr = min(kER2, a.rows - r0);
   if (nr <= 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const NetDesc& F = m.fwd;
   const NetDesc& I = m.inv;
   const NetDesc& H = m.dec_head;
+  const int ldl = (m.lat + 3) & ~3, ldx = (m.in + 3) & ~3, ldo = (ldbuf + 3) & ~3;
   float* wf = sm;
-  float* wi = wf + F.count;
-  float* wh = wi + I.count;
-  float* bufA = wh + (H.L > 0 ? H.count : 0);
-  float* bufB = bufA + kER2 * ldbuf;
-  float* lat = bufB + kER2 * ldbuf;
-  float* xs = lat + kER2 * m.lat;
-  for (int i = threadIdx.x; i < F.count; i += blockDim.x) wf[i] = a.cf[c][F.base + i];
-  for (int i = threadIdx.x; i < I.count; i += blockDim.x) wi[i] = a.ci[c][I.base + i];
-  if (H.L > 0)
-    for (int i = threadIdx.x; i < H.count; i += blockDim.x) wh[i] = a.dec[H.base + i];
-  for (int i = threadIdx.x; i < nr * m.in; i += blockDim.x) xs[i] = a.x[(long long)r0 * m.in + i];
-  __syncthreads();
-  // latent = fwd(x)
-  mlp_forward_sm(F, wf, xs, m.in, nr, bufA, bufB, ldbuf);
-  const float* latent = ((F.L - 1) & 1) ? bufB : bufA;
-  for (int i = threadIdx.x; i < nr * m.lat; i += blockDim.x) lat[i] = latent[(i / m.lat) * ldbuf + i % m.lat];
-  __syncthreads();
-  // recovered = inv(latent); per-row sum of |recovered - x| in double
-  mlp_forward_sm(I, wi, lat, m.lat, nr, bufA, bufB, ldbuf);
-  const float* recov = ((I.L - 1) & 1) ? bufB : bufA;
-  for (int r = threadIdx.x; r < nr; r += blockDim.x) {
-    double acc = 0.0;
-    for (int k = 0; k < m.in; ++k) acc += fabs((double)recov[r * ldbuf + k] - (double)xs[r * m.in + k]);
-    a.inv_row[(long long)c * a.rows + r0 + r] = acc;
+  float* wi = wf + ((F.count + 3) & ~3);
+  float* wh = wi + ((I.count + 3) & ~3);
+  float* bufA = wh + (H.L > 0 ? ((H.count + 3) & ~3) : 0);
+  float* bufB = bufA + kER2 * ldo;
+  float* lat = bufB + kER2 * ldo;
+  float* xs = lat + kER2 * ldl;
+  float* rec = xs + kER2 * ldx;  // the inverse output [64 x in] (ld ldx)
+  // every load of a chunk in flight before the stores (one L2 round trip per chunk)
+  auto stage = [&](float* dst, const float* src, int n) {
+    constexpr int kU = 8;
+    for (int bb = 0; bb < n; bb += kU * (int)blockDim.x) {
+      float v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = bb + u * (int)blockDim.x + (int)threadIdx.x;
+        v[u] = i < n ? __ldg(src + i) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = bb + u * (int)blockDim.x + (int)threadIdx.x;
+        if (i < n) dst[i] = v[u];
+      }
+    }
+  };
+  stage(wf, a.cf[c] + F.base, (int)F.count);
+  stage(wi, a.ci[c] + I.base, (int)I.count);
+  if (H.L > 0) stage(wh, a.dec + H.base, (int)H.count);
+  for (int i = threadIdx.x; i < kER2 * m.in; i += blockDim.x) {  // x rows (zero past the slice)
+    const int r = i / m.in, k = i - r * m.in;
+    xs[r * ldx + k] = r < nr ? __ldg(a.x + (long long)(r0 + r) * m.in + k) : 0.0f;
   }
   __syncthreads();
-  // h = dec head(latent)
+  // latent = fwd(x), recovered = inv(latent), h = dec head(latent): warp-local rows
+  warp_mlp(F, wf, xs, ldx, bufA, bufB, ldo, lat, ldl);
+  warp_mlp(I, wi, lat, ldl, bufA, bufB, ldo, rec, ldx);
+  if (lane < 8) {  // per-row sum of |recovered - x| in double, k order
+    const int r = warp + 8 * lane;
+    if (r < nr) {
+      double acc = 0.0;
+      for (int k = 0; k < m.in; ++k) acc += fabs((double)rec[r * ldx + k] - (double)xs[r * ldx + k]);
+      a.inv_row[(long long)c * a.rows + r0 + r] = acc;
+    }
+  }
   float* hdst = a.h + ((long long)c * a.rows + r0) * m.D;
+  const float* hh = lat;
+  int ldh = ldl;
   if (H.L > 0) {
-    mlp_forward_sm(H, wh, lat, m.lat, nr, bufA, bufB, ldbuf);
-    const float* hh = ((H.L - 1) & 1) ? bufB : bufA;
-    for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = hh[(i / m.D) * ldbuf + i % m.D];
-  } else {
-    for (int i = threadIdx.x; i < nr * m.D; i += blockDim.x) hdst[i] = lat[i];
+    float* hb = ((H.L - 1) & 1) ? bufB : bufA;  // the buffer the layer rule gives the top layer (never its input)
+    warp_mlp(H, wh, lat, ldl, bufA, bufB, ldo, hb, ldo);
+    hh = hb;
+    ldh = ldo;
+  }
+  for (int i = 0; i < 8; ++i) {
+    const int r = warp + 8 * i;
+    if (r < nr)
+      for (int j = lane; j < m.D; j += 32) hdst[(long long)r * m.D + j] = hh[r * ldh + j];
   }
 }
 
@@ -294,9 +348,11 @@ void launch_eval(const EvalArgs& a, cudaStream_t s, const EvalTcHost* tc, bool p
   attr.once([] { cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   const ModelArgs& m = a.m;
   const int ldbuf = std::max({m.fwd.max_w(), m.inv.max_w(), m.dec_head.L > 0 ? m.dec_head.max_w() : 0, m.lat, m.in});
-  const std::size_t sm2 = sizeof(float) * (std::size_t)(m.fwd.count + m.inv.count +
-                                                        (m.dec_head.L > 0 ? m.dec_head.count : 0) +
-                                                        2 * kER2 * ldbuf + kER2 * m.lat + kER2 * m.in);
+  auto up4 = [](long long v) { return (v + 3) & ~3LL; };
+  const std::size_t sm2 = sizeof(float) * (std::size_t)(up4(m.fwd.count) + up4(m.inv.count) +
+                                                        (m.dec_head.L > 0 ? up4(m.dec_head.count) : 0) +
+                                                        2 * kER2 * up4(ldbuf) + kER2 * up4(m.lat) +
+                                                        2 * kER2 * up4(m.in));
   if (a.rows >= 64 * kER2 && sm2 <= 200 * 1024 && !std::getenv("LTFB_EVAL_SMALL8")) {  // large slices (C5)
     static PerDevice attr;
     attr.once([] { cudaFuncSetAttribute(k_eval_small_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });

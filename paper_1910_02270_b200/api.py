@@ -665,6 +665,15 @@ class Trainer:
             self._dirty = False
         return self._mirror
 
+    def net_hash(self, net: str) -> int:
+        """FNV-1a of one network's parameters (model.hpp:48-58 per net), read
+        from HBM without refreshing the whole host mirror (a round needs only
+        the disc hash; model() would copy every blob and Adam state)."""
+        i = NET_NAMES.index(net)
+        b = np.empty_like(self._mirror.blobs[net])
+        check(lib.ltfb_trainer_get_params(self._h, i, b, b.size))
+        return fnv1a64(b)
+
     def replica_hashes(self) -> list:
         h = self.model().model_hash()
         return [h] * self.cfg.n_shards
@@ -1037,7 +1046,7 @@ def tournament_round(trainers: list, matching: Matching, round_index: int) -> Ro
     records = []
     for to, frm in exchanges:
         t = trainers[to]
-        disc_hash = hex64(t.model().disc_hash())
+        disc_hash = hex64(t.net_hash("disc"))
         loc, inc, adopted = t._decide()
         records.append(TrainerRoundRecord(round_index, step, to, frm, loc.combined, inc.combined,
                                           adopted, disc_hash))

@@ -459,7 +459,8 @@ def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     transfers = [TransferRecord(round_index, me, peer, "fwd", f.nbytes, hex64(fnv1a64(f))),
                  TransferRecord(round_index, me, peer, "inv", iv.nbytes, hex64(fnv1a64(iv)))]
     comm.exchange(trainer, peer)
-    disc_hash = hex64(trainer.model().disc_hash())
+    nh = getattr(trainer, "net_hash", None)  # (a trainer without it: the full model copy)
+    disc_hash = hex64(nh("disc") if nh else trainer.model().disc_hash())
     loc, inc, adopted = trainer._decide()
     rec = TrainerRoundRecord(round_index, step, me, peer, loc.combined, inc.combined, adopted, disc_hash)
     return rr, rec, transfers

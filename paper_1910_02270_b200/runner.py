@@ -25,6 +25,10 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+import sys
+import time
+
 import numpy as np
 
 from .api import (BundleDataset, IoError, write_synth_bundles, CycleGan, Dataset, EvalRecord, HistorySegment, RoundRecord, Trainer, TrainerConfig,
@@ -427,6 +431,9 @@ def warm_peer_links(trainer, comm):
             peer = (2 * r - me) % (n - 1)
         if peer < k and peer != me:
             comm.exchange(trainer, peer)
+    # the round's step-synchronisation all-gather goes through the process
+    # group, whose collectives are also set up lazily (~10 ms on first use)
+    comm.all_gather(None)
     if hasattr(trainer, "synchronize"):
         trainer.synchronize()
 
@@ -437,7 +444,10 @@ def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     swaps generator payloads, and each side evaluates local vs incoming on
     its own tournament slice and adopts on the device if the incoming one
     wins. Returns (RoundRecord, TrainerRoundRecord | None, [TransferRecord])."""
+    _tt = [time.perf_counter()] if os.environ.get("LTFB_ROUND_TIMING") else None
     steps = comm.all_gather(trainer.step())
+    if _tt is not None:
+        _tt.append(time.perf_counter())
     if len(set(steps)) != 1:
         raise ContractError("tournament_round: trainers are not step-synchronized")
     step = steps[0]
@@ -458,10 +468,21 @@ def distributed_round(trainer, comm, k: int, round_index: int, seed: int):
     f, iv = blob[:nf], blob[nf:]
     transfers = [TransferRecord(round_index, me, peer, "fwd", f.nbytes, hex64(fnv1a64(f))),
                  TransferRecord(round_index, me, peer, "inv", iv.nbytes, hex64(fnv1a64(iv)))]
+    if _tt is not None:
+        _tt.append(time.perf_counter())
     comm.exchange(trainer, peer)
+    if _tt is not None:
+        _tt.append(time.perf_counter())
     nh = getattr(trainer, "net_hash", None)  # (a trainer without it: the full model copy)
     disc_hash = hex64(nh("disc") if nh else trainer.model().disc_hash())
+    if _tt is not None:
+        _tt.append(time.perf_counter())
     loc, inc, adopted = trainer._decide()
+    if _tt is not None:  # LTFB_ROUND_TIMING: host wall per phase (dev aid)
+        _tt.append(time.perf_counter())
+        d = [round((b - a) * 1e3, 3) for a, b in zip(_tt, _tt[1:])]
+        print(f"[round {round_index} rank {me}] ms: step all_gather {d[0]}, payload+hashes {d[1]}, "
+              f"exchange {d[2]}, disc hash {d[3]}, decide {d[4]}", file=sys.stderr)
     rec = TrainerRoundRecord(round_index, step, me, peer, loc.combined, inc.combined, adopted, disc_hash)
     return rr, rec, transfers
 
